@@ -1,0 +1,137 @@
+/*
+ * dtwgpu.h -- C-ABI of the B200 DTW distance-matrix fill + k-medoids sweeps.
+ *
+ * This is the drop-in boundary for the reference's hot path (arXiv 2307.04904,
+ * dtwclust). The reference exposes that path only as C++ inline/template
+ * functions in namespace dtwclust; these entry points are what
+ * an FFI/plugin seam for that path binds. Plain pointers and sizes, no exceptions
+ * across the boundary, no torch types. The C++ drop-in with the reference's own
+ * signatures sits on top of this in include/dtwgpu/dtwclust_gpu.hpp.
+ *
+ * Return codes: 0 = OK; 2..14 mirror dtwclust::ErrorCode (errors.hpp:11-25), so a
+ * wrapper rethrows the same exception class; >= 100 = CUDA / internal failure
+ * (message in dtwg_last_error). Threading: one context per host thread; calls on
+ * one context are serialised on its stream.
+ *
+ * Series are passed packed CSR: series i is samples[offsets[i] .. offsets[i+1]),
+ * offsets has p+1 entries. half_width < 0 means WarpWindow::unlimited().
+ * The condensed matrix is the reference's layout (distance_matrix.hpp:20-78):
+ * p(p-1)/2 doubles, row-major upper triangle, slot(i,j) = i*p - i*(i+1)/2 + j-i-1.
+ */
+#ifndef DTWGPU_H_
+#define DTWGPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error codes (errors.hpp:11-25) plus device failures. */
+enum {
+  DTWG_OK = 0,
+  DTWG_INVALID_ARGUMENTS = 2,
+  DTWG_INVALID_SERIES = 5,
+  DTWG_EMPTY_DATASET = 7,
+  DTWG_BAND_INFEASIBLE = 8,
+  DTWG_K_OUT_OF_RANGE = 10,
+  DTWG_DISTANCE_MATRIX_INVALID = 11,
+  DTWG_INDEX_OUT_OF_RANGE = 12,
+  DTWG_CUDA_ERROR = 100,
+  DTWG_NO_DEVICE = 101,
+  DTWG_INTERNAL = 102
+};
+
+/* Arithmetic of the fill. FP64 is bit-exact with the reference (dtw.hpp:59-73). */
+enum { DTWG_FP64 = 0, DTWG_FP32 = 1 };
+
+typedef struct dtwg_ctx dtwg_ctx;
+
+/* Context: owns device buffers, a stream, the resident series and matrix. */
+int dtwg_create(int device, dtwg_ctx** out);
+void dtwg_destroy(dtwg_ctx* ctx);
+const char* dtwg_last_error(const dtwg_ctx* ctx);
+/* Pair reported by the last BandInfeasible error (pairwise.hpp:70-79), else -1,-1. */
+void dtwg_last_error_pair(const dtwg_ctx* ctx, int64_t* i, int64_t* j);
+/* Run on a caller-owned cudaStream_t (e.g. torch.cuda.current_stream()). NULL = own stream. */
+int dtwg_set_stream(dtwg_ctx* ctx, void* cuda_stream);
+int dtwg_synchronize(dtwg_ctx* ctx);
+
+/*
+ * Replaces dtwclust::build_matrix (pairwise.hpp:62-127) end to end, host buffers in
+ * and out: validation in the reference's order (EmptyDataset, workers==0,
+ * InvalidSeries, first infeasible pair when banded without auto_widen), the fill,
+ * and from_condensed's finite/non-negative check (distance_matrix.hpp:27-41).
+ * `workers` is validated (>= 1) and otherwise ignored. out_condensed: p(p-1)/2
+ * doubles (may be NULL when p < 2). evaluations (may be NULL) = p(p-1)/2
+ * (BuildStats, pairwise.hpp:21-23). The filled matrix stays resident on the device
+ * for the k-medoids calls below.
+ */
+int dtwg_build_matrix(dtwg_ctx* ctx, const double* samples, const int64_t* offsets, int64_t p,
+                      int64_t half_width, int auto_widen, unsigned workers, int precision,
+                      double* out_condensed, uint64_t* evaluations);
+
+/*
+ * Lower-level pieces of the same call, for sharded / device-resident use:
+ * upload + validate the series (time_series.hpp:24-45, per-series checks only; id
+ * uniqueness is the caller's), then fill condensed slots [slot_begin, slot_end)
+ * into a DEVICE buffer (slot s written at d_out[s - slot_begin]). d_out == NULL
+ * fills the context's resident matrix (allocated for all p(p-1)/2 slots).
+ * The band-feasibility error is reported for the first infeasible pair of the
+ * whole dataset, as the reference does.
+ */
+int dtwg_upload_series(dtwg_ctx* ctx, const double* samples, const int64_t* offsets, int64_t p);
+int dtwg_fill_slots(dtwg_ctx* ctx, int64_t half_width, int auto_widen, int precision,
+                    int64_t slot_begin, int64_t slot_end, double* d_out);
+/* In-band DP cells of slots [slot_begin, slot_end) (the GCUPS numerator). */
+int dtwg_count_cells(dtwg_ctx* ctx, int64_t half_width, int auto_widen, int64_t slot_begin,
+                     int64_t slot_end, uint64_t* cells);
+/* Device-event time of the last dtwg_fill_slots / dtwg_build_matrix fill, in ms. */
+int dtwg_last_fill_ms(dtwg_ctx* ctx, float* ms);
+/* Number of kernels this context has launched so far (bench `gpu_launches`). */
+uint64_t dtwg_launch_count(const dtwg_ctx* ctx);
+/* Diagnostics/tests: force kernel family (0 = full, 1 = band) and (G, R) for every
+ * pair shape it can legally run; family < 0 restores the cost-model planner. */
+int dtwg_force_kernel(dtwg_ctx* ctx, int family, int G, int R);
+/* Human-readable plan of the last fill (kernel family, group lanes, cells per lane). */
+const char* dtwg_last_plan(const dtwg_ctx* ctx);
+
+/*
+ * Adopt a condensed matrix as the resident k-medoids source (DistanceMatrix::
+ * from_condensed, distance_matrix.hpp:27-41: entries must be finite and >= 0).
+ * on_device != 0: `condensed` is a device pointer (e.g. the all-gathered result).
+ */
+int dtwg_adopt_condensed(dtwg_ctx* ctx, const double* condensed, int64_t p, int on_device);
+/* Copy the resident condensed matrix to host memory (p(p-1)/2 doubles). */
+int dtwg_download_condensed(dtwg_ctx* ctx, double* out_condensed);
+
+typedef void (*dtwg_observer_fn)(void* user, int64_t restart, int64_t iteration, double cost);
+
+/*
+ * Replaces dtwclust::kmedoids (kmedoids.hpp:148-189) over the resident matrix.
+ * Restarts [restart_begin, restart_end) of a run with `restarts` total are executed
+ * (restart_stream(seed, r), rng.hpp:37-41), so restarts can be sharded over GPUs;
+ * pass 0, restarts for the whole run. The best restart (strict <, earliest wins,
+ * kmedoids.hpp:182) is returned: medoids_out[k] ascending, assignment_out[p],
+ * *cost_out, *best_restart_out. Errors: KOutOfRange (k<1 || k>p), InvalidArguments
+ * (restarts < 1 || max_iterations < 1) -- kmedoids.hpp:152-154.
+ */
+int dtwg_kmedoids(dtwg_ctx* ctx, int64_t k, int64_t restarts, int64_t max_iterations,
+                  uint64_t seed, int64_t restart_begin, int64_t restart_end,
+                  dtwg_observer_fn observer, void* user, int64_t* medoids_out,
+                  int64_t* assignment_out, double* cost_out, int64_t* best_restart_out);
+
+/* One sweep's pieces (cluster_result.hpp:40-72; kmedoids.hpp:48-52, 84-139). */
+int dtwg_km_nearest_update(dtwg_ctx* ctx, int64_t current, const uint8_t* chosen,
+                           double* nearest_inout);
+int dtwg_km_assign(dtwg_ctx* ctx, const int64_t* medoids, int64_t k, int64_t* assignment_out,
+                   double* dist_to_assigned_out);
+int dtwg_km_update(dtwg_ctx* ctx, const int64_t* medoids, int64_t k, const int64_t* assignment,
+                   int64_t* updated_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DTWGPU_H_ */

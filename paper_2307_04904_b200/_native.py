@@ -1,0 +1,89 @@
+"""ctypes binding of libdtwgpu.so (include/dtwgpu.h).
+
+The CUDA library is the product: there is no CPU fallback. If the shared object is
+missing or no CUDA device is visible, every entry point raises -- loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from functools import lru_cache
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdtwgpu.so")
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_ip = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_u8 = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+_i64 = C.c_int64
+_vp = C.c_void_p
+OBSERVER = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_int64, C.c_double)
+
+# Every symbol include/dtwgpu.h declares (checked by tests/test_native_abi.py).
+EXPORTS = [
+    "dtwg_create", "dtwg_destroy", "dtwg_last_error", "dtwg_last_error_pair", "dtwg_set_stream",
+    "dtwg_synchronize", "dtwg_build_matrix", "dtwg_upload_series", "dtwg_fill_slots",
+    "dtwg_count_cells", "dtwg_last_fill_ms", "dtwg_launch_count", "dtwg_last_plan",
+    "dtwg_adopt_condensed", "dtwg_download_condensed", "dtwg_kmedoids", "dtwg_km_nearest_update",
+    "dtwg_km_assign", "dtwg_km_update", "dtwg_force_kernel",
+]
+
+
+class NativeMissingError(RuntimeError):
+    pass
+
+
+def build() -> None:
+    import subprocess
+    subprocess.run(["make", "-s", "-j4", "-C", os.path.join(HERE, "csrc")], check=True)
+
+
+@lru_cache(None)
+def lib() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise NativeMissingError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    P = C.POINTER
+    L.dtwg_create.argtypes = [C.c_int, P(_vp)]
+    L.dtwg_create.restype = C.c_int
+    L.dtwg_destroy.argtypes = [_vp]
+    L.dtwg_destroy.restype = None
+    L.dtwg_last_error.argtypes = [_vp]
+    L.dtwg_last_error.restype = C.c_char_p
+    L.dtwg_last_error_pair.argtypes = [_vp, P(_i64), P(_i64)]
+    L.dtwg_last_error_pair.restype = None
+    L.dtwg_set_stream.argtypes = [_vp, _vp]
+    L.dtwg_synchronize.argtypes = [_vp]
+    L.dtwg_build_matrix.argtypes = [_vp, _dp, _ip, _i64, _i64, C.c_int, C.c_uint, C.c_int, _vp,
+                                    P(C.c_uint64)]
+    L.dtwg_upload_series.argtypes = [_vp, _dp, _ip, _i64]
+    L.dtwg_fill_slots.argtypes = [_vp, _i64, C.c_int, C.c_int, _i64, _i64, _vp]
+    L.dtwg_count_cells.argtypes = [_vp, _i64, C.c_int, _i64, _i64, P(C.c_uint64)]
+    L.dtwg_last_fill_ms.argtypes = [_vp, P(C.c_float)]
+    L.dtwg_launch_count.argtypes = [_vp]
+    L.dtwg_launch_count.restype = C.c_uint64
+    L.dtwg_last_plan.argtypes = [_vp]
+    L.dtwg_last_plan.restype = C.c_char_p
+    L.dtwg_adopt_condensed.argtypes = [_vp, _vp, _i64, C.c_int]
+    L.dtwg_download_condensed.argtypes = [_vp, _dp]
+    L.dtwg_kmedoids.argtypes = [_vp, _i64, _i64, _i64, C.c_uint64, _i64, _i64, OBSERVER, _vp,
+                                _ip, _ip, P(C.c_double), P(_i64)]
+    L.dtwg_km_nearest_update.argtypes = [_vp, _i64, _u8, _dp]
+    L.dtwg_km_assign.argtypes = [_vp, _ip, _i64, _ip, _dp]
+    L.dtwg_km_update.argtypes = [_vp, _ip, _i64, _ip, _ip]
+    L.dtwg_force_kernel.argtypes = [_vp, C.c_int, C.c_int, C.c_int]
+    for name in EXPORTS:
+        fn = getattr(L, name)
+        if fn.restype is C.c_int or name in ("dtwg_set_stream", "dtwg_synchronize",
+                                              "dtwg_build_matrix", "dtwg_upload_series",
+                                              "dtwg_fill_slots", "dtwg_count_cells",
+                                              "dtwg_last_fill_ms", "dtwg_adopt_condensed",
+                                              "dtwg_download_condensed", "dtwg_kmedoids",
+                                              "dtwg_km_nearest_update", "dtwg_km_assign",
+                                              "dtwg_km_update", "dtwg_force_kernel"):
+            fn.restype = C.c_int
+    return L

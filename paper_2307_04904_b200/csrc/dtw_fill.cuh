@@ -1,0 +1,62 @@
+// dtw_fill.cuh -- shared declarations of the sm_100a DTW fill kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dtwgpu {
+
+// Work description for one fill launch. Pairs are condensed slots (row-major upper
+// triangle, pairwise.hpp:36-53); either the contiguous range [begin, begin+count) or
+// the explicit slot list list[0..count).
+struct FillArgs {
+  const double* samples;   // packed series, fp64
+  const float* samples32;  // same series rounded to fp32 (precision == fp32 only)
+  const int64_t* offsets;  // p + 1
+  int64_t p;
+  int64_t half_width;      // < 0: unlimited
+  int auto_widen;
+  const int64_t* list;     // nullptr: range mode
+  int64_t begin;
+  int64_t count;
+  int64_t out_base;        // out[slot - out_base]
+  double* out;
+  double* scratch;         // boundary columns for multi-pass fills (one per group)
+  int64_t scratch_stride;  // doubles per group
+};
+
+enum class Family : int { Full = 0, Band = 1 };
+
+// One kernel configuration: family, lanes per pair (G), DP cells per lane per row (R),
+// and whether per-cell band masking may be needed (Full family only).
+struct KernelCfg {
+  Family family;
+  int G;
+  int R;
+  bool mask;
+  bool fp32;
+};
+
+// Launches cfg over args on stream with `blocks` CTAs of kThreads threads.
+cudaError_t launch_fill(const KernelCfg& cfg, const FillArgs& args, int blocks,
+                        cudaStream_t stream);
+// CTAs per SM the configuration can keep resident.
+int fill_blocks_per_sm(const KernelCfg& cfg);
+// Whether (family, G, R, fp32) has a compiled instantiation.
+bool fill_cfg_supported(const KernelCfg& cfg);
+
+constexpr int kThreads = 128;
+
+// ---- k-medoids sweep kernels (kmedoids.cu) -------------------------------------
+cudaError_t launch_expand_square(const double* condensed, int64_t p, double* square,
+                                 cudaStream_t s);
+cudaError_t launch_validate_condensed(const double* condensed, int64_t total, int* bad,
+                                      cudaStream_t s);
+cudaError_t launch_nearest_update(const double* square, int64_t p, int64_t current,
+                                  const uint8_t* chosen, double* nearest, cudaStream_t s);
+cudaError_t launch_assign(const double* square, int64_t p, const int64_t* medoids, int64_t k,
+                          int64_t* assignment, double* dist, cudaStream_t s);
+cudaError_t launch_update(const double* square, int64_t p, const int32_t* members,
+                          const int64_t* cluster_begin, int64_t k, int64_t* best_member,
+                          double* best_sum, cudaStream_t s);
+
+}  // namespace dtwgpu

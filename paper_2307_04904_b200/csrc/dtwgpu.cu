@@ -1,0 +1,1075 @@
+// dtwgpu.cu -- native host side of the C-ABI (include/dtwgpu.h).
+//
+// Mirrors the reference's host logic around the hot path and drives the sm_100a
+// kernels:
+//   * build_matrix's validation order and errors (pairwise.hpp:62-79,
+//     time_series.hpp:24-45, distance_matrix.hpp:27-41);
+//   * the per-pair window (pair_window, pairwise.hpp:29-33) and a cost-model planner
+//     that assigns each pair shape to a kernel family / (G, R) instantiation;
+//   * kmedoids' restart loop, RNG, seeding draws, empty-cluster repair, dedupe and
+//     refill, convergence test and ordered cost sums, line for line with
+//     kmedoids.hpp:33-189 and cluster_result.hpp:40-72, with the O(p k) and
+//     O(sum |C|^2) distance reads on the GPU (kmedoids.cu).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <string>
+#include <tuple>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/dtwgpu.h"
+#include "dtw_fill.cuh"
+
+using dtwgpu::Family;
+using dtwgpu::FillArgs;
+using dtwgpu::KernelCfg;
+
+namespace {
+
+constexpr double kInf = std::numeric_limits<double>::infinity();
+
+template <class T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t cap = 0;  // elements
+  cudaError_t reserve(size_t n) {
+    if (n <= cap && ptr) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&ptr, std::max<size_t>(n, 1) * sizeof(T));
+    if (e == cudaSuccess) cap = std::max<size_t>(n, 1);
+    return e;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+  }
+};
+
+// SplitMix64 / restart_stream, rng.hpp:10-41.
+struct SplitMix64 {
+  uint64_t state;
+  explicit SplitMix64(uint64_t s) : state(s) {}
+  uint64_t next() {
+    uint64_t z = (state += 0x9E3779B97F4A7C15ULL);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+  }
+  double next_double() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+  uint64_t next_below(uint64_t n) {
+    return static_cast<uint64_t>((static_cast<unsigned __int128>(next()) *
+                                  static_cast<unsigned __int128>(n)) >> 64);
+  }
+};
+SplitMix64 restart_stream(uint64_t seed, uint64_t restart) {
+  SplitMix64 mixer(seed);
+  const uint64_t base = mixer.next();
+  return SplitMix64(base + (restart + 1) * 0xD1B54A32D192ED03ULL);
+}
+
+struct Shape {
+  int64_t n, m, hw;  // n >= m; hw effective (unlimited -> n)
+  bool operator<(const Shape& o) const {
+    return std::tie(n, m, hw) < std::tie(o.n, o.m, o.hw);
+  }
+};
+
+struct PlanClass {
+  KernelCfg cfg;
+  std::vector<int64_t> slots;  // empty + range mode when uniform
+  double cost = 0;
+  int64_t max_n = 0;
+};
+
+int64_t row_off(int64_t i, int64_t p) { return i * p - i * (i + 1) / 2; }
+
+// In-band cells of one pair.
+int64_t pair_cells(int64_t n, int64_t m, int64_t hw) {
+  if (hw >= n) return n * m;
+  const int64_t T = std::max<int64_t>(n - hw - 1, 0);
+  const int64_t a = std::min(T, m);
+  const int64_t left = a * (a + 1) / 2 + std::max<int64_t>(T - m, 0) * m;
+  const int64_t S = std::max<int64_t>(m - hw - 1, 0);
+  return n * m - left - S * (S + 1) / 2;
+}
+
+// ---- planner ------------------------------------------------------------------------
+struct Cand {
+  int G, R;
+};
+const Cand kFull[] = {{2, 23}, {4, 12}, {8, 8}, {16, 8}, {16, 16},
+                      {32, 4}, {32, 8}, {32, 12}, {32, 15}, {32, 16}};
+const Cand kBand[] = {{16, 7}, {16, 9}, {16, 11}, {16, 13}, {32, 3},
+                      {32, 5}, {32, 7}, {32, 9},  {32, 13}};
+
+double full_cost(const Shape& s, int G, int R, bool mask) {
+  const int64_t W = (int64_t)G * R;
+  const int64_t npass = (s.m + W - 1) / W;
+  double steps = 0;
+  for (int64_t p = 0; p < npass; ++p) {
+    const int64_t c0 = p * W;
+    int64_t rs = 1, re = s.n;
+    if (mask) {
+      rs = std::max<int64_t>(1, c0 + 1 - s.hw);
+      re = std::min<int64_t>(s.n, c0 + W + s.hw);
+    }
+    steps += double(re - rs + 1 + G - 1);
+  }
+  const double per_pair = G * (4.0 * R + 60.0);
+  return steps * G * (9.0 * R + 12.0 + (mask ? 4.0 : 0.0)) + per_pair;
+}
+
+double band_cost(const Shape& s, int G, int R) {
+  return double(s.n + G - 1) * G * (9.0 * R + 24.0) + G * (4.0 * R + 60.0);
+}
+
+KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out);
+
+// Planner entry: a forced (family, G, R) wins when it can legally run the shape.
+KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cost_out);
+
+KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out) {
+  KernelCfg best{Family::Full, 32, 16, true, fp32};
+  double bc = 1e300;
+  const bool mask = s.hw < s.n - 1;  // a band that excludes some cell
+  for (const Cand& c : kFull) {
+    const double cst = full_cost(s, c.G, c.R, mask);
+    if (cst < bc) {
+      bc = cst;
+      best = KernelCfg{Family::Full, c.G, c.R, mask, fp32};
+    }
+  }
+  if (mask) {
+    const int64_t K = 2 * s.hw + 1;
+    for (const Cand& c : kBand) {
+      if ((int64_t)c.G * c.R < K) continue;
+      const double cst = band_cost(s, c.G, c.R);
+      if (cst < bc) {
+        bc = cst;
+        best = KernelCfg{Family::Band, c.G, c.R, false, fp32};
+      }
+    }
+  }
+  if (cost_out) *cost_out = bc;
+  return best;
+}
+
+const char* family_name(Family f) { return f == Family::Full ? "full" : "band"; }
+
+}  // namespace
+
+struct dtwg_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  float last_fill_ms = 0.f;
+  uint64_t launches = 0;
+  std::string last_error;
+  std::string last_plan;
+  int64_t err_i = -1, err_j = -1;
+  int force_family = -1, force_G = 0, force_R = 0;  // dtwg_force_kernel (tests/diagnostics)
+
+  // series
+  int64_t p = 0;
+  std::vector<int64_t> h_offsets;
+  std::vector<int64_t> h_len;
+  std::vector<double> h_samples;  // kept for fp32 conversion
+  bool uniform = true;
+  DevBuf<double> d_samples;
+  DevBuf<float> d_samples32;
+  bool have32 = false;
+  DevBuf<int64_t> d_offsets;
+  DevBuf<double> d_scratch;
+  DevBuf<int64_t> d_list;
+
+  // resident matrix
+  int64_t mat_p = 0;
+  DevBuf<double> d_cond;
+  bool cond_valid = false;
+  DevBuf<double> d_square;
+  bool square_valid = false;
+  DevBuf<int> d_flag;
+
+  // k-medoids scratch
+  DevBuf<int64_t> d_medoids, d_assign, d_best_member, d_cb;
+  DevBuf<double> d_dist, d_nearest, d_best_sum;
+  DevBuf<uint8_t> d_chosen;
+  DevBuf<int32_t> d_members;
+
+  int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    last_error = buf;
+    return code;
+  }
+  int cuda_fail(cudaError_t e, const char* what) {
+    return fail(DTWG_CUDA_ERROR, "%s: %s", what, cudaGetErrorString(e));
+  }
+};
+
+#define CU(call, what)                                   \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return ctx->cuda_fail(e_, what); \
+  } while (0)
+
+namespace {
+
+KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cost_out) {
+  const bool mask = s.hw < s.n - 1;
+  if (ctx->force_family >= 0) {
+    KernelCfg f{(Family)ctx->force_family, ctx->force_G, ctx->force_R,
+                ctx->force_family == 0 ? mask : false, fp32};
+    const bool ok = dtwgpu::fill_cfg_supported(f) &&
+                    (f.family == Family::Full ||
+                     (mask && f.R >= 2 && (int64_t)f.G * f.R >= 2 * s.hw + 1));
+    if (ok) {
+      if (cost_out) *cost_out = 1.0;
+      return f;
+    }
+  }
+  return choose_cfg_model(s, fp32, cost_out);
+}
+
+// time_series.hpp:24-33 per-series checks (ids are the caller's; see dtwgpu.hpp).
+int validate_series(dtwg_ctx* ctx, const double* samples, const int64_t* offsets, int64_t p) {
+  for (int64_t i = 0; i < p; ++i) {
+    const int64_t b = offsets[i], e = offsets[i + 1];
+    if (e < b) return ctx->fail(DTWG_INVALID_ARGUMENTS, "offsets must be non-decreasing");
+    if (e == b) return ctx->fail(DTWG_INVALID_SERIES, "series #%lld: series is empty", (long long)i);
+    for (int64_t t = b; t < e; ++t) {
+      if (!std::isfinite(samples[t]))
+        return ctx->fail(DTWG_INVALID_SERIES, "series #%lld: series contains a non-finite sample",
+                         (long long)i);
+    }
+  }
+  return DTWG_OK;
+}
+
+// pairwise.hpp:70-79: first infeasible pair in row-major order.
+int check_band(dtwg_ctx* ctx, int64_t hw, int auto_widen) {
+  ctx->err_i = ctx->err_j = -1;
+  if (auto_widen || hw < 0 || ctx->p < 2) return DTWG_OK;
+  const auto mm = std::minmax_element(ctx->h_len.begin(), ctx->h_len.end());
+  if (*mm.second - *mm.first <= hw) return DTWG_OK;  // every gap fits
+  const int64_t p = ctx->p;
+  for (int64_t i = 0; i < p; ++i) {
+    for (int64_t j = i + 1; j < p; ++j) {
+      const int64_t a = ctx->h_len[i], b = ctx->h_len[j];
+      const int64_t gap = a > b ? a - b : b - a;
+      if (gap > hw) {
+        ctx->err_i = i;
+        ctx->err_j = j;
+        return ctx->fail(DTWG_BAND_INFEASIBLE,
+                         "pair (%lld, %lld): half-width %lld is narrower than the length gap of "
+                         "%lld (lengths %lld and %lld)",
+                         (long long)i, (long long)j, (long long)hw, (long long)gap, (long long)a,
+                         (long long)b);
+      }
+    }
+  }
+  return DTWG_OK;
+}
+
+Shape shape_of(const dtwg_ctx* ctx, int64_t a, int64_t b, int64_t hw, int auto_widen) {
+  int64_t la = ctx->h_len[a], lb = ctx->h_len[b];
+  Shape s;
+  s.n = std::max(la, lb);
+  s.m = std::min(la, lb);
+  if (hw < 0) {
+    s.hw = s.n;
+  } else {
+    const int64_t gap = s.n - s.m;
+    s.hw = (auto_widen && gap > hw) ? gap : hw;
+  }
+  if (s.hw > s.n) s.hw = s.n;  // a band at least max(n,m) wide is the unlimited window
+  return s;
+}
+
+std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool fp32,
+                                 int64_t sb, int64_t se) {
+  std::vector<PlanClass> plan;
+  if (se <= sb) return plan;
+  const int64_t p = ctx->p;
+  if (ctx->uniform) {
+    PlanClass pc;
+    const Shape s = shape_of(ctx, 0, 1, hw, auto_widen);
+    pc.cfg = choose_cfg(ctx, s, fp32, &pc.cost);
+    pc.max_n = s.n;
+    plan.push_back(pc);
+    return plan;
+  }
+  std::map<Shape, int> cls_of_shape;
+  std::map<std::tuple<int, int, int, bool>, int> cls_of_cfg;
+  std::vector<std::vector<std::pair<double, int64_t>>> items;
+  int64_t i = 0;
+  // decode sb
+  {
+    int64_t lo = 0, hi = p - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) / 2;
+      if (row_off(mid, p) <= sb) lo = mid;
+      else hi = mid - 1;
+    }
+    i = lo;
+  }
+  int64_t j = i + 1 + (sb - row_off(i, p));
+  for (int64_t slot = sb; slot < se; ++slot) {
+    const Shape s = shape_of(ctx, i, j, hw, auto_widen);
+    auto it = cls_of_shape.find(s);
+    int cls;
+    if (it == cls_of_shape.end()) {
+      double cst = 0;
+      const KernelCfg cfg = choose_cfg(ctx, s, fp32, &cst);
+      const auto key = std::make_tuple((int)cfg.family, cfg.G, cfg.R, cfg.mask);
+      auto ic = cls_of_cfg.find(key);
+      if (ic == cls_of_cfg.end()) {
+        PlanClass pc;
+        pc.cfg = cfg;
+        plan.push_back(pc);
+        items.emplace_back();
+        cls = (int)plan.size() - 1;
+        cls_of_cfg[key] = cls;
+      } else {
+        cls = ic->second;
+      }
+      cls_of_shape[s] = cls;
+    } else {
+      cls = it->second;
+    }
+    const double cst = double(s.n) * double(s.m);
+    items[cls].emplace_back(cst, slot);
+    plan[cls].cost += cst;
+    plan[cls].max_n = std::max(plan[cls].max_n, s.n);
+    if (++j == p) {
+      ++i;
+      j = i + 1;
+    }
+  }
+  for (size_t c = 0; c < plan.size(); ++c) {
+    auto& v = items[c];
+    // Longest pairs first, so the grid-stride schedule ends on short pairs (LPT).
+    std::stable_sort(v.begin(), v.end(),
+                     [](const auto& x, const auto& y) { return x.first > y.first; });
+    plan[c].slots.reserve(v.size());
+    for (const auto& e : v) plan[c].slots.push_back(e.second);
+  }
+  return plan;
+}
+
+int ensure_fp32(dtwg_ctx* ctx) {
+  if (ctx->have32) return DTWG_OK;
+  std::vector<float> f(ctx->h_samples.size());
+  for (size_t t = 0; t < f.size(); ++t) f[t] = static_cast<float>(ctx->h_samples[t]);
+  CU(ctx->d_samples32.reserve(f.size()), "cudaMalloc samples32");
+  CU(cudaMemcpyAsync(ctx->d_samples32.ptr, f.data(), f.size() * sizeof(float),
+                     cudaMemcpyHostToDevice, ctx->stream),
+     "H2D samples32");
+  CU(cudaStreamSynchronize(ctx->stream), "sync");
+  ctx->have32 = true;
+  return DTWG_OK;
+}
+
+int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t sb, int64_t se,
+             double* d_out, int64_t out_base) {
+  const bool fp32 = precision == DTWG_FP32;
+  if (fp32) {
+    const int rc = ensure_fp32(ctx);
+    if (rc) return rc;
+  }
+  std::vector<PlanClass> plan = make_plan(ctx, hw, auto_widen, fp32, sb, se);
+  ctx->last_plan.clear();
+  CU(cudaEventRecord(ctx->ev0, ctx->stream), "event");
+  // Upload all class lists in one buffer.
+  size_t total_list = 0;
+  for (auto& pc : plan) total_list += pc.slots.size();
+  if (total_list) {
+    CU(ctx->d_list.reserve(total_list), "cudaMalloc list");
+    size_t pos = 0;
+    for (auto& pc : plan) {
+      if (!pc.slots.empty())
+        CU(cudaMemcpyAsync(ctx->d_list.ptr + pos, pc.slots.data(), pc.slots.size() * 8,
+                           cudaMemcpyHostToDevice, ctx->stream),
+           "H2D list");
+      pos += pc.slots.size();
+    }
+  }
+  size_t pos = 0;
+  for (auto& pc : plan) {
+    if (!dtwgpu::fill_cfg_supported(pc.cfg))
+      return ctx->fail(DTWG_INTERNAL, "no kernel for %s G=%d R=%d", family_name(pc.cfg.family),
+                       pc.cfg.G, pc.cfg.R);
+    const int64_t count = ctx->uniform ? (se - sb) : (int64_t)pc.slots.size();
+    if (count == 0) continue;
+    const int bps = dtwgpu::fill_blocks_per_sm(pc.cfg);
+    const int64_t groups_per_block = dtwgpu::kThreads / pc.cfg.G;
+    int64_t blocks = (int64_t)ctx->num_sms * bps;
+    blocks = std::min<int64_t>(blocks, (count + groups_per_block - 1) / groups_per_block);
+    blocks = std::max<int64_t>(blocks, 1);
+    FillArgs a{};
+    a.samples = ctx->d_samples.ptr;
+    a.samples32 = fp32 ? ctx->d_samples32.ptr : nullptr;
+    a.offsets = ctx->d_offsets.ptr;
+    a.p = ctx->p;
+    a.half_width = hw;
+    a.auto_widen = auto_widen;
+    a.list = ctx->uniform ? nullptr : ctx->d_list.ptr + pos;
+    a.begin = ctx->uniform ? sb : 0;
+    a.count = count;
+    a.out_base = out_base;
+    a.out = d_out;
+    const int64_t W = (int64_t)pc.cfg.G * pc.cfg.R;
+    const bool multipass = pc.cfg.family == Family::Full &&
+                           (ctx->uniform ? (ctx->h_len[0] > W) : true);
+    if (multipass) {
+      const int64_t stride = pc.max_n + 2;
+      const int64_t groups = blocks * groups_per_block;
+      CU(ctx->d_scratch.reserve((size_t)(stride * groups)), "cudaMalloc scratch");
+      a.scratch = ctx->d_scratch.ptr;
+      a.scratch_stride = stride;
+    }
+    CU(dtwgpu::launch_fill(pc.cfg, a, (int)blocks, ctx->stream), "fill launch");
+    ctx->launches++;
+    char buf[160];
+    snprintf(buf, sizeof(buf), "%s%s[G=%d,R=%d%s%s] pairs=%lld blocks=%lld(%d/SM)",
+             ctx->last_plan.empty() ? "" : "; ", family_name(pc.cfg.family), pc.cfg.G, pc.cfg.R,
+             pc.cfg.mask ? ",mask" : "", fp32 ? ",fp32" : "", (long long)count, (long long)blocks,
+             bps);
+    ctx->last_plan += buf;
+    pos += pc.slots.size();
+  }
+  CU(cudaEventRecord(ctx->ev1, ctx->stream), "event");
+  CU(cudaEventSynchronize(ctx->ev1), "fill sync");
+  CU(cudaEventElapsedTime(&ctx->last_fill_ms, ctx->ev0, ctx->ev1), "elapsed");
+  return DTWG_OK;
+}
+
+int ensure_resident(dtwg_ctx* ctx, int64_t p) {
+  const size_t total = (size_t)(p * (p - 1) / 2);
+  CU(ctx->d_cond.reserve(total), "cudaMalloc condensed");
+  ctx->mat_p = p;
+  ctx->square_valid = false;
+  return DTWG_OK;
+}
+
+int validate_resident(dtwg_ctx* ctx) {
+  const int64_t total = ctx->mat_p * (ctx->mat_p - 1) / 2;
+  if (total == 0) return DTWG_OK;
+  CU(ctx->d_flag.reserve(1), "cudaMalloc flag");
+  CU(cudaMemsetAsync(ctx->d_flag.ptr, 0, sizeof(int), ctx->stream), "memset");
+  CU(dtwgpu::launch_validate_condensed(ctx->d_cond.ptr, total, ctx->d_flag.ptr, ctx->stream),
+     "validate");
+  ctx->launches++;
+  int bad = 0;
+  CU(cudaMemcpyAsync(&bad, ctx->d_flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream),
+     "D2H flag");
+  CU(cudaStreamSynchronize(ctx->stream), "sync");
+  if (bad) {
+    ctx->cond_valid = false;
+    return ctx->fail(DTWG_DISTANCE_MATRIX_INVALID, "entries must be finite and non-negative");
+  }
+  ctx->cond_valid = true;
+  return DTWG_OK;
+}
+
+int ensure_square(dtwg_ctx* ctx) {
+  if (ctx->square_valid) return DTWG_OK;
+  if (!ctx->cond_valid) return ctx->fail(DTWG_INVALID_ARGUMENTS, "no resident distance matrix");
+  const int64_t p = ctx->mat_p;
+  CU(ctx->d_square.reserve((size_t)(p * p)), "cudaMalloc square");
+  if (p >= 2) {
+    CU(dtwgpu::launch_expand_square(ctx->d_cond.ptr, p, ctx->d_square.ptr, ctx->stream),
+       "expand");
+    ctx->launches++;
+  } else {
+    CU(cudaMemsetAsync(ctx->d_square.ptr, 0, sizeof(double), ctx->stream), "memset");
+  }
+  ctx->square_valid = true;
+  return DTWG_OK;
+}
+
+// ---- k-medoids host loop ------------------------------------------------------------
+struct KmState {
+  dtwg_ctx* ctx;
+  int64_t p, k;
+  std::vector<int64_t> assignment;
+  std::vector<double> dist;
+};
+
+int km_assign(KmState& S, const std::vector<int64_t>& medoids) {
+  dtwg_ctx* ctx = S.ctx;
+  CU(cudaMemcpyAsync(ctx->d_medoids.ptr, medoids.data(), medoids.size() * 8,
+                     cudaMemcpyHostToDevice, ctx->stream),
+     "H2D medoids");
+  CU(dtwgpu::launch_assign(ctx->d_square.ptr, S.p, ctx->d_medoids.ptr, (int64_t)medoids.size(),
+                           ctx->d_assign.ptr, ctx->d_dist.ptr, ctx->stream),
+     "assign");
+  ctx->launches++;
+  S.assignment.resize(S.p);
+  S.dist.resize(S.p);
+  CU(cudaMemcpyAsync(S.assignment.data(), ctx->d_assign.ptr, S.p * 8, cudaMemcpyDeviceToHost,
+                     ctx->stream),
+     "D2H assignment");
+  CU(cudaMemcpyAsync(S.dist.data(), ctx->d_dist.ptr, S.p * 8, cudaMemcpyDeviceToHost,
+                     ctx->stream),
+     "D2H dist");
+  CU(cudaStreamSynchronize(ctx->stream), "sync");
+  return DTWG_OK;
+}
+
+// cluster_result.hpp:65-72 -- ascending-j sequential sum on the host.
+double km_cost(const KmState& S) {
+  double total = 0.0;
+  for (int64_t j = 0; j < S.p; ++j) total += S.dist[j];
+  return total;
+}
+
+// kmedoids.hpp:84-139.
+int km_update(KmState& S, const std::vector<int64_t>& medoids, std::vector<int64_t>& updated) {
+  dtwg_ctx* ctx = S.ctx;
+  const int64_t p = S.p, k = (int64_t)medoids.size();
+  // Stable bucket by lower_bound slot (kmedoids.hpp:88-92).
+  std::vector<int64_t> cb(k + 1, 0);
+  std::vector<int64_t> slot_of(p);
+  for (int64_t j = 0; j < p; ++j) {
+    const int64_t c = std::lower_bound(medoids.begin(), medoids.end(), S.assignment[j]) -
+                      medoids.begin();
+    slot_of[j] = c;
+    cb[c + 1]++;
+  }
+  for (int64_t c = 0; c < k; ++c) cb[c + 1] += cb[c];
+  std::vector<int32_t> members(p);
+  {
+    std::vector<int64_t> fill(cb.begin(), cb.end() - 1);
+    for (int64_t j = 0; j < p; ++j) members[fill[slot_of[j]]++] = (int32_t)j;
+  }
+  CU(cudaMemcpyAsync(ctx->d_members.ptr, members.data(), p * 4, cudaMemcpyHostToDevice,
+                     ctx->stream),
+     "H2D members");
+  CU(cudaMemcpyAsync(ctx->d_cb.ptr, cb.data(), (k + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
+     "H2D cb");
+  CU(dtwgpu::launch_update(ctx->d_square.ptr, p, ctx->d_members.ptr, ctx->d_cb.ptr, k,
+                           ctx->d_best_member.ptr, ctx->d_best_sum.ptr, ctx->stream),
+     "update");
+  ctx->launches += 2;
+  std::vector<int64_t> best(k);
+  CU(cudaMemcpyAsync(best.data(), ctx->d_best_member.ptr, k * 8, cudaMemcpyDeviceToHost,
+                     ctx->stream),
+     "D2H best");
+  CU(cudaStreamSynchronize(ctx->stream), "sync");
+
+  updated.assign(k, 0);
+  for (int64_t c = 0; c < k; ++c) {
+    if (cb[c] == cb[c + 1]) {  // kmedoids.hpp:97-109: worst-served non-medoid, strict >
+      int64_t worst = medoids[c];
+      double worst_d = -1.0;
+      for (int64_t j = 0; j < p; ++j) {
+        if (std::find(medoids.begin(), medoids.end(), j) != medoids.end()) continue;
+        const double d = S.dist[j];  // == D(j, assignment[j])
+        if (d > worst_d) {
+          worst_d = d;
+          worst = j;
+        }
+      }
+      updated[c] = worst;
+      continue;
+    }
+    updated[c] = best[c];
+  }
+  std::sort(updated.begin(), updated.end());
+  updated.erase(std::unique(updated.begin(), updated.end()), updated.end());
+  if ((int64_t)updated.size() < k) {  // kmedoids.hpp:127-137
+    std::vector<char> used(p, 0);
+    for (int64_t m : updated) used[m] = 1;
+    for (int64_t j = 0; j < p && (int64_t)updated.size() < k; ++j) {
+      if (!used[j]) {
+        updated.push_back(j);
+        used[j] = 1;
+      }
+    }
+    std::sort(updated.begin(), updated.end());
+  }
+  return DTWG_OK;
+}
+
+// kmedoids.hpp:33-79.
+int km_seeds(KmState& S, int64_t k, SplitMix64& rng, std::vector<int64_t>& medoids) {
+  dtwg_ctx* ctx = S.ctx;
+  const int64_t p = S.p;
+  medoids.clear();
+  std::vector<uint8_t> chosen(p, 0);
+  std::vector<double> nearest(p, kInf);
+  CU(cudaMemsetAsync(ctx->d_chosen.ptr, 0, p, ctx->stream), "memset chosen");
+  CU(cudaMemcpyAsync(ctx->d_nearest.ptr, nearest.data(), p * 8, cudaMemcpyHostToDevice,
+                     ctx->stream),
+     "H2D nearest");
+  int64_t current = (int64_t)rng.next_below((uint64_t)p);
+  while ((int64_t)medoids.size() < k) {
+    medoids.push_back(current);
+    chosen[current] = 1;
+    if ((int64_t)medoids.size() == k) break;
+    CU(cudaMemcpyAsync(ctx->d_chosen.ptr + current, &chosen[current], 1, cudaMemcpyHostToDevice,
+                       ctx->stream),
+       "H2D chosen");
+    CU(dtwgpu::launch_nearest_update(ctx->d_square.ptr, p, current, ctx->d_chosen.ptr,
+                                     ctx->d_nearest.ptr, ctx->stream),
+       "nearest");
+    ctx->launches++;
+    CU(cudaMemcpyAsync(nearest.data(), ctx->d_nearest.ptr, p * 8, cudaMemcpyDeviceToHost,
+                       ctx->stream),
+       "D2H nearest");
+    CU(cudaStreamSynchronize(ctx->stream), "sync");
+    double total = 0.0;
+    for (int64_t j = 0; j < p; ++j) {
+      if (chosen[j]) continue;
+      total += nearest[j];
+    }
+    int64_t next = p;
+    if (total > 0.0) {
+      const double target = rng.next_double() * total;
+      double acc = 0.0;
+      for (int64_t j = 0; j < p; ++j) {
+        if (chosen[j]) continue;
+        acc += nearest[j];
+        if (acc > target) {
+          next = j;
+          break;
+        }
+      }
+    }
+    if (next == p) {
+      for (int64_t j = 0; j < p; ++j) {
+        if (!chosen[j]) {
+          next = j;
+          break;
+        }
+      }
+    }
+    current = next;
+  }
+  std::sort(medoids.begin(), medoids.end());
+  return DTWG_OK;
+}
+
+int km_reserve(dtwg_ctx* ctx, int64_t p, int64_t k) {
+  CU(ctx->d_medoids.reserve(k), "malloc");
+  CU(ctx->d_assign.reserve(p), "malloc");
+  CU(ctx->d_dist.reserve(p), "malloc");
+  CU(ctx->d_nearest.reserve(p), "malloc");
+  CU(ctx->d_chosen.reserve(p), "malloc");
+  CU(ctx->d_members.reserve(p), "malloc");
+  CU(ctx->d_cb.reserve(k + 1), "malloc");
+  CU(ctx->d_best_member.reserve(k), "malloc");
+  CU(ctx->d_best_sum.reserve(k + p), "malloc");
+  return DTWG_OK;
+}
+
+}  // namespace
+
+// =====================================================================================
+// C-ABI
+// =====================================================================================
+extern "C" {
+
+int dtwg_create(int device, dtwg_ctx** out) {
+  if (!out) return DTWG_INVALID_ARGUMENTS;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0 || device < 0 || device >= n) {
+    cudaGetLastError();
+    return DTWG_NO_DEVICE;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) return DTWG_NO_DEVICE;
+  auto* ctx = new dtwg_ctx();
+  ctx->device = device;
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) {
+    delete ctx;
+    return DTWG_CUDA_ERROR;
+  }
+  ctx->own_stream = true;
+  *out = ctx;
+  return DTWG_OK;
+}
+
+void dtwg_destroy(dtwg_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  ctx->d_samples.release();
+  ctx->d_samples32.release();
+  ctx->d_offsets.release();
+  ctx->d_scratch.release();
+  ctx->d_list.release();
+  ctx->d_cond.release();
+  ctx->d_square.release();
+  ctx->d_flag.release();
+  ctx->d_medoids.release();
+  ctx->d_assign.release();
+  ctx->d_best_member.release();
+  ctx->d_cb.release();
+  ctx->d_dist.release();
+  ctx->d_nearest.release();
+  ctx->d_best_sum.release();
+  ctx->d_chosen.release();
+  ctx->d_members.release();
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* dtwg_last_error(const dtwg_ctx* ctx) { return ctx ? ctx->last_error.c_str() : ""; }
+
+void dtwg_last_error_pair(const dtwg_ctx* ctx, int64_t* i, int64_t* j) {
+  if (i) *i = ctx ? ctx->err_i : -1;
+  if (j) *j = ctx ? ctx->err_j : -1;
+}
+
+int dtwg_set_stream(dtwg_ctx* ctx, void* stream) {
+  if (!ctx) return DTWG_INVALID_ARGUMENTS;
+  cudaSetDevice(ctx->device);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (stream) {
+    ctx->stream = (cudaStream_t)stream;
+    ctx->own_stream = false;
+  } else {
+    CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+    ctx->own_stream = true;
+  }
+  return DTWG_OK;
+}
+
+int dtwg_synchronize(dtwg_ctx* ctx) {
+  if (!ctx) return DTWG_INVALID_ARGUMENTS;
+  CU(cudaStreamSynchronize(ctx->stream), "sync");
+  return DTWG_OK;
+}
+
+int dtwg_upload_series(dtwg_ctx* ctx, const double* samples, const int64_t* offsets, int64_t p) {
+  if (!ctx) return DTWG_INVALID_ARGUMENTS;
+  cudaSetDevice(ctx->device);
+  if (p <= 0) return ctx->fail(DTWG_EMPTY_DATASET, "dataset contains no series");
+  if (!offsets || (offsets[p] > 0 && !samples))
+    return ctx->fail(DTWG_INVALID_ARGUMENTS, "null series buffers");
+  int rc = validate_series(ctx, samples, offsets, p);
+  if (rc) return rc;
+  ctx->p = p;
+  ctx->h_offsets.assign(offsets, offsets + p + 1);
+  const int64_t base = offsets[0];
+  for (auto& o : ctx->h_offsets) o -= base;
+  ctx->h_len.resize(p);
+  ctx->uniform = true;
+  for (int64_t i = 0; i < p; ++i) {
+    ctx->h_len[i] = offsets[i + 1] - offsets[i];
+    if (ctx->h_len[i] != ctx->h_len[0]) ctx->uniform = false;
+  }
+  const int64_t n = ctx->h_offsets[p];
+  ctx->h_samples.assign(samples + base, samples + base + n);
+  ctx->have32 = false;
+  CU(ctx->d_samples.reserve(n), "cudaMalloc samples");
+  CU(ctx->d_offsets.reserve(p + 1), "cudaMalloc offsets");
+  CU(cudaMemcpyAsync(ctx->d_samples.ptr, ctx->h_samples.data(), n * sizeof(double),
+                     cudaMemcpyHostToDevice, ctx->stream),
+     "H2D samples");
+  CU(cudaMemcpyAsync(ctx->d_offsets.ptr, ctx->h_offsets.data(), (p + 1) * sizeof(int64_t),
+                     cudaMemcpyHostToDevice, ctx->stream),
+     "H2D offsets");
+  CU(cudaStreamSynchronize(ctx->stream), "sync");
+  return DTWG_OK;
+}
+
+int dtwg_fill_slots(dtwg_ctx* ctx, int64_t half_width, int auto_widen, int precision,
+                    int64_t slot_begin, int64_t slot_end, double* d_out) {
+  if (!ctx) return DTWG_INVALID_ARGUMENTS;
+  cudaSetDevice(ctx->device);
+  if (ctx->p <= 0) return ctx->fail(DTWG_EMPTY_DATASET, "dataset contains no series");
+  if (precision != DTWG_FP64 && precision != DTWG_FP32)
+    return ctx->fail(DTWG_INVALID_ARGUMENTS, "precision must be 0 (fp64) or 1 (fp32)");
+  const int64_t total = ctx->p * (ctx->p - 1) / 2;
+  if (slot_begin < 0 || slot_end > total || slot_begin > slot_end)
+    return ctx->fail(DTWG_INVALID_ARGUMENTS, "slot range [%lld, %lld) outside [0, %lld)",
+                     (long long)slot_begin, (long long)slot_end, (long long)total);
+  int rc = check_band(ctx, half_width, auto_widen);
+  if (rc) return rc;
+  int64_t out_base = slot_begin;
+  if (!d_out) {
+    rc = ensure_resident(ctx, ctx->p);
+    if (rc) return rc;
+    d_out = ctx->d_cond.ptr;
+    out_base = 0;
+    ctx->cond_valid = false;
+  }
+  rc = run_fill(ctx, half_width, auto_widen, precision, slot_begin, slot_end, d_out, out_base);
+  if (rc) return rc;
+  if (d_out == ctx->d_cond.ptr && slot_begin == 0 && slot_end == total) ctx->cond_valid = true;
+  return DTWG_OK;
+}
+
+int dtwg_count_cells(dtwg_ctx* ctx, int64_t half_width, int auto_widen, int64_t sb, int64_t se,
+                     uint64_t* cells) {
+  if (!ctx || !cells) return DTWG_INVALID_ARGUMENTS;
+  const int64_t p = ctx->p;
+  uint64_t total = 0;
+  if (se > sb && p >= 2) {
+    if (ctx->uniform) {
+      const Shape s = shape_of(ctx, 0, 1, half_width, auto_widen);
+      total = (uint64_t)pair_cells(s.n, s.m, s.hw) * (uint64_t)(se - sb);
+    } else {
+      int64_t lo = 0, hi = p - 1;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) / 2;
+        if (row_off(mid, p) <= sb) lo = mid;
+        else hi = mid - 1;
+      }
+      int64_t i = lo, j = lo + 1 + (sb - row_off(lo, p));
+      for (int64_t s = sb; s < se; ++s) {
+        const Shape sh = shape_of(ctx, i, j, half_width, auto_widen);
+        total += (uint64_t)pair_cells(sh.n, sh.m, sh.hw);
+        if (++j == p) {
+          ++i;
+          j = i + 1;
+        }
+      }
+    }
+  }
+  *cells = total;
+  return DTWG_OK;
+}
+
+int dtwg_last_fill_ms(dtwg_ctx* ctx, float* ms) {
+  if (!ctx || !ms) return DTWG_INVALID_ARGUMENTS;
+  *ms = ctx->last_fill_ms;
+  return DTWG_OK;
+}
+
+int dtwg_force_kernel(dtwg_ctx* ctx, int family, int G, int R) {
+  if (!ctx) return DTWG_INVALID_ARGUMENTS;
+  ctx->force_family = family;
+  ctx->force_G = G;
+  ctx->force_R = R;
+  return DTWG_OK;
+}
+
+uint64_t dtwg_launch_count(const dtwg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+const char* dtwg_last_plan(const dtwg_ctx* ctx) { return ctx ? ctx->last_plan.c_str() : ""; }
+
+int dtwg_build_matrix(dtwg_ctx* ctx, const double* samples, const int64_t* offsets, int64_t p,
+                      int64_t half_width, int auto_widen, unsigned workers, int precision,
+                      double* out_condensed, uint64_t* evaluations) {
+  if (!ctx) return DTWG_INVALID_ARGUMENTS;
+  cudaSetDevice(ctx->device);
+  ctx->err_i = ctx->err_j = -1;
+  // pairwise.hpp:65-67: EmptyDataset, then workers, then series validation.
+  if (p <= 0) return ctx->fail(DTWG_EMPTY_DATASET, "dataset contains no series");
+  if (workers == 0) return ctx->fail(DTWG_INVALID_ARGUMENTS, "workers must be >= 1");
+  int rc = dtwg_upload_series(ctx, samples, offsets, p);
+  if (rc) return rc;
+  const int64_t total = p * (p - 1) / 2;
+  rc = dtwg_fill_slots(ctx, half_width, auto_widen, precision, 0, total, nullptr);
+  if (rc) return rc;
+  if (total == 0) {
+    ensure_resident(ctx, p);
+    ctx->cond_valid = true;
+  }
+  rc = validate_resident(ctx);  // distance_matrix.hpp:34-38
+  if (rc) return rc;
+  if (total > 0 && out_condensed) {
+    CU(cudaMemcpyAsync(out_condensed, ctx->d_cond.ptr, total * sizeof(double),
+                       cudaMemcpyDeviceToHost, ctx->stream),
+       "D2H condensed");
+    CU(cudaStreamSynchronize(ctx->stream), "sync");
+  }
+  if (evaluations) *evaluations = (uint64_t)total;
+  return DTWG_OK;
+}
+
+int dtwg_adopt_condensed(dtwg_ctx* ctx, const double* condensed, int64_t p, int on_device) {
+  if (!ctx) return DTWG_INVALID_ARGUMENTS;
+  cudaSetDevice(ctx->device);
+  if (p <= 0) return ctx->fail(DTWG_DISTANCE_MATRIX_INVALID, "matrix needs at least one series");
+  int rc = ensure_resident(ctx, p);
+  if (rc) return rc;
+  const int64_t total = p * (p - 1) / 2;
+  if (total > 0) {
+    if (!condensed) return ctx->fail(DTWG_INVALID_ARGUMENTS, "null condensed buffer");
+    CU(cudaMemcpyAsync(ctx->d_cond.ptr, condensed, total * sizeof(double),
+                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       ctx->stream),
+       "copy condensed");
+  }
+  return validate_resident(ctx);
+}
+
+int dtwg_download_condensed(dtwg_ctx* ctx, double* out) {
+  if (!ctx || !out) return DTWG_INVALID_ARGUMENTS;
+  if (!ctx->cond_valid) return ctx->fail(DTWG_INVALID_ARGUMENTS, "no resident distance matrix");
+  const int64_t total = ctx->mat_p * (ctx->mat_p - 1) / 2;
+  if (total > 0) {
+    CU(cudaMemcpyAsync(out, ctx->d_cond.ptr, total * 8, cudaMemcpyDeviceToHost, ctx->stream),
+       "D2H");
+    CU(cudaStreamSynchronize(ctx->stream), "sync");
+  }
+  return DTWG_OK;
+}
+
+int dtwg_kmedoids(dtwg_ctx* ctx, int64_t k, int64_t restarts, int64_t max_iterations,
+                  uint64_t seed, int64_t restart_begin, int64_t restart_end,
+                  dtwg_observer_fn observer, void* user, int64_t* medoids_out,
+                  int64_t* assignment_out, double* cost_out, int64_t* best_restart_out) {
+  if (!ctx) return DTWG_INVALID_ARGUMENTS;
+  cudaSetDevice(ctx->device);
+  if (!ctx->cond_valid) return ctx->fail(DTWG_INVALID_ARGUMENTS, "no resident distance matrix");
+  const int64_t p = ctx->mat_p;
+  // kmedoids.hpp:152-154
+  if (k < 1 || k > p)
+    return ctx->fail(DTWG_K_OUT_OF_RANGE, "k=%lld is outside [1, p] with p=%lld", (long long)k,
+                     (long long)p);
+  if (restarts < 1) return ctx->fail(DTWG_INVALID_ARGUMENTS, "restarts must be >= 1");
+  if (max_iterations < 1) return ctx->fail(DTWG_INVALID_ARGUMENTS, "max_iterations must be >= 1");
+  if (restart_end > restarts) restart_end = restarts;
+  if (restart_begin < 0 || restart_begin >= restart_end)
+    return ctx->fail(DTWG_INVALID_ARGUMENTS, "empty restart range");
+  int rc = ensure_square(ctx);
+  if (rc) return rc;
+  rc = km_reserve(ctx, p, k);
+  if (rc) return rc;
+
+  KmState S{ctx, p, k, {}, {}};
+  bool have_best = false;
+  double best_cost = 0.0;
+  std::vector<int64_t> medoids, updated;
+  for (int64_t r = restart_begin; r < restart_end; ++r) {  // kmedoids.hpp:158-187
+    SplitMix64 rng = restart_stream(seed, (uint64_t)r);
+    rc = km_seeds(S, k, rng, medoids);
+    if (rc) return rc;
+    double cost = 0.0;
+    bool converged = false;
+    for (int64_t it = 0; it < max_iterations && !converged; ++it) {
+      rc = km_assign(S, medoids);
+      if (rc) return rc;
+      cost = km_cost(S);
+      if (observer) observer(user, r, it, cost);
+      rc = km_update(S, medoids, updated);
+      if (rc) return rc;
+      if (updated == medoids) converged = true;
+      else medoids = updated;
+    }
+    if (!converged) {
+      rc = km_assign(S, medoids);
+      if (rc) return rc;
+      cost = km_cost(S);
+    }
+    if (!have_best || cost < best_cost) {
+      best_cost = cost;
+      have_best = true;
+      if (medoids_out) std::copy(medoids.begin(), medoids.end(), medoids_out);
+      if (assignment_out) std::copy(S.assignment.begin(), S.assignment.end(), assignment_out);
+      if (best_restart_out) *best_restart_out = r;
+    }
+  }
+  if (cost_out) *cost_out = best_cost;
+  return DTWG_OK;
+}
+
+int dtwg_km_nearest_update(dtwg_ctx* ctx, int64_t current, const uint8_t* chosen,
+                           double* nearest_inout) {
+  if (!ctx || !chosen || !nearest_inout) return DTWG_INVALID_ARGUMENTS;
+  cudaSetDevice(ctx->device);
+  int rc = ensure_square(ctx);
+  if (rc) return rc;
+  const int64_t p = ctx->mat_p;
+  if (current < 0 || current >= p)
+    return ctx->fail(DTWG_INDEX_OUT_OF_RANGE, "index %lld is outside [0, %lld)",
+                     (long long)current, (long long)p);
+  rc = km_reserve(ctx, p, 1);
+  if (rc) return rc;
+  CU(cudaMemcpyAsync(ctx->d_chosen.ptr, chosen, p, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  CU(cudaMemcpyAsync(ctx->d_nearest.ptr, nearest_inout, p * 8, cudaMemcpyHostToDevice,
+                     ctx->stream),
+     "H2D");
+  CU(dtwgpu::launch_nearest_update(ctx->d_square.ptr, p, current, ctx->d_chosen.ptr,
+                                   ctx->d_nearest.ptr, ctx->stream),
+     "nearest");
+  ctx->launches++;
+  CU(cudaMemcpyAsync(nearest_inout, ctx->d_nearest.ptr, p * 8, cudaMemcpyDeviceToHost,
+                     ctx->stream),
+     "D2H");
+  CU(cudaStreamSynchronize(ctx->stream), "sync");
+  return DTWG_OK;
+}
+
+int dtwg_km_assign(dtwg_ctx* ctx, const int64_t* medoids, int64_t k, int64_t* assignment_out,
+                   double* dist_out) {
+  if (!ctx || !medoids) return DTWG_INVALID_ARGUMENTS;
+  cudaSetDevice(ctx->device);
+  int rc = ensure_square(ctx);
+  if (rc) return rc;
+  const int64_t p = ctx->mat_p;
+  if (k < 1 || k > p) return ctx->fail(DTWG_K_OUT_OF_RANGE, "k=%lld is outside [1, p]", (long long)k);
+  rc = km_reserve(ctx, p, k);
+  if (rc) return rc;
+  KmState S{ctx, p, k, {}, {}};
+  std::vector<int64_t> med(medoids, medoids + k);
+  rc = km_assign(S, med);
+  if (rc) return rc;
+  if (assignment_out) std::copy(S.assignment.begin(), S.assignment.end(), assignment_out);
+  if (dist_out) std::copy(S.dist.begin(), S.dist.end(), dist_out);
+  return DTWG_OK;
+}
+
+int dtwg_km_update(dtwg_ctx* ctx, const int64_t* medoids, int64_t k, const int64_t* assignment,
+                   int64_t* updated_out) {
+  if (!ctx || !medoids || !assignment || !updated_out) return DTWG_INVALID_ARGUMENTS;
+  cudaSetDevice(ctx->device);
+  int rc = ensure_square(ctx);
+  if (rc) return rc;
+  const int64_t p = ctx->mat_p;
+  if (k < 1 || k > p) return ctx->fail(DTWG_K_OUT_OF_RANGE, "k=%lld is outside [1, p]", (long long)k);
+  rc = km_reserve(ctx, p, k);
+  if (rc) return rc;
+  KmState S{ctx, p, k, {}, {}};
+  std::vector<int64_t> med(medoids, medoids + k);
+  // Needs D(j, assignment[j]) for the empty-cluster repair: one assign-side gather.
+  S.assignment.assign(assignment, assignment + p);
+  S.dist.resize(p);
+  {
+    // dist[j] = D(j, assignment[j]) from the dense matrix rows.
+    std::vector<double> row(p);
+    for (int64_t j = 0; j < p; ++j) {
+      const int64_t a = assignment[j];
+      if (a < 0 || a >= p) return ctx->fail(DTWG_INDEX_OUT_OF_RANGE, "assignment out of range");
+      if (a == j) {
+        S.dist[j] = 0.0;
+        continue;
+      }
+      CU(cudaMemcpy(&S.dist[j], ctx->d_square.ptr + a * p + j, 8, cudaMemcpyDeviceToHost),
+         "D2H entry");
+    }
+  }
+  std::vector<int64_t> upd;
+  rc = km_update(S, med, upd);
+  if (rc) return rc;
+  std::copy(upd.begin(), upd.end(), updated_out);
+  return DTWG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,230 @@
+// kmedoids.cu -- sm_100a sweep kernels over the device-resident distance matrix.
+//
+// They replace the O(p*k) and O(sum |C|^2) distance reads of the reference's
+// k-medoids: the nearest-distance refresh of spread seeding
+// (kmedoids.hpp:48-52), nearest-medoid assignment (cluster_result.hpp:40-61) and the
+// per-candidate member sums of the medoid update (kmedoids.hpp:111-121). Every
+// floating-point reduction keeps the reference's order: per-candidate sums are one
+// thread's ascending-member sequential loop (never a tree), comparisons are strict
+// with the lowest index winning. Sequential scalar sums over p (assignment_cost,
+// seeding weights) stay on the host, exactly as written in the reference.
+//
+// The matrix is expanded once from condensed to a dense p x p square so every sweep
+// reads contiguous rows (D is symmetric and D[i][j], D[j][i] are the same stored
+// double, so reading the transposed entry is bit-identical).
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+
+#include "dtw_fill.cuh"
+
+namespace dtwgpu {
+namespace {
+
+__device__ __forceinline__ int64_t coff(int64_t i, int64_t p) { return i * p - i * (i + 1) / 2; }
+
+// Dense square from condensed: 32x32 tiles; lower tiles read their transposed upper
+// tile coalesced through shared memory.
+__global__ void expand_square_kernel(const double* __restrict__ cond, int64_t p,
+                                     double* __restrict__ sq) {
+  __shared__ double tile[32][33];
+  const int64_t bi = (int64_t)blockIdx.y * 32, bj = (int64_t)blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  if (bi <= bj) {
+    for (int r = ty; r < 32; r += 8) {
+      const int64_t i = bi + r, j = bj + tx;
+      if (i < p && j < p) {
+        double v;
+        if (i == j) v = 0.0;
+        else if (i < j) v = cond[coff(i, p) + (j - i - 1)];
+        else v = cond[coff(j, p) + (i - j - 1)];
+        sq[i * p + j] = v;
+      }
+    }
+  } else {
+    // tile (bi, bj) below the diagonal = transpose of upper tile (bj, bi)
+    for (int r = ty; r < 32; r += 8) {
+      const int64_t i = bj + r, j = bi + tx;  // upper element (i < j)
+      if (i < p && j < p) tile[r][tx] = cond[coff(i, p) + (j - i - 1)];
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+      const int64_t i = bi + r, j = bj + tx;
+      if (i < p && j < p) sq[i * p + j] = tile[tx][r];
+    }
+  }
+}
+
+// DistanceMatrix::from_condensed validation (distance_matrix.hpp:34-38).
+__global__ void validate_kernel(const double* __restrict__ cond, int64_t total, int* bad) {
+  int local = 0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const double v = cond[t];
+    if (!(isfinite(v) && v >= 0.0)) local = 1;
+  }
+  if (__any_sync(0xffffffffu, local) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+}
+
+// kmedoids.hpp:48-52: nearest[j] = std::min(nearest[j], D(j, current)) for unchosen j.
+__global__ void nearest_update_kernel(const double* __restrict__ sq, int64_t p, int64_t current,
+                                      const uint8_t* __restrict__ chosen,
+                                      double* __restrict__ nearest) {
+  const double* row = sq + current * p;  // D(current, j) == D(j, current)
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    if (chosen[j]) continue;
+    const double a = nearest[j], b = row[j];
+    nearest[j] = b < a ? b : a;
+  }
+}
+
+// cluster_result.hpp:40-61. Medoids ascending; a medoid owns itself; otherwise the
+// strictly smaller distance wins, so ties keep the lowest medoid index. Row reads
+// D(medoid_t, j) are coalesced across j.
+__global__ void assign_kernel(const double* __restrict__ sq, int64_t p,
+                              const int64_t* __restrict__ medoids, int64_t k,
+                              int64_t* __restrict__ assignment, double* __restrict__ dist) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    bool is_med = false;
+    for (int64_t t = 0; t < k; ++t) is_med |= (__ldg(medoids + t) == j);
+    if (is_med) {
+      assignment[j] = j;
+      dist[j] = 0.0;
+      continue;
+    }
+    int64_t best = __ldg(medoids);
+    double bd = sq[best * p + j];
+    for (int64_t t = 1; t < k; ++t) {
+      const int64_t mt = __ldg(medoids + t);
+      const double d = sq[mt * p + j];
+      if (d < bd) {
+        bd = d;
+        best = mt;
+      }
+    }
+    assignment[j] = best;
+    dist[j] = bd;
+  }
+}
+
+// kmedoids.hpp:113-120: one thread per candidate; sequential ascending-member sum.
+// members: all clusters concatenated, each ascending; cluster c = [cb[c], cb[c+1]).
+__global__ void candidate_sum_kernel(const double* __restrict__ sq, int64_t p,
+                                     const int32_t* __restrict__ members,
+                                     const int64_t* __restrict__ cb, int64_t k,
+                                     double* __restrict__ sums) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < p;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = k - 1;  // cluster c with cb[c] <= q < cb[c+1]
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) / 2;
+      if (__ldg(cb + mid) <= q) lo = mid;
+      else hi = mid - 1;
+    }
+    const int64_t b = __ldg(cb + lo), e = __ldg(cb + lo + 1);
+    const int64_t a = members[q];
+    double sum = 0.0;
+    int64_t t = b;
+    for (; t + 8 <= e; t += 8) {  // loads batched, additions kept in order
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = sq[(int64_t)__ldg(members + t + u) * p + a];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sum = __dadd_rn(sum, v[u]);
+    }
+    for (; t < e; ++t) sum = __dadd_rn(sum, sq[(int64_t)__ldg(members + t) * p + a]);
+    sums[q] = sum;
+  }
+}
+
+// kmedoids.hpp:111-121 selection: first candidate (ascending) with the smallest sum,
+// i.e. lexicographic (sum, position) minimum -- exact in any reduction order.
+__global__ void cluster_argmin_kernel(const int32_t* __restrict__ members,
+                                      const int64_t* __restrict__ cb,
+                                      const double* __restrict__ sums, int64_t* best_member,
+                                      double* best_sum) {
+  const int64_t c = blockIdx.x;
+  const int64_t b = cb[c], e = cb[c + 1];
+  double bv = CUDART_INF;
+  int64_t bq = -1;
+  for (int64_t q = b + threadIdx.x; q < e; q += blockDim.x) {
+    const double v = sums[q];
+    if (bq < 0 || v < bv) {  // q ascending per thread: strict < keeps the first minimum
+      bv = v;
+      bq = q;
+    }
+  }
+  __shared__ double sv[256];
+  __shared__ int64_t sq_[256];
+  sv[threadIdx.x] = bv;
+  sq_[threadIdx.x] = bq;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      const double ov = sv[threadIdx.x + w];
+      const int64_t oq = sq_[threadIdx.x + w];
+      const int64_t mq = sq_[threadIdx.x];
+      if (oq >= 0 && (mq < 0 || ov < sv[threadIdx.x] || (ov == sv[threadIdx.x] && oq < mq))) {
+        sv[threadIdx.x] = ov;
+        sq_[threadIdx.x] = oq;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    best_member[c] = sq_[0] >= 0 ? (int64_t)members[sq_[0]] : -1;
+    best_sum[c] = sv[0];
+  }
+}
+
+int grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > 148 * 32) g = 148 * 32;
+  return (int)(g > 0 ? g : 1);
+}
+
+}  // namespace
+
+cudaError_t launch_expand_square(const double* condensed, int64_t p, double* square,
+                                 cudaStream_t s) {
+  const unsigned nb = (unsigned)((p + 31) / 32);
+  expand_square_kernel<<<dim3(nb, nb), dim3(32, 8), 0, s>>>(condensed, p, square);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_validate_condensed(const double* condensed, int64_t total, int* bad,
+                                      cudaStream_t s) {
+  validate_kernel<<<grid_for(total, 256), 256, 0, s>>>(condensed, total, bad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_nearest_update(const double* square, int64_t p, int64_t current,
+                                  const uint8_t* chosen, double* nearest, cudaStream_t s) {
+  nearest_update_kernel<<<grid_for(p, 256), 256, 0, s>>>(square, p, current, chosen, nearest);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_assign(const double* square, int64_t p, const int64_t* medoids, int64_t k,
+                          int64_t* assignment, double* dist, cudaStream_t s) {
+  assign_kernel<<<grid_for(p, 256), 256, 0, s>>>(square, p, medoids, k, assignment, dist);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update(const double* square, int64_t p, const int32_t* members,
+                          const int64_t* cluster_begin, int64_t k, int64_t* best_member,
+                          double* best_sum, cudaStream_t s) {
+  // sums scratch lives right after best_sum (k doubles) -- caller allocates p more.
+  double* sums = best_sum + k;
+  candidate_sum_kernel<<<grid_for(p, 128), 128, 0, s>>>(square, p, members, cluster_begin, k,
+                                                         sums);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  cluster_argmin_kernel<<<(unsigned)k, 256, 0, s>>>(members, cluster_begin, sums, best_member,
+                                                    best_sum);
+  return cudaGetLastError();
+}
+
+}  // namespace dtwgpu

@@ -1,0 +1,263 @@
+"""GPU parity of the DTW fill (through the C-ABI) against the oracle and the reference.
+
+Bar (BASELINE.json north_star): fp64 distances bitwise-equal to the reference built
+without FMA (the contract's 1e-12 relative is met with 0 ulp); fp32 mode within 1e-5
+relative. Mirrors test_dtw.cpp, test_distance_matrix.cpp and acceptance criteria 1, 2, 7.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2307_04904_b200 import api, generators as gen
+from paper_2307_04904_b200.api import (BandInfeasibleError, BuildStats, EmptyDatasetError,
+                                       InvalidArgumentsError, InvalidSeriesError, TimeSeries,
+                                       WarpWindow, build_matrix)
+from tests.helpers import ScalarRng, assert_bitwise, pack, random_int_series
+
+pytestmark = pytest.mark.gpu
+
+U = WarpWindow.unlimited()
+
+
+def ts(name, vals):
+    return TimeSeries(name, np.array(vals, dtype=np.float64))
+
+
+def gpu_pair(x, y, w):
+    m = build_matrix([ts("x", x), ts("y", y)], w, 1)
+    return m.distance(0, 1)
+
+
+# ---------------------------------------------------------------- test_dtw.cpp:30-78
+def test_identical_series_is_zero():
+    assert gpu_pair([1, 2, 3], [1, 2, 3], U) == 0.0
+    assert gpu_pair([1, 2, 3], [1, 2, 3], WarpWindow.banded(0)) == 0.0
+
+
+def test_two_singletons():
+    assert gpu_pair([0], [5], U) == 25.0
+
+
+def test_one_to_many():
+    assert gpu_pair([1, 2, 3], [1, 2, 2, 3], U) == 0.0
+
+
+def test_zero_width_band_forces_diagonal():
+    assert gpu_pair([0, 0, 0, 10], [10, 0, 0, 0], WarpWindow.banded(0)) == 200.0
+    assert gpu_pair([0, 0, 0, 10], [10, 0, 0, 0], U) == oracle.dtw_brute_force(
+        [0, 0, 0, 10], [10, 0, 0, 0])
+
+
+def test_invalid_series_rejected():
+    good = ts("good", [1, 2])
+    with pytest.raises(InvalidSeriesError):
+        build_matrix([ts("empty", []), good], U, 1)
+    with pytest.raises(InvalidSeriesError):
+        build_matrix([ts("nan", [1, np.nan]), good], U, 1)
+    with pytest.raises(InvalidSeriesError):
+        build_matrix([ts("inf", [np.inf]), good], U, 1)
+
+
+def test_band_narrower_than_gap_rejected():
+    x, y = [1, 2, 3, 4, 5], [1, 2]
+    with pytest.raises(BandInfeasibleError):
+        build_matrix([ts("x", x), ts("y", y)], WarpWindow.banded(2), 1)
+    assert gpu_pair(x, y, WarpWindow.banded(3)) == oracle.dtw_brute_force(x, y, 3)
+
+
+# ---------------------------------------------------------------- test_dtw.cpp:80-124
+def _random_pairs(seed, count, max_len):
+    rng = ScalarRng(seed)
+    out = []
+    for _ in range(count):
+        x = random_int_series(rng, max_len, -5, 5)
+        y = random_int_series(rng, max_len, -5, 5)
+        gap = abs(len(x) - len(y))
+        windows = [-1] + [hw for hw in (0, 1, 2) if hw >= gap]
+        w = windows[rng.next_below(len(windows))]
+        out.append((x, y, w))
+    return out
+
+
+@pytest.mark.parametrize("seed,count", [(20240601, 500), (0xAC5E01, 2000)])
+def test_matches_exhaustive_oracle_on_random_small_pairs(eng, seed, count):
+    pairs = _random_pairs(seed, count, 8)
+    for w in (-1, 0, 1, 2):
+        sel = [(x, y) for (x, y, ww) in pairs if ww == w]
+        rows = []
+        for x, y in sel:
+            rows += [x, y]
+        samples, offsets = pack(rows)
+        # auto_widen so that cross pairs (not in the reference test) stay feasible
+        got = eng.build_condensed(samples, offsets, w, auto_widen=True)
+        want = oracle.build_condensed(samples, offsets, w, True)
+        assert_bitwise(got, want, f"w={w}")
+        p = len(rows)
+        for t, (x, y) in enumerate(sel):
+            i, j = 2 * t, 2 * t + 1
+            slot = i * p - i * (i + 1) // 2 + (j - i - 1)
+            assert got[slot] == oracle.dtw_brute_force(x, y, w)
+
+
+def test_symmetric_and_band_monotone():
+    rng = ScalarRng(99)
+    for _ in range(30):
+        x = random_int_series(rng, 8, -5, 5)
+        y = random_int_series(rng, 8, -5, 5)
+        gap = abs(len(x) - len(y))
+        sat = max(len(x), len(y))
+        prev = np.inf
+        for hw in range(gap, sat + 1):
+            c = gpu_pair(x, y, WarpWindow.banded(hw))
+            assert c <= prev
+            assert c == gpu_pair(y, x, WarpWindow.banded(hw))
+            prev = c
+        assert prev == gpu_pair(x, y, U)
+
+
+# ---------------------------------------------------------------- every instantiation
+FULL = [(2, 23), (4, 12), (8, 8), (16, 8), (16, 16), (32, 4), (32, 8), (32, 12), (32, 15),
+        (32, 16)]
+BAND = [(16, 7), (16, 9), (16, 11), (16, 13), (32, 3), (32, 5), (32, 7), (32, 9), (32, 13)]
+
+
+def _walks(seed, lengths):
+    rng = gen.SplitMix64(seed)
+    rows = []
+    for L in lengths:
+        rows.append(np.cumsum(rng.gaussian(int(L))))
+    return pack(rows)
+
+
+@pytest.mark.parametrize("G,R", FULL)
+@pytest.mark.parametrize("fp32", [False, True])
+def test_full_family_every_instantiation(eng, G, R, fp32):
+    rng = np.random.default_rng(G * 100 + R)
+    lengths = rng.integers(1, 700, size=14)
+    lengths[:3] = [1, G * R, G * R + 1]
+    samples, offsets = _walks(7 + G + R, lengths)
+    for hw, aw in ((-1, False), (40, True), (3, True)):
+        eng.force_kernel(0, G, R)
+        got = eng.build_condensed(samples, offsets, hw, aw, precision=1 if fp32 else 0)
+        plan = eng.last_plan()
+        assert f"full[G={G},R={R}" in plan, plan
+        want = oracle.build_condensed(samples, offsets, hw, aw)
+        if fp32:
+            np.testing.assert_allclose(got, want, rtol=1e-5, atol=0)
+        else:
+            assert_bitwise(got, want, f"full G={G} R={R} hw={hw}")
+
+
+@pytest.mark.parametrize("G,R", BAND)
+@pytest.mark.parametrize("fp32", [False, True])
+def test_band_family_every_instantiation(eng, G, R, fp32):
+    rng = np.random.default_rng(G * 1000 + R)
+    kmax = G * R
+    for hw in sorted({0, 1, (kmax - 1) // 2, max((kmax - 1) // 2 - 3, 0), 7}):
+        if 2 * hw + 1 > kmax:
+            continue
+        base = int(rng.integers(hw + 2, 400))
+        lengths = [base + int(d) for d in rng.integers(-hw, hw + 1, size=10)]
+        lengths = [max(L, 1) for L in lengths]
+        samples, offsets = _walks(11 + hw, lengths)
+        eng.force_kernel(1, G, R)
+        got = eng.build_condensed(samples, offsets, hw, True, precision=1 if fp32 else 0)
+        plan = eng.last_plan()
+        want = oracle.build_condensed(samples, offsets, hw, True)
+        if fp32:
+            np.testing.assert_allclose(got, want, rtol=1e-5, atol=0)
+        else:
+            assert_bitwise(got, want, f"band G={G} R={R} hw={hw} plan={plan}")
+
+
+# ---------------------------------------------------------------- configs (oracle-sized)
+@pytest.mark.parametrize("cfg,q", [(1, 100), (2, 60), (3, 400), (4, 6), (5, 70)])
+def test_config_parity_bitwise(eng, cfg, q):
+    ds = gen.make_config(cfg).subset(q)
+    got = eng.build_condensed(ds.samples, ds.offsets, ds.half_width, ds.auto_widen)
+    want = oracle.build_condensed(ds.samples, ds.offsets, ds.half_width, ds.auto_widen)
+    assert_bitwise(got, want, f"c{cfg}[:{q}] plan={eng.last_plan()}")
+
+
+def test_config4_fp32_within_tolerance(eng):
+    ds = gen.config4().subset(8)
+    got = eng.build_condensed(ds.samples, ds.offsets, -1, precision=1)
+    want = oracle.build_condensed(ds.samples, ds.offsets, -1)
+    rel = np.abs(got - want) / np.abs(want)
+    assert rel.max() <= 1e-5, rel.max()
+
+
+def test_slot_ranges_assemble_the_matrix(eng):
+    import torch
+    ds = gen.config5().subset(50)
+    p = ds.p
+    total = p * (p - 1) // 2
+    full = eng.build_condensed(ds.samples, ds.offsets, ds.half_width, True)
+    eng.upload(ds.samples, ds.offsets)
+    parts = []
+    cuts = [0, 1, 333, 334, 900, total]
+    for b, e in zip(cuts[:-1], cuts[1:]):
+        buf = torch.empty(max(e - b, 1), dtype=torch.float64, device="cuda")
+        eng.fill_slots(ds.half_width, True, 0, b, e, buf.data_ptr())
+        torch.cuda.synchronize()
+        parts.append(buf[: e - b].cpu().numpy())
+    assert_bitwise(np.concatenate(parts), full, "slot ranges")
+
+
+# ---------------------------------------------------------------- matrix semantics
+def test_single_series_gives_1x1():
+    stats = BuildStats()
+    m = build_matrix([ts("only", [1, 2, 3])], U, 1, stats)
+    assert m.size() == 1 and m.distance(0, 0) == 0.0 and stats.evaluations == 0
+
+
+def test_evaluations_and_worker_invariance():
+    rng = ScalarRng(11)
+    data = [ts(f"s{i}", random_int_series(rng, 12, -5, 5)) for i in range(17)]
+    s1 = BuildStats()
+    a = build_matrix(data, U, 1, s1)
+    assert s1.evaluations == 17 * 16 // 2
+    for w in (2, 3, 8, 64):
+        st = BuildStats()
+        b = build_matrix(data, U, w, st)
+        assert st.evaluations == 17 * 16 // 2
+        assert_bitwise(a.condensed(), b.condensed())
+    samples, offsets = pack([d.samples for d in data])
+    ref, ev = oracle.ref_build_condensed(samples, offsets, -1, workers=3) if oracle.have_ref() \
+        else (oracle.build_condensed(samples, offsets), 136)
+    assert_bitwise(a.condensed(), ref)
+
+
+def test_build_rejects_bad_inputs():
+    with pytest.raises(EmptyDatasetError):
+        build_matrix([], U, 1)
+    with pytest.raises(InvalidArgumentsError):
+        build_matrix([ts("a", [1])], U, 0)
+    with pytest.raises(InvalidSeriesError):
+        build_matrix([ts("a", [1]), ts("a", [2])], U, 1)
+    with pytest.raises(InvalidSeriesError):
+        build_matrix([ts("a", [1]), ts("b", [])], U, 1)
+
+
+def test_first_band_infeasible_pair():
+    data = [ts("a", [1, 2]), ts("b", [1, 2, 3]), ts("c", [1, 2, 3, 4, 5, 6])]
+    with pytest.raises(BandInfeasibleError) as ei:
+        build_matrix(data, WarpWindow.banded(1), 1)
+    assert ei.value.has_pair() and (ei.value.pair_i, ei.value.pair_j) == (0, 2)
+
+
+def test_auto_widen_equals_gap_band():
+    data = [ts("a", [1, 2]), ts("b", [1, 2, 3, 4, 5, 6])]
+    widened = build_matrix(data, WarpWindow.banded(1), 1, None, True)
+    assert widened.distance(0, 1) == gpu_pair([1, 2], [1, 2, 3, 4, 5, 6], WarpWindow.banded(4))
+
+
+def test_memory_scale_long_pair(eng):
+    """acceptance criterion 3 analogue: n = m = 20000 random walks, one pair."""
+    rng = ScalarRng(0x3E)
+    from tests.helpers import random_walk_series
+    x = random_walk_series(rng, 20000)
+    y = random_walk_series(rng, 20000)
+    samples, offsets = pack([x, y])
+    got = eng.build_condensed(samples, offsets, -1)
+    assert got[0] == oracle.dtw(x, y, -1)

@@ -1,0 +1,127 @@
+"""GPU k-medoids sweeps vs the reference's kmedoids (oracle/_ref) and the C restatement.
+
+Bar: medoids and labels identical, total cost bit-identical (test_kmedoids.cpp,
+acceptance criterion 7, test_csv_runner.cpp:192-200 reconstructed cost).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2307_04904_b200 import api, generators as gen
+from paper_2307_04904_b200.api import (DistanceMatrix, InvalidArgumentsError, KMedoidsConfig,
+                                       KOutOfRangeError, TimeSeries, WarpWindow, build_matrix,
+                                       kmedoids)
+from tests.helpers import ScalarRng, blob_series, random_condensed
+
+pytestmark = pytest.mark.gpu
+
+
+def kref(D, p, cfg, observer=None):
+    if oracle.have_ref():
+        return oracle.ref_kmedoids(D, p, cfg.k, cfg.restarts, cfg.max_iterations, cfg.seed,
+                                   observer)
+    return oracle.kmedoids(D, p, cfg.k, cfg.restarts, cfg.max_iterations, cfg.seed, observer)
+
+
+def check_same(D, p, cfg):
+    m = DistanceMatrix.from_condensed(p, D)
+    got = kmedoids(m, cfg)
+    med, asg, cost = kref(D, p, cfg)
+    assert got.medoids == [int(v) for v in med]
+    assert got.assignment == [int(v) for v in asg]
+    assert got.total_cost == cost
+    return got
+
+
+def test_k_equals_p():
+    D = random_condensed(ScalarRng(1), 6)
+    got = check_same(D, 6, KMedoidsConfig(k=6, restarts=2))
+    assert got.total_cost == 0.0 and got.assignment == list(range(6))
+
+
+def test_k_one_global_medoid():
+    D = random_condensed(ScalarRng(2), 9)
+    check_same(D, 9, KMedoidsConfig(k=1, restarts=1))
+
+
+def test_two_blobs():
+    data = []
+    for i in range(5):
+        data.append(TimeSeries(f"low{i}", [0.1 * i] * 4))
+    for i in range(5):
+        data.append(TimeSeries(f"high{i}", [100 + 0.1 * i] * 4))
+    m = build_matrix(data, WarpWindow.unlimited(), 1)
+    got = kmedoids(m, KMedoidsConfig(k=2, seed=11))
+    med, asg, cost = kref(m.condensed(), 10, KMedoidsConfig(k=2, seed=11))
+    assert got.total_cost == cost and got.medoids == list(med)
+    assert len(set(got.assignment[:5])) == 1 and len(set(got.assignment[5:])) == 1
+
+
+@pytest.mark.parametrize("p,k,seed", [(20, 4, 20240101), (15, 3, 5), (25, 4, 99), (30, 5, 1234),
+                                      (200, 7, 0xDEED), (1000, 8, 0)])
+def test_random_matrices_match_reference(p, k, seed):
+    D = random_condensed(ScalarRng(p + k), p)
+    check_same(D, p, KMedoidsConfig(k=k, restarts=6, seed=seed))
+
+
+def test_observer_trace_matches_and_descends():
+    D = random_condensed(ScalarRng(6), 25)
+    cfg = KMedoidsConfig(k=4, restarts=6, seed=99)
+    trace_gpu, trace_ref = [], []
+    kmedoids(DistanceMatrix.from_condensed(25, D), cfg,
+             lambda r, it, c: trace_gpu.append((r, it, c)))
+    kref(D, 25, cfg, lambda r, it, c: trace_ref.append((r, it, c)))
+    assert trace_gpu == trace_ref
+    by_r = {}
+    for r, it, c in trace_gpu:
+        by_r.setdefault(r, []).append(c)
+    for costs in by_r.values():
+        assert all(b <= a for a, b in zip(costs, costs[1:]))
+
+
+def test_duplicates_and_fixed_point():
+    data = [TimeSeries(f"dup{i}", [1.0, 2.0, 3.0]) for i in range(6)]
+    m = build_matrix(data, WarpWindow.unlimited(), 1)
+    got = kmedoids(m, KMedoidsConfig(k=3, seed=9))
+    med, asg, cost = kref(m.condensed(), 6, KMedoidsConfig(k=3, seed=9))
+    assert got.total_cost == 0.0 == cost and got.medoids == list(med)
+    D = random_condensed(ScalarRng(4), 15)
+    mm = DistanceMatrix.from_condensed(15, D)
+    res = kmedoids(mm, KMedoidsConfig(k=3, seed=5))
+    assert api.assign_to_medoids(mm, res.medoids) == res.assignment
+    assert api.update_medoids(mm, res.medoids, res.assignment) == res.medoids
+    assert api.assignment_cost(mm, res.assignment) == res.total_cost
+
+
+def test_invalid_configs():
+    m = DistanceMatrix.from_condensed(4, random_condensed(ScalarRng(10), 4))
+    with pytest.raises(KOutOfRangeError):
+        kmedoids(m, KMedoidsConfig(k=5))
+    with pytest.raises(KOutOfRangeError):
+        kmedoids(m, KMedoidsConfig(k=0))
+    with pytest.raises(InvalidArgumentsError):
+        kmedoids(m, KMedoidsConfig(k=2, restarts=0))
+
+
+def test_sweep_pieces_match_reference():
+    p, k = 300, 9
+    D = random_condensed(ScalarRng(77), p)
+    m = DistanceMatrix.from_condensed(p, D)
+    medoids = sorted(np.random.default_rng(0).choice(p, k, replace=False).tolist())
+    asg_ref, cost_ref, upd_ref = oracle.ref_sweep(D, p, medoids) if oracle.have_ref() else (
+        oracle.assign(D, p, medoids), None, None)
+    assert api.assign_to_medoids(m, medoids) == list(asg_ref)
+    if upd_ref is not None:
+        assert api.update_medoids(m, medoids, list(asg_ref)) == list(upd_ref)
+
+
+@pytest.mark.parametrize("cfgno,q", [(1, 100), (3, 600), (5, 150)])
+def test_config_pipeline_matches_reference(eng, cfgno, q):
+    ds = gen.make_config(cfgno).subset(q)
+    m = api.build_matrix_packed(ds.samples, ds.offsets,
+                                WarpWindow(None if ds.half_width < 0 else ds.half_width),
+                                ds.auto_widen)
+    cfg = KMedoidsConfig(k=ds.k, restarts=3, seed=0)
+    got = kmedoids(m, cfg)
+    med, asg, cost = kref(m.condensed(), ds.p, cfg)
+    assert got.medoids == list(med) and got.assignment == list(asg) and got.total_cost == cost

@@ -1,0 +1,83 @@
+// cell_microbench.cu -- measures the sm_100a ceiling of the DTW cell update itself.
+//
+// Each thread runs CH independent chains of the exact fp64 cell body used by the fill
+//   v = (x - y)^2 + min(min(diag, up), left)     (DADD, DMUL, 2x DSETP+2 FSEL, DADD)
+// (and the fp32 body FADD, FMUL, FMNMX3, FADD), so the result is the issue/pipe-bound
+// peak in cells per SM-clock, independent of memory and of the wavefront. Reported as
+// GCUPS at the measured SM clock; compare with the 148*64*f/5 fp64 estimate.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o cell_microbench cell_microbench.cu
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+template <int CH, class T>
+__global__ void cells(const T* in, T* out, int iters) {
+  T x = in[threadIdx.x & 7], y[CH], a[CH], b[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    y[c] = in[(c + 1) & 7];
+    a[c] = in[(c + 2) & 7];
+    b[c] = in[(c + 3) & 7];
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      T d, v;
+      if constexpr (sizeof(T) == 8) {
+        d = __dsub_rn(x, y[c]);
+        const T m1 = b[c] < a[c] ? b[c] : a[c];
+        const T m2 = y[c] < m1 ? y[c] : m1;
+        v = __dadd_rn(__dmul_rn(d, d), m2);
+      } else {
+        d = __fsub_rn(x, y[c]);
+        v = __fadd_rn(__fmul_rn(d, d), fminf(fminf(a[c], b[c]), y[c]));
+      }
+      a[c] = b[c];
+      b[c] = v;
+      y[c] = v;  // keep the chain dependent like cur[j-1]
+    }
+  }
+  T s = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s += b[c];
+  if (s == (T)-1) out[threadIdx.x] = s;
+}
+
+template <class T>
+void run(const char* name) {
+  T* in;
+  T* out;
+  cudaMalloc(&in, 64 * sizeof(T));
+  cudaMalloc(&out, 1024 * sizeof(T));
+  T h[8] = {1, 2, 3, 4, 5, 6, 7, 8};
+  cudaMemcpy(in, h, sizeof(h), cudaMemcpyHostToDevice);
+  int sms = 0, clk = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  const int iters = 4096;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int warps : {4, 8, 16, 32}) {
+    const int blocks = sms * warps / 4;
+    cells<8, T><<<blocks, 128>>>(in, out, iters);
+    cudaEventRecord(e0);
+    cells<8, T><<<blocks, 128>>>(in, out, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double cellsn = (double)blocks * 128 * 8 * iters;
+    const double gcups = cellsn / (ms * 1e-3) / 1e9;
+    printf("{\"body\":\"%s\",\"warps_per_sm\":%d,\"gcups\":%.1f,\"cells_per_sm_clk_at_max\":%.2f}\n",
+           name, warps, gcups, gcups * 1e9 / (sms * (clk * 1e3)));
+  }
+  cudaFree(in);
+  cudaFree(out);
+}
+
+int main() {
+  run<double>("fp64");
+  run<float>("fp32");
+  return 0;
+}
