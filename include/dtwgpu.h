@@ -91,6 +91,10 @@ int dtwg_count_cells(dtwg_ctx* ctx, int64_t half_width, int auto_widen, int64_t 
 int dtwg_last_fill_ms(dtwg_ctx* ctx, float* ms);
 /* Number of kernels this context has launched so far (bench `gpu_launches`). */
 uint64_t dtwg_launch_count(const dtwg_ctx* ctx);
+/* Roofline denominator, measured live: cells/s of the bare cell body (5 fp64-pipe ops:
+ * sub, mul, two compare-selects, add; or the fp32 body) on every SM with no memory or
+ * dependency stalls. */
+int dtwg_measure_cell_peak(dtwg_ctx* ctx, int precision, double* cells_per_s);
 /* Diagnostics/tests: force kernel family (0 = full, 1 = band) and (G, R) for every
  * pair shape it can legally run; family < 0 restores the cost-model planner. */
 int dtwg_force_kernel(dtwg_ctx* ctx, int family, int G, int R);

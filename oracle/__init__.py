@@ -55,6 +55,10 @@ def lib():
     L.oracle_kmedoids.argtypes = [_dp, _i64, _i64, _i64, _i64, C.c_uint64, OBSERVER, C.c_void_p,
                                   _ip, _ip, C.POINTER(C.c_double)]
     L.oracle_kmedoids.restype = C.c_int
+    L.oracle_kmedoids_range.argtypes = [_dp, _i64, _i64, _i64, _i64, C.c_uint64, _i64, _i64,
+                                        OBSERVER, C.c_void_p, _ip, _ip, C.POINTER(C.c_double),
+                                        C.POINTER(_i64)]
+    L.oracle_kmedoids_range.restype = C.c_int
     L.oracle_splitmix_next.argtypes = [C.POINTER(C.c_uint64)]
     L.oracle_splitmix_next.restype = C.c_uint64
     return L
@@ -160,6 +164,20 @@ def kmedoids(D, p, k, restarts=10, max_iterations=100, seed=0, observer=None):
     if rc:
         raise RuntimeError(f"oracle_kmedoids error code {rc}")
     return med[:k], asg, cost.value
+
+
+def kmedoids_range(D, p, k, restarts, max_iterations, seed, rb, re):
+    """Restarts [rb, re) only; returns (medoids, assignment, cost, best_restart)."""
+    med = np.empty(max(k, 1), dtype=np.int64)
+    asg = np.empty(p, dtype=np.int64)
+    cost = C.c_double()
+    br = _i64(-1)
+    rc = lib().oracle_kmedoids_range(_f64(D), p, k, restarts, max_iterations, seed, rb, re,
+                                     OBSERVER(lambda *a: None), None, med, asg, C.byref(cost),
+                                     C.byref(br))
+    if rc:
+        raise RuntimeError(f"oracle_kmedoids_range error code {rc}")
+    return med[:k], asg, cost.value, int(br.value)
 
 
 # ---------------------------------------------------------------- reference itself

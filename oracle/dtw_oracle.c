@@ -398,18 +398,35 @@ typedef void (*oracle_observer_fn)(void* user, int64_t restart, int64_t iteratio
  * kmedoids.hpp:148-189 kmedoids over a condensed matrix. Returns 0, or the
  * reference error code (KOutOfRange=10, InvalidArguments=2).
  */
+int oracle_kmedoids_range(const double* D, int64_t p, int64_t k, int64_t restarts,
+                          int64_t max_iter, uint64_t seed, int64_t rb, int64_t re,
+                          oracle_observer_fn observer, void* user, int64_t* medoids_out,
+                          int64_t* assignment_out, double* cost_out, int64_t* best_r_out);
+
 int oracle_kmedoids(const double* D, int64_t p, int64_t k, int64_t restarts, int64_t max_iter,
                     uint64_t seed, oracle_observer_fn observer, void* user, int64_t* medoids_out,
                     int64_t* assignment_out, double* cost_out) {
+  int64_t best_r = -1;
+  return oracle_kmedoids_range(D, p, k, restarts, max_iter, seed, 0, restarts, observer, user,
+                               medoids_out, assignment_out, cost_out, &best_r);
+}
+
+/* Restarts [rb, re) of a `restarts`-restart run (restart_stream(seed, r) per restart), so a
+ * run can be split across workers and reduced in restart order. */
+int oracle_kmedoids_range(const double* D, int64_t p, int64_t k, int64_t restarts,
+                          int64_t max_iter, uint64_t seed, int64_t rb, int64_t re,
+                          oracle_observer_fn observer, void* user, int64_t* medoids_out,
+                          int64_t* assignment_out, double* cost_out, int64_t* best_r_out) {
   if (k < 1 || k > p) return 10;
   if (restarts < 1) return 2;
   if (max_iter < 1) return 2;
+  if (re > restarts) re = restarts;
   int64_t* med = (int64_t*)malloc(sizeof(int64_t) * (size_t)k);
   int64_t* upd = (int64_t*)malloc(sizeof(int64_t) * (size_t)k);
   int64_t* asg = (int64_t*)malloc(sizeof(int64_t) * (size_t)p);
   int have_best = 0;
   double best_cost = 0.0;
-  for (int64_t r = 0; r < restarts; ++r) {
+  for (int64_t r = rb; r < re; ++r) {
     oracle_rng rng = restart_stream(seed, (uint64_t)r);
     spread_seeds(D, p, k, &rng, med);
     double cost = 0.0;
@@ -431,6 +448,7 @@ int oracle_kmedoids(const double* D, int64_t p, int64_t k, int64_t restarts, int
       memcpy(medoids_out, med, sizeof(int64_t) * (size_t)k);
       memcpy(assignment_out, asg, sizeof(int64_t) * (size_t)p);
       have_best = 1;
+      *best_r_out = r;
     }
   }
   *cost_out = best_cost;

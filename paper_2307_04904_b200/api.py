@@ -175,6 +175,12 @@ class Engine:
         """Tests/diagnostics: pin the kernel family/(G, R); family < 0 = cost model."""
         self.check(self.L.dtwg_force_kernel(self.h, family, G, R))
 
+    def measure_cell_peak(self, precision: int = FP64) -> float:
+        """Cells/s ceiling of the bare cell body on this GPU (roofline denominator)."""
+        v = C.c_double()
+        self.check(self.L.dtwg_measure_cell_peak(self.h, precision, C.byref(v)))
+        return float(v.value)
+
     def last_plan(self) -> str:
         return self.L.dtwg_last_plan(self.h).decode()
 

@@ -34,6 +34,7 @@ struct KernelCfg {
   int R;
   bool mask;
   bool fp32;
+  int kr = -1;  // Band family: (2hw+1) % R when every pair of the launch shares it, else -1
 };
 
 // Launches cfg over args on stream with `blocks` CTAs of kThreads threads.
@@ -45,6 +46,9 @@ int fill_blocks_per_sm(const KernelCfg& cfg);
 bool fill_cfg_supported(const KernelCfg& cfg);
 
 constexpr int kThreads = 128;
+
+// ---- cell-body ceiling (peak.cu) -------------------------------------------------
+cudaError_t measure_cell_peak(cudaStream_t st, int sms, bool fp32, double* cells_per_s);
 
 // ---- k-medoids sweep kernels (kmedoids.cu) -------------------------------------
 cudaError_t launch_expand_square(const double* condensed, int64_t p, double* square,

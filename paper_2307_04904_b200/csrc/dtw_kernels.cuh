@@ -1,0 +1,498 @@
+// dtw_kernels.cuh -- sm_100a kernels for the all-pairs banded DTW distance-matrix fill.
+//
+// Replaces the inside of dtwclust::build_matrix (pairwise.hpp:81-126), whose per-pair
+// work is dtw_distance (dtw.hpp:40-75, hot loop :59-73):
+//     cur[j] = (x_i - y_j)^2 + min(prev[j-1], prev[j], cur[j-1])
+// Two kernel families, both "one group of G lanes per pair, R DP cells per lane per
+// row, anti-diagonal wavefront across lanes, rolling rows in registers":
+//
+//  * Full  (column strips).  Lane l owns R consecutive columns of the shorter series
+//    (y held in registers) and runs one step behind lane l-1; each step it advances TWO
+//    rows, interleaving the two cell chains (ILP 2). The cells left of its strip arrive
+//    from lane l-1 by __shfl_up_sync. Series longer than G*R columns are done in
+//    passes; the strip's last column is handed to the next pass through a per-group
+//    boundary column in global memory (L2-resident). Used for unlimited and wide
+//    (auto-widened) bands; `MASK` adds warp-uniform band masking.
+//  * Band  (sheared coordinates k = j - i + hw).  For narrow Sakoe-Chiba bands: lane l
+//    owns band offsets [lR, lR+R), so the 2hw+1-wide band is covered by one group and
+//    almost no out-of-band cell is computed. Dependencies become left (k-1, same row),
+//    diag (k, prev row) and up (k+1, prev row): the left cell arrives from lane l-1
+//    (shfl_up, previous step), the up cell of the strip's last column from lane l+1's
+//    first cell of the previous row (shfl_down, same step). The y window slides one
+//    sample per row; it rotates through registers (R steps unrolled) and is fed from
+//    lane l+1 by shfl_down, so there are no per-cell loads.
+//
+// All loops are warp-uniform (groups of one warp run the warp's maximum trip count and
+// idle through the surplus), so every shuffle uses the full mask and no divergence
+// checks are emitted. Per-pair indices are 32-bit.
+//
+// Arithmetic (fp64): __dsub_rn / __dmul_rn / __dadd_rn (no FMA contraction) and a
+// plain compare-select min -- bit-identical to the reference built without -march
+// (SURVEY.md finding 4, hard part H1). Out-of-band and padding cells are +inf, as in
+// dtw.hpp:61-71. Orientation (longer series on rows) follows dtw.hpp:45-47; the
+// recurrence is bitwise transposable anyway.
+//
+// fp32 mode (precision == DTWG_FP32): samples rounded to fp32, squared differences
+// and running sums in fp32, each lane keeping its values relative to a private fp64
+// offset that is renormalised to the strip minimum every few rows, so fp32 magnitudes
+// stay small. Cells crossing lanes are re-based with the
+// neighbour's offset.
+#pragma once
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+
+#include "dtw_fill.cuh"
+
+namespace dtwgpu {
+namespace kern {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kRenormSteps = 8;  // fp32 mode: steps between per-lane offset renormalisations
+
+__device__ __forceinline__ int64_t row_off(int64_t i, int64_t p) { return i * p - i * (i + 1) / 2; }
+
+// Condensed slot -> (i, j), i < j (pairwise.hpp:41-53), closed form + fix-up.
+__device__ __forceinline__ void decode_slot(int64_t s, int64_t p, int64_t& i, int64_t& j) {
+  const double tp = 2.0 * (double)p - 1.0;
+  const double disc = tp * tp - 8.0 * (double)s;
+  int64_t r = (int64_t)((tp - sqrt(disc > 0.0 ? disc : 0.0)) * 0.5);
+  if (r < 0) r = 0;
+  if (r > p - 2) r = p - 2;
+  while (r > 0 && row_off(r, p) > s) --r;
+  while (r + 1 <= p - 2 && row_off(r + 1, p) <= s) ++r;
+  i = r;
+  j = r + 1 + (s - row_off(r, p));
+}
+
+// ---- arithmetic policies ----------------------------------------------------------
+struct F64 {
+  using T = double;
+  static __device__ __forceinline__ T inf() { return CUDART_INF; }
+  static __device__ __forceinline__ T mn(T a, T b) { return b < a ? b : a; }
+  // (x - y)^2 + best, each op rounded separately (dtw.hpp:16-19, :69).
+  static __device__ __forceinline__ T cell(T x, T y, T best) {
+    const T d = __dsub_rn(x, y);
+    return __dadd_rn(__dmul_rn(d, d), best);
+  }
+  static __device__ __forceinline__ const T* base(const FillArgs& A) { return A.samples; }
+};
+
+struct F32 {
+  using T = float;
+  static __device__ __forceinline__ T inf() { return CUDART_INF_F; }
+  static __device__ __forceinline__ T mn(T a, T b) { return fminf(a, b); }
+  static __device__ __forceinline__ T cell(T x, T y, T best) {
+    const T d = __fsub_rn(x, y);
+    return __fadd_rn(__fmul_rn(d, d), best);
+  }
+  static __device__ __forceinline__ const T* base(const FillArgs& A) { return A.samples32; }
+};
+
+struct Pair {
+  int64_t slot;
+  int64_t xoff, yoff;  // rows series (longer), columns series (shorter)
+  int n, m;            // n >= m
+  int hw;              // effective half width (pair_window, pairwise.hpp:29-33)
+};
+
+__device__ __forceinline__ Pair load_pair(const FillArgs& A, int64_t item) {
+  Pair P;
+  P.slot = A.list ? A.list[item] : A.begin + item;
+  int64_t a, b;
+  decode_slot(P.slot, A.p, a, b);
+  const int64_t oa = A.offsets[a], ob = A.offsets[b];
+  const int la = (int)(A.offsets[a + 1] - oa), lb = (int)(A.offsets[b + 1] - ob);
+  if (la >= lb) {
+    P.xoff = oa; P.n = la; P.yoff = ob; P.m = lb;
+  } else {
+    P.xoff = ob; P.n = lb; P.yoff = oa; P.m = la;
+  }
+  if (A.half_width < 0 || A.half_width >= P.n) {
+    P.hw = P.n;  // warp_window.hpp:33-35: unlimited -> max(n, m)
+  } else {
+    const int gap = P.n - P.m;
+    P.hw = (A.auto_widen && gap > (int)A.half_width) ? gap : (int)A.half_width;
+  }
+  return P;
+}
+
+// Value re-based from a neighbour's fp32 offset to ours (fp32 mode only).
+__device__ __forceinline__ float rebase(float v, double from, double to) {
+  return v == CUDART_INF_F ? v : (float)((double)v + (from - to));
+}
+
+// ===================================================================================
+// Full family: column strips, two rows per step, multi-pass, optional band mask.
+// ===================================================================================
+template <int R, bool MASK, class Ar>
+struct FullRows {
+  using T = typename Ar::T;
+  // Two rows (a = r0, b = r0+1): a_r needs (pv[r-1]|diag0, pv[r], a_{r-1});
+  // b_r needs (a_{r-1}|L0, a_r, b_{r-1}). pv becomes row b.
+  static __device__ __forceinline__ void two(T (&pv)[R], const T (&yv)[R], T x0, T x1, T diag0,
+                                             T L0, T L1, int jl, int r0, int hw, T& aout,
+                                             T& bout) {
+    const T INF = Ar::inf();
+    T ad = diag0, al = L0, bd = L0, bl = L1;
+    const int lo0 = r0 - hw, hi0 = r0 + hw;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const T up = pv[r];
+      T a = Ar::cell(x0, yv[r], Ar::mn(Ar::mn(ad, up), al));
+      if (MASK) a = (jl + r >= lo0 && jl + r <= hi0) ? a : INF;
+      T b = Ar::cell(x1, yv[r], Ar::mn(Ar::mn(bd, a), bl));
+      if (MASK) b = (jl + r >= lo0 + 1 && jl + r <= hi0 + 1) ? b : INF;
+      ad = up;
+      al = a;
+      bd = a;
+      bl = b;
+      pv[r] = b;
+    }
+    aout = al;
+    bout = bl;
+  }
+  static __device__ __forceinline__ void one(T (&pv)[R], const T (&yv)[R], T x0, T diag0, T L0,
+                                             int jl, int r0, int hw, T& aout) {
+    const T INF = Ar::inf();
+    T ad = diag0, al = L0;
+    const int lo0 = r0 - hw, hi0 = r0 + hw;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const T up = pv[r];
+      T a = Ar::cell(x0, yv[r], Ar::mn(Ar::mn(ad, up), al));
+      if (MASK) a = (jl + r >= lo0 && jl + r <= hi0) ? a : INF;
+      ad = up;
+      al = a;
+      pv[r] = a;
+    }
+    aout = al;
+  }
+};
+
+template <int G, int R, bool MASK, class Ar>
+__global__ void __launch_bounds__(kThreads) dtw_full_kernel(const FillArgs A) {
+  using T = typename Ar::T;
+  constexpr bool kF32 = sizeof(T) == 4;
+  constexpr int GPW = 32 / G;
+  constexpr int W = G * R;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % G;
+  const int gw = lane / G;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double* bnd = A.scratch ? A.scratch + (warp * GPW + gw) * A.scratch_stride : nullptr;
+  const T INF = Ar::inf();
+  const T* S = Ar::base(A);
+
+  for (int64_t base = warp * GPW; base < A.count; base += nwarps * GPW) {
+    const int64_t item = base + gw;
+    const bool valid = item < A.count;
+    const Pair P = load_pair(A, valid ? item : base);
+    const T* X = S + P.xoff;
+    const T* Y = S + P.yoff;
+    const int n = P.n, m = P.m, hw = P.hw;
+    const int npass_g = (m + W - 1) / W;
+    const int npass = __reduce_max_sync(kFull, npass_g);
+    int written_hi = 0;
+    double result = 0.0;
+
+    for (int pass = 0; pass < npass; ++pass) {
+      const bool pvalid = pass < npass_g;
+      const int c0 = pass * W;
+      int rs = 1, re = n;
+      if (MASK) {
+        rs = max(1, c0 + 1 - hw);
+        re = min(n, c0 + W + hw);
+      }
+      if (!pvalid) re = rs - 1;
+      const int my_steps = pvalid ? ((re - rs + 2) >> 1) + G - 1 : 0;
+      const int nsteps = __reduce_max_sync(kFull, my_steps);
+      const int jl = c0 + gl * R + 1;  // 1-based first column of this lane
+      T yv[R], pv[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        yv[r] = (jl + r <= m) ? __ldg(Y + jl + r - 1) : T(0);
+        pv[r] = INF;
+      }
+      T diag0 = INF;  // cell (r0-1, jl-1)
+      if (gl == 0) {
+        if (pass == 0) diag0 = (rs == 1) ? T(0) : INF;
+        else if (rs - 1 >= 1 && rs - 1 <= written_hi) diag0 = (T)bnd[rs - 1];
+      }
+      double off = 0.0;  // fp32: this lane's offset
+      T send0 = INF, send1 = INF;
+      double send_off = 0.0;
+      const bool last_pass = pass == npass_g - 1;
+      const bool hold = pvalid && last_pass && ((m - 1 - c0) / R) == gl;
+      const int r_res = hold ? (m - 1 - c0) % R : -1;
+      const bool wb = pvalid && !last_pass && gl == G - 1;
+      const bool use_bnd = gl == 0 && pass > 0;
+
+      int r0 = rs - 2 * gl;  // this lane's first row at step 0
+      const int xmax = n - 1;
+      T xa = __ldg(X + min(max(r0 - 1, 0), xmax));
+      T xb = __ldg(X + min(max(r0, 0), xmax));
+      double ba = Ar::inf(), bb = Ar::inf();
+      if (use_bnd) {
+        if (r0 <= written_hi) ba = bnd[r0];
+        if (r0 + 1 <= written_hi) bb = bnd[r0 + 1];
+      }
+
+      for (int s = 0; s < nsteps; ++s, r0 += 2) {
+        const T x0 = xa, x1 = xb;
+        const double b0 = ba, b1 = bb;
+        xa = __ldg(X + min(max(r0 + 1, 0), xmax));
+        xb = __ldg(X + min(max(r0 + 2, 0), xmax));
+        if (use_bnd) {
+          ba = (r0 + 2 <= written_hi) ? bnd[r0 + 2] : (double)Ar::inf();
+          bb = (r0 + 3 <= written_hi) ? bnd[r0 + 3] : (double)Ar::inf();
+        }
+        T L0 = __shfl_up_sync(kFull, send0, 1, G);
+        T L1 = __shfl_up_sync(kFull, send1, 1, G);
+        if constexpr (kF32) {
+          const double loff = __shfl_up_sync(kFull, send_off, 1, G);
+          if (gl == 0) {
+            L0 = (b0 == (double)INF) ? INF : (T)(b0 - off);
+            L1 = (b1 == (double)INF) ? INF : (T)(b1 - off);
+          } else {
+            L0 = rebase(L0, loff, off);
+            L1 = rebase(L1, loff, off);
+          }
+        } else {
+          if (gl == 0) {
+            L0 = (T)b0;
+            L1 = (T)b1;
+          }
+        }
+        const bool work = s >= gl && r0 <= re;
+        bool fast = true;
+        if (MASK) {
+          // Rows r0, r0+1 entirely inside |i-j| <= hw for every working lane of the warp?
+          const bool in = (jl >= r0 + 1 - hw) && (jl + R - 1 <= r0 + hw);
+          fast = __all_sync(kFull, in || !work);
+        }
+        if (work) {
+          T aout, bout;
+          const bool two = r0 + 1 <= re;
+          if (two) {
+            if (!MASK || fast)
+              FullRows<R, false, Ar>::two(pv, yv, x0, x1, diag0, L0, L1, jl, r0, hw, aout, bout);
+            else
+              FullRows<R, MASK, Ar>::two(pv, yv, x0, x1, diag0, L0, L1, jl, r0, hw, aout, bout);
+            diag0 = L1;
+          } else {
+            if (!MASK || fast)
+              FullRows<R, false, Ar>::one(pv, yv, x0, diag0, L0, jl, r0, hw, aout);
+            else
+              FullRows<R, MASK, Ar>::one(pv, yv, x0, diag0, L0, jl, r0, hw, aout);
+            bout = aout;
+            diag0 = L0;
+          }
+          if constexpr (kF32) {
+            if ((s & (kRenormSteps - 1)) == kRenormSteps - 1) {
+              T mnv = pv[0];
+#pragma unroll
+              for (int r = 1; r < R; ++r) mnv = Ar::mn(mnv, pv[r]);
+              if (mnv != INF) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) pv[r] = __fsub_rn(pv[r], mnv);
+                diag0 = (diag0 == INF) ? INF : __fsub_rn(diag0, mnv);
+                // aout/bout were produced before the shift: re-base them too
+                aout = (aout == INF) ? INF : __fsub_rn(aout, mnv);
+                bout = (bout == INF) ? INF : __fsub_rn(bout, mnv);
+                off += (double)mnv;
+              }
+            }
+            send_off = off;
+          }
+          send0 = aout;
+          send1 = bout;
+          if (wb) {
+            if constexpr (kF32) {
+              bnd[r0] = (aout == INF) ? (double)INF : (double)aout + off;
+              if (two) bnd[r0 + 1] = (bout == INF) ? (double)INF : (double)bout + off;
+            } else {
+              bnd[r0] = aout;
+              if (two) bnd[r0 + 1] = bout;
+            }
+          }
+          // Row n is always the last row this lane writes into pv (re <= n, so a step
+          // with r0 == n is a single-row step).
+          if (hold && (r0 == n || (two && r0 + 1 == n))) {
+            T rv = pv[0];
+#pragma unroll
+            for (int r = 1; r < R; ++r) rv = (r == r_res) ? pv[r] : rv;
+            result = (double)rv + (kF32 ? off : 0.0);
+          }
+        }
+      }
+      written_hi = re;
+      __syncwarp();
+    }
+    const int last_c0 = (npass_g - 1) * W;
+    if (valid && ((m - 1 - last_c0) / R) == gl) A.out[P.slot - A.out_base] = result;
+  }
+}
+
+// ===================================================================================
+// Band family: sheared band coordinates, one group covers the whole band.
+// ===================================================================================
+// pv[rK] = inf for a uniform runtime rK: one jump-table branch instead of R selects.
+template <int R, class T>
+__device__ __forceinline__ void kill_cell(T (&pv)[R], int rK, T inf) {
+  switch (rK) {
+#define DTWG_KILL(c) \
+  case c:            \
+    if constexpr (c < R) pv[c] = inf; \
+    break;
+    DTWG_KILL(1) DTWG_KILL(2) DTWG_KILL(3) DTWG_KILL(4) DTWG_KILL(5) DTWG_KILL(6) DTWG_KILL(7)
+    DTWG_KILL(8) DTWG_KILL(9) DTWG_KILL(10) DTWG_KILL(11) DTWG_KILL(12) DTWG_KILL(13)
+    DTWG_KILL(14) DTWG_KILL(15)
+#undef DTWG_KILL
+    default:
+      break;
+  }
+}
+
+template <class Ar>
+__device__ __forceinline__ typename Ar::T band_y(const typename Ar::T* Y, int m, int j) {
+  return (j >= 1 && j <= m) ? __ldg(Y + j - 1) : Ar::inf();
+}
+
+// KR >= 0: K % R known at compile time (static kill position); KR < 0: runtime switch.
+template <int G, int R, int KR, class Ar>
+__global__ void __launch_bounds__(kThreads) dtw_band_kernel(const FillArgs A) {
+  static_assert(R >= 2, "band family needs R >= 2");
+  using T = typename Ar::T;
+  constexpr bool kF32 = sizeof(T) == 4;
+  constexpr int GPW = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % G;
+  const int gw = lane / G;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const T INF = Ar::inf();
+  const T* S = Ar::base(A);
+
+  for (int64_t base = warp * GPW; base < A.count; base += nwarps * GPW) {
+    const int64_t item = base + gw;
+    const bool valid = item < A.count;
+    const Pair P = load_pair(A, valid ? item : base);
+    const T* X = S + P.xoff;
+    const T* Y = S + P.yoff;
+    const int n = P.n, m = P.m, hw = P.hw;
+    const int K = 2 * hw + 1;          // band width; k = j - i + hw in [0, K)
+    const int lK = K / R;              // lane holding k == K (first cell right of band)
+    const int rK = KR >= 0 ? KR : K % R;
+    const bool kill_lane = lK == gl;
+    const bool kill0 = kill_lane && rK == 0;
+    const bool killr = kill_lane && rK != 0;
+    const int kres = m - n + hw;       // k of cell (n, m)
+    const bool hold = valid && (kres / R) == gl;
+    const int r_res = kres % R;
+    const int kbase = gl * R;
+
+    T pv[R], yb[R];
+    double off = 0.0;  // fp32 offset of this lane
+#pragma unroll
+    for (int r = 0; r < R; ++r) pv[r] = (kbase + r == hw) ? T(0) : INF;  // row 0: cell (0,0) = 0
+    // y window before step 0 is that of row -gl: yb[r] = y(-gl + kbase + r - hw).
+#pragma unroll
+    for (int r = 0; r < R; ++r) yb[r] = band_y<Ar>(Y, m, -gl + kbase + r - hw);
+
+    T send = INF;
+    double send_off = 0.0;
+    double result = 0.0;
+    const int nsteps = __reduce_max_sync(kFull, n + G - 1);
+    const bool last = gl == G - 1;
+    int i1 = 1 - gl;  // this lane's row at step 0
+    const int xmax = n - 1;
+    const int jfetch = G * R - 1 - hw;  // last lane's new y index = i1 + jfetch
+    T xq = __ldg(X + min(max(i1 - 1, 0), xmax));
+    T yq = last ? band_y<Ar>(Y, m, i1 + jfetch) : T(0);
+
+    for (int s0 = 0; s0 < nsteps; s0 += R) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) {  // phase q: logical y[r] lives in yb[(r + q) % R]
+        if (s0 + q < nsteps) {
+          const T x = xq;
+          const T yf = yq;
+          xq = __ldg(X + min(max(i1, 0), xmax));
+          if (last) yq = band_y<Ar>(Y, m, i1 + 1 + jfetch);
+
+          // Slide the y window by one: the new last sample is lane l+1's logical y[1]
+          // before its own slide (= y(i + lR + R - 1 - hw)); the last lane loads it.
+          const T ynb = __shfl_down_sync(kFull, yb[(1 + q) % R], 1, G);
+          yb[q % R] = last ? yf : ynb;  // physical slot of the dropped logical y[0]
+          // From here on logical y[r] = yb[(r + q + 1) % R].
+
+          T L = __shfl_up_sync(kFull, send, 1, G);
+          double loff = 0.0, uoff = 0.0;
+          if constexpr (kF32) {
+            loff = __shfl_up_sync(kFull, send_off, 1, G);
+            uoff = __shfl_down_sync(kFull, off, 1, G);
+            L = rebase(L, loff, off);
+          }
+          if (gl == 0) L = INF;  // k = -1 is outside the band
+          // Rows 1..n only: before its first row a lane keeps the row-0 state; after
+          // row n it keeps row n (the result is read from pv after the loop).
+          const bool started = i1 >= 1 && i1 <= n;
+
+          // First cell of the strip (k = lR): needs only own previous row + L.
+          T v0 = Ar::cell(x, yb[(q + 1) % R], Ar::mn(Ar::mn(pv[0], pv[1]), L));
+          v0 = started ? v0 : pv[0];
+          if (kill0) v0 = INF;  // k == K is this lane's first cell
+          // Up neighbour of the strip's last cell = lane l+1's first cell, previous row.
+          T U = __shfl_down_sync(kFull, v0, 1, G);
+          if constexpr (kF32) U = rebase(U, uoff, off);
+          if (last) U = INF;
+          if (started) {
+            T left = v0;
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+              const T up = (r < R - 1) ? pv[r + 1] : U;
+              const T v = Ar::cell(x, yb[(r + q + 1) % R], Ar::mn(Ar::mn(pv[r], up), left));
+              pv[r] = v;
+              left = v;
+            }
+            pv[0] = v0;
+            // Cell k == K lies right of the band: keep it at +inf (dtw.hpp:71). Cells
+            // beyond it may hold garbage; only cell K feeds a valid cell (as "up").
+            if constexpr (KR > 0) {
+              if (kill_lane) pv[KR] = INF;
+            } else if constexpr (KR < 0) {
+              if (killr) kill_cell<R>(pv, rK, INF);
+            }
+            if constexpr (kF32) {
+              if (((i1 - 1) & (kRenormSteps - 1)) == kRenormSteps - 1) {
+                T mnv = pv[0];
+#pragma unroll
+                for (int r = 1; r < R; ++r) mnv = Ar::mn(mnv, pv[r]);
+                if (mnv != INF) {
+#pragma unroll
+                  for (int r = 0; r < R; ++r) pv[r] = __fsub_rn(pv[r], mnv);
+                  off += (double)mnv;
+                }
+              }
+              send_off = off;
+            }
+            send = pv[R - 1];
+          }
+          ++i1;
+        }
+      }
+    }
+    if (hold) {
+      T rv = pv[0];
+#pragma unroll
+      for (int r = 1; r < R; ++r) rv = (r == r_res) ? pv[r] : rv;
+      result = (double)rv + (kF32 ? off : 0.0);
+      A.out[P.slot - A.out_base] = result;
+    }
+  }
+}
+
+}  // namespace kern
+}  // namespace dtwgpu

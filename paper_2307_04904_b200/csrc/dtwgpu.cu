@@ -105,18 +105,26 @@ int64_t pair_cells(int64_t n, int64_t m, int64_t hw) {
 }
 
 // ---- planner ------------------------------------------------------------------------
+// Candidate instantiations with their measured throughput in computed lane-cells per
+// ns on one B200 (tools/sweep.py, profiles/round1_sweep.md): the cost of a shape is
+// the lane-cells a configuration computes (band waste, wavefront fill/drain, padding
+// columns, masked rows all included) divided by that rate. Multi-pass Full fills with
+// few lanes pay an extra per-pass boundary-column cost (measured on c4).
 struct Cand {
   int G, R;
+  double rate;  // computed lane-cells / ns
 };
-const Cand kFull[] = {{2, 23}, {4, 12}, {8, 8}, {16, 8}, {16, 16},
-                      {32, 4}, {32, 8}, {32, 12}, {32, 15}, {32, 16}};
-const Cand kBand[] = {{16, 7}, {16, 9}, {16, 11}, {16, 13}, {32, 3},
-                      {32, 5}, {32, 7}, {32, 9},  {32, 13}};
+const Cand kFull[] = {{2, 23, 1845}, {4, 12, 1846}, {8, 8, 1714},   {16, 8, 1700},
+                      {16, 16, 2020}, {32, 4, 1300}, {32, 8, 1750}, {32, 12, 1900},
+                      {32, 15, 2165}, {32, 16, 2170}};
+const Cand kBand[] = {{16, 7, 1500}, {16, 9, 1600}, {16, 11, 1700}, {16, 13, 1800},
+                      {32, 3, 1000}, {32, 5, 1250}, {32, 7, 1490}, {32, 9, 1500},
+                      {32, 13, 1450}};
 
-double full_cost(const Shape& s, int G, int R, bool mask) {
-  const int64_t W = (int64_t)G * R;
+double full_cost(const Shape& s, const Cand& c, bool mask) {
+  const int64_t W = (int64_t)c.G * c.R;
   const int64_t npass = (s.m + W - 1) / W;
-  double steps = 0;
+  double cells = 0;
   for (int64_t p = 0; p < npass; ++p) {
     const int64_t c0 = p * W;
     int64_t rs = 1, re = s.n;
@@ -124,14 +132,17 @@ double full_cost(const Shape& s, int G, int R, bool mask) {
       rs = std::max<int64_t>(1, c0 + 1 - s.hw);
       re = std::min<int64_t>(s.n, c0 + W + s.hw);
     }
-    steps += double(re - rs + 1 + G - 1);
+    // two rows per step, G-1 steps of wavefront fill/drain
+    cells += double(((re - rs + 2) / 2) * 2 + 2 * (c.G - 1)) * double(W);
   }
-  const double per_pair = G * (4.0 * R + 60.0);
-  return steps * G * (9.0 * R + 12.0 + (mask ? 4.0 : 0.0)) + per_pair;
+  double rate = c.rate;
+  if (mask) rate *= 0.75;                       // masked steps (measured on c2 / c5)
+  if (npass > 1 && c.G <= 4) rate *= 0.55;      // boundary column round trips
+  return cells / rate;
 }
 
-double band_cost(const Shape& s, int G, int R) {
-  return double(s.n + G - 1) * G * (9.0 * R + 24.0) + G * (4.0 * R + 60.0);
+double band_cost(const Shape& s, const Cand& c) {
+  return double(s.n + c.G - 1) * double(c.G * c.R) / c.rate;
 }
 
 KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out);
@@ -144,7 +155,7 @@ KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out) {
   double bc = 1e300;
   const bool mask = s.hw < s.n - 1;  // a band that excludes some cell
   for (const Cand& c : kFull) {
-    const double cst = full_cost(s, c.G, c.R, mask);
+    const double cst = full_cost(s, c, mask);
     if (cst < bc) {
       bc = cst;
       best = KernelCfg{Family::Full, c.G, c.R, mask, fp32};
@@ -154,10 +165,10 @@ KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out) {
     const int64_t K = 2 * s.hw + 1;
     for (const Cand& c : kBand) {
       if ((int64_t)c.G * c.R < K) continue;
-      const double cst = band_cost(s, c.G, c.R);
+      const double cst = band_cost(s, c);
       if (cst < bc) {
         bc = cst;
-        best = KernelCfg{Family::Band, c.G, c.R, false, fp32};
+        best = KernelCfg{Family::Band, c.G, c.R, false, fp32, fp32 ? -1 : (int)(K % c.R)};
       }
     }
   }
@@ -235,7 +246,10 @@ KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cos
   const bool mask = s.hw < s.n - 1;
   if (ctx->force_family >= 0) {
     KernelCfg f{(Family)ctx->force_family, ctx->force_G, ctx->force_R,
-                ctx->force_family == 0 ? mask : false, fp32};
+                ctx->force_family == 0 ? mask : false, fp32,
+                (ctx->force_family == 1 && !fp32 && ctx->force_R > 0)
+                    ? (int)((2 * s.hw + 1) % ctx->force_R)
+                    : -1};
     const bool ok = dtwgpu::fill_cfg_supported(f) &&
                     (f.family == Family::Full ||
                      (mask && f.R >= 2 && (int64_t)f.G * f.R >= 2 * s.hw + 1));
@@ -316,7 +330,7 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
     return plan;
   }
   std::map<Shape, int> cls_of_shape;
-  std::map<std::tuple<int, int, int, bool>, int> cls_of_cfg;
+  std::map<std::tuple<int, int, int, bool, int>, int> cls_of_cfg;
   std::vector<std::vector<std::pair<double, int64_t>>> items;
   int64_t i = 0;
   // decode sb
@@ -337,7 +351,7 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
     if (it == cls_of_shape.end()) {
       double cst = 0;
       const KernelCfg cfg = choose_cfg(ctx, s, fp32, &cst);
-      const auto key = std::make_tuple((int)cfg.family, cfg.G, cfg.R, cfg.mask);
+      const auto key = std::make_tuple((int)cfg.family, cfg.G, cfg.R, cfg.mask, cfg.kr);
       auto ic = cls_of_cfg.find(key);
       if (ic == cls_of_cfg.end()) {
         PlanClass pc;
@@ -447,10 +461,12 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
     CU(dtwgpu::launch_fill(pc.cfg, a, (int)blocks, ctx->stream), "fill launch");
     ctx->launches++;
     char buf[160];
-    snprintf(buf, sizeof(buf), "%s%s[G=%d,R=%d%s%s] pairs=%lld blocks=%lld(%d/SM)",
+    char krs[16] = "";
+    if (pc.cfg.family == Family::Band && pc.cfg.kr >= 0) snprintf(krs, sizeof(krs), ",kr=%d", pc.cfg.kr);
+    snprintf(buf, sizeof(buf), "%s%s[G=%d,R=%d%s%s%s] pairs=%lld blocks=%lld(%d/SM)",
              ctx->last_plan.empty() ? "" : "; ", family_name(pc.cfg.family), pc.cfg.G, pc.cfg.R,
-             pc.cfg.mask ? ",mask" : "", fp32 ? ",fp32" : "", (long long)count, (long long)blocks,
-             bps);
+             pc.cfg.mask ? ",mask" : "", fp32 ? ",fp32" : "", krs, (long long)count,
+             (long long)blocks, bps);
     ctx->last_plan += buf;
     pos += pc.slots.size();
   }
@@ -857,6 +873,14 @@ int dtwg_count_cells(dtwg_ctx* ctx, int64_t half_width, int auto_widen, int64_t 
 int dtwg_last_fill_ms(dtwg_ctx* ctx, float* ms) {
   if (!ctx || !ms) return DTWG_INVALID_ARGUMENTS;
   *ms = ctx->last_fill_ms;
+  return DTWG_OK;
+}
+
+int dtwg_measure_cell_peak(dtwg_ctx* ctx, int precision, double* cells_per_s) {
+  if (!ctx || !cells_per_s) return DTWG_INVALID_ARGUMENTS;
+  cudaSetDevice(ctx->device);
+  CU(dtwgpu::measure_cell_peak(ctx->stream, ctx->num_sms, precision == DTWG_FP32, cells_per_s),
+     "cell peak");
   return DTWG_OK;
 }
 

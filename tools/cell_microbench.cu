@@ -76,8 +76,58 @@ void run(const char* name) {
   cudaFree(out);
 }
 
+// Latency of one dependent cell chain (1 warp per SM, 1 chain per thread), in SM clocks.
+template <class T>
+__global__ void chain_lat(const T* in, T* out, int iters, long long* clk) {
+  // The DTW left-chain: v_j = (x - y_j)^2 + min(min(d_j, u_j), v_{j-1}); only v_{j-1}
+  // is loop-carried, as in the fill (d/u come from the previous row).
+  T x = in[threadIdx.x & 7], y = in[1], a = in[2], b = in[3], left = in[4];
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    T d, v;
+    if constexpr (sizeof(T) == 8) {
+      d = __dsub_rn(x, y);
+      const T m1 = b < a ? b : a;
+      const T m2 = left < m1 ? left : m1;
+      v = __dadd_rn(__dmul_rn(d, d), m2);
+    } else {
+      d = __fsub_rn(x, y);
+      v = __fadd_rn(__fmul_rn(d, d), fminf(fminf(a, b), left));
+    }
+    left = v;
+    y = y + (T)1;
+    a = a + (T)1;
+    b = b + (T)2;
+  }
+  const T b_out = left;
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) *clk = t1 - t0;
+  if (b_out == (T)-1) out[0] = b_out;
+}
+
+template <class T>
+void lat(const char* name) {
+  T* in;
+  T* out;
+  long long* clk;
+  cudaMalloc(&in, 64 * sizeof(T));
+  cudaMalloc(&out, 64 * sizeof(T));
+  cudaMalloc(&clk, 8);
+  T h[8] = {1, 2, 3, 4, 5, 6, 7, 8};
+  cudaMemcpy(in, h, sizeof(h), cudaMemcpyHostToDevice);
+  const int iters = 1 << 16;
+  chain_lat<T><<<1, 32>>>(in, out, iters, clk);
+  chain_lat<T><<<1, 32>>>(in, out, iters, clk);
+  long long c = 0;
+  cudaMemcpy(&c, clk, 8, cudaMemcpyDeviceToHost);
+  // the chain here runs through y = v: sub -> mul -> add plus the min chain
+  printf("{\"body\":\"%s\",\"chain_cycles_per_cell\":%.2f}\n", name, (double)c / iters);
+}
+
 int main() {
   run<double>("fp64");
   run<float>("fp32");
+  lat<double>("fp64");
+  lat<float>("fp32");
   return 0;
 }
