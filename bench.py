@@ -326,7 +326,7 @@ def run_gpu_arm(a, ds):
             if prec == 0 else None,
             "roofline": {"bound": "fp64" if prec == 0 else "fp32",
                          "achieved": achieved, "peak": peak,
-                         "unit": "GCUPS (cell updates/s; 5 fp64-pipe ops per cell)",
+                         "unit": "GCUPS (cell updates/s; fp64 cell = 5 fp64-pipe ops, fp32 cell = FADD FMUL FMNMX3 FADD)",
                          "frac": (achieved / peak) if achieved else None,
                          "traffic": traffic,
                          "peak_source": "measured live: dtwg_measure_cell_peak (cell body, "

@@ -1,0 +1,172 @@
+// dtwclust_gpu.hpp -- C++ drop-in for the reference's hot path, on top of include/dtwgpu.h.
+//
+// Include it after the reference's own headers (it uses dtwclust's types, unchanged) and
+// replace
+//     dtwclust::build_matrix(dataset, window, workers, &stats, auto_widen)   // pairwise.hpp:62
+//     dtwclust::kmedoids(matrix, config, observer)                           // kmedoids.hpp:148
+// by the same calls in namespace dtwgpu. Signatures, results (bit-identical matrices,
+// identical ClusterResult) and thrown exception types follow the reference; the work runs
+// on the B200 through the C-ABI. Host-side types, data loading, the exact (MIP) solver
+// and the scores keep consuming the returned dtwclust::DistanceMatrix unchanged.
+//
+// Threading: one device context per host thread (thread_local), as the C-ABI requires.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <dtwclust/cluster_result.hpp>
+#include <dtwclust/distance_matrix.hpp>
+#include <dtwclust/errors.hpp>
+#include <dtwclust/kmedoids.hpp>
+#include <dtwclust/pairwise.hpp>
+#include <dtwclust/time_series.hpp>
+#include <dtwclust/warp_window.hpp>
+
+#include "../dtwgpu.h"
+
+namespace dtwgpu {
+
+class DeviceError : public std::runtime_error {
+ public:
+  DeviceError(int code, const std::string& what)
+      : std::runtime_error("dtwgpu [code " + std::to_string(code) + "]: " + what), code_(code) {}
+  int code() const noexcept { return code_; }
+
+ private:
+  int code_;
+};
+
+/// RAII owner of one dtwg_ctx on `device`.
+class Context {
+ public:
+  explicit Context(int device = 0) {
+    const int rc = dtwg_create(device, &ctx_);
+    if (rc != DTWG_OK) throw DeviceError(rc, "no CUDA device available (there is no CPU fallback)");
+  }
+  ~Context() { dtwg_destroy(ctx_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  dtwg_ctx* get() const noexcept { return ctx_; }
+
+ private:
+  dtwg_ctx* ctx_ = nullptr;
+};
+
+inline Context& thread_context() {
+  thread_local std::unique_ptr<Context> ctx;
+  if (!ctx) ctx = std::make_unique<Context>(0);
+  return *ctx;
+}
+
+namespace detail {
+
+/// Rethrows a C-ABI error code as the reference's exception class (errors.hpp:11-176).
+[[noreturn]] inline void rethrow(dtwg_ctx* ctx, int rc, const std::vector<dtwclust::TimeSeries>* ds,
+                                 std::int64_t hw) {
+  const std::string msg = dtwg_last_error(ctx);
+  switch (rc) {
+    case DTWG_INVALID_ARGUMENTS:
+      throw dtwclust::InvalidArgumentsError(msg);
+    case DTWG_EMPTY_DATASET:
+      throw dtwclust::EmptyDatasetError();
+    case DTWG_INVALID_SERIES:
+      throw dtwclust::InvalidSeriesError("?", msg);
+    case DTWG_BAND_INFEASIBLE: {
+      std::int64_t i = -1, j = -1;
+      dtwg_last_error_pair(ctx, &i, &j);
+      if (ds && i >= 0 && j >= 0) {
+        const auto& a = (*ds)[static_cast<std::size_t>(i)];
+        const auto& b = (*ds)[static_cast<std::size_t>(j)];
+        throw dtwclust::BandInfeasibleError(
+            static_cast<std::size_t>(i), static_cast<std::size_t>(j),
+            dtwclust::BandInfeasibleError(a.length(), b.length(), static_cast<std::size_t>(hw)));
+      }
+      throw DeviceError(rc, msg);
+    }
+    case DTWG_DISTANCE_MATRIX_INVALID:
+      throw dtwclust::DistanceMatrixInvalidError(msg);
+    default:
+      throw DeviceError(rc, msg);
+  }
+}
+
+}  // namespace detail
+
+/// pairwise.hpp:62-127 on the GPU: same signature, same validation order, bit-identical
+/// condensed matrix (fp64), BuildStats::evaluations = p(p-1)/2.
+inline dtwclust::DistanceMatrix build_matrix(const std::vector<dtwclust::TimeSeries>& dataset,
+                                             const dtwclust::WarpWindow& w, unsigned workers,
+                                             dtwclust::BuildStats* stats = nullptr,
+                                             bool auto_widen = false) {
+  if (dataset.empty()) throw dtwclust::EmptyDatasetError();
+  if (workers == 0) throw dtwclust::InvalidArgumentsError("workers must be >= 1");
+  dtwclust::validate_dataset(dataset);  // the reference's own checks, ids included
+
+  const std::size_t p = dataset.size();
+  std::vector<std::int64_t> offsets(p + 1, 0);
+  for (std::size_t i = 0; i < p; ++i)
+    offsets[i + 1] = offsets[i] + static_cast<std::int64_t>(dataset[i].length());
+  std::vector<double> samples(static_cast<std::size_t>(offsets[p]));
+  for (std::size_t i = 0; i < p; ++i)
+    std::copy(dataset[i].samples.begin(), dataset[i].samples.end(),
+              samples.begin() + offsets[i]);
+
+  const std::int64_t hw = w.is_unlimited() ? -1 : static_cast<std::int64_t>(w.half_width());
+  std::vector<double> values(dtwclust::DistanceMatrix::condensed_size(p));
+  std::uint64_t evaluations = 0;
+  dtwg_ctx* ctx = thread_context().get();
+  const int rc = dtwg_build_matrix(ctx, samples.data(), offsets.data(),
+                                   static_cast<std::int64_t>(p), hw, auto_widen ? 1 : 0, workers,
+                                   DTWG_FP64, values.empty() ? nullptr : values.data(),
+                                   &evaluations);
+  if (rc != DTWG_OK) detail::rethrow(ctx, rc, &dataset, hw);
+  if (stats) stats->evaluations = evaluations;
+  return dtwclust::DistanceMatrix::from_condensed(p, std::move(values));
+}
+
+/// kmedoids.hpp:148-189 over a DistanceMatrix, sweeps on the GPU: identical medoids,
+/// assignment, total_cost and observer trace.
+inline dtwclust::ClusterResult kmedoids(const dtwclust::DistanceMatrix& source,
+                                        const dtwclust::KMedoidsConfig& config,
+                                        const dtwclust::IterationObserver& observer = {}) {
+  const std::size_t p = source.size();
+  if (config.k < 1 || config.k > p) throw dtwclust::KOutOfRangeError(config.k, p);
+  if (config.restarts < 1) throw dtwclust::InvalidArgumentsError("restarts must be >= 1");
+  if (config.max_iterations < 1)
+    throw dtwclust::InvalidArgumentsError("max_iterations must be >= 1");
+  dtwg_ctx* ctx = thread_context().get();
+  const auto& cond = source.condensed();
+  int rc = dtwg_adopt_condensed(ctx, cond.empty() ? nullptr : cond.data(),
+                                static_cast<std::int64_t>(p), 0);
+  if (rc != DTWG_OK) detail::rethrow(ctx, rc, nullptr, 0);
+
+  struct Trampoline {
+    static void call(void* user, std::int64_t r, std::int64_t it, double cost) {
+      (*static_cast<const dtwclust::IterationObserver*>(user))(static_cast<std::size_t>(r),
+                                                               static_cast<std::size_t>(it), cost);
+    }
+  };
+  std::vector<std::int64_t> medoids(config.k), assignment(p);
+  double cost = 0.0;
+  std::int64_t best_restart = -1;
+  rc = dtwg_kmedoids(ctx, static_cast<std::int64_t>(config.k),
+                     static_cast<std::int64_t>(config.restarts),
+                     static_cast<std::int64_t>(config.max_iterations), config.seed, 0,
+                     static_cast<std::int64_t>(config.restarts),
+                     observer ? &Trampoline::call : nullptr,
+                     const_cast<dtwclust::IterationObserver*>(&observer), medoids.data(),
+                     assignment.data(), &cost, &best_restart);
+  if (rc != DTWG_OK) detail::rethrow(ctx, rc, nullptr, 0);
+  dtwclust::ClusterResult result;
+  result.medoids.assign(medoids.begin(), medoids.end());
+  result.assignment.assign(assignment.begin(), assignment.end());
+  result.total_cost = cost;
+  result.certificate = dtwclust::Certificate::LocalHeuristic;
+  return result;
+}
+
+}  // namespace dtwgpu

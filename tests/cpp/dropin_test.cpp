@@ -1,0 +1,133 @@
+// dropin_test.cpp -- framework-free parity test of the C++ drop-in (include/dtwgpu/
+// dtwclust_gpu.hpp) against the unmodified reference, in the style of the reference's
+// acceptance suite (acceptance_main.cpp: Check{name, body}, PASS/FAIL lines, exit code).
+// Built by tests/cpp/Makefile against /root/reference/proj headers + libdtwgpu.so; run
+// on the GPU box by tests/test_gpu_dropin.py.
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include <dtwclust/dtw.hpp>
+#include <dtwclust/kmedoids.hpp>
+#include <dtwclust/pairwise.hpp>
+
+#include "support/synthetic.hpp"
+
+#include <dtwgpu/dtwclust_gpu.hpp>
+
+using namespace dtwclust;
+
+namespace {
+
+struct Check {
+  std::string name;
+  std::function<std::string()> body;
+};
+
+void require(bool ok, const std::string& what) {
+  if (!ok) throw std::runtime_error(what);
+}
+
+std::vector<TimeSeries> walks(std::uint64_t seed, std::size_t p, std::size_t lo, std::size_t hi) {
+  SplitMix64 rng(seed);
+  std::vector<TimeSeries> ds;
+  for (std::size_t i = 0; i < p; ++i) {
+    const std::size_t len = lo + rng.next_below(hi - lo + 1);
+    ds.push_back(testing::random_walk_series(rng, len, "s" + std::to_string(i)));
+  }
+  return ds;
+}
+
+std::string same_matrix(const std::vector<TimeSeries>& ds, const WarpWindow& w, bool widen) {
+  BuildStats a, b;
+  const DistanceMatrix ref = dtwclust::build_matrix(ds, w, 4, &a, widen);
+  const DistanceMatrix gpu = dtwgpu::build_matrix(ds, w, 4, &b, widen);
+  require(ref.condensed() == gpu.condensed(), "condensed matrices differ");
+  require(a.evaluations == b.evaluations, "evaluation counts differ");
+  return std::to_string(ds.size()) + " series, " + std::to_string(ref.condensed().size()) +
+         " pairs bit-identical";
+}
+
+}  // namespace
+
+int main() {
+  std::vector<Check> checks = {
+      {"matrix: unlimited window, ragged lengths",
+       [] { return same_matrix(walks(1, 60, 20, 300), WarpWindow::unlimited(), false); }},
+      {"matrix: banded window, equal lengths",
+       [] { return same_matrix(walks(2, 40, 500, 500), WarpWindow::banded(50), false); }},
+      {"matrix: auto-widen, ragged lengths",
+       [] { return same_matrix(walks(3, 50, 50, 700), WarpWindow::banded(30), true); }},
+      {"matrix: short series (many pairs)",
+       [] { return same_matrix(walks(4, 300, 30, 46), WarpWindow::unlimited(), false); }},
+      {"errors: first band-infeasible pair",
+       [] {
+         const std::vector<TimeSeries> ds = {testing::make_series("a", {1, 2}),
+                                             testing::make_series("b", {1, 2, 3}),
+                                             testing::make_series("c", {1, 2, 3, 4, 5, 6})};
+         try {
+           dtwgpu::build_matrix(ds, WarpWindow::banded(1), 1);
+         } catch (const BandInfeasibleError& e) {
+           require(e.has_pair() && e.pair_i() == 0 && e.pair_j() == 2, "wrong pair");
+           return std::string("BandInfeasibleError at (0, 2)");
+         }
+         throw std::runtime_error("no exception");
+       }},
+      {"errors: validation order",
+       [] {
+         int hits = 0;
+         try { dtwgpu::build_matrix({}, WarpWindow::unlimited(), 1); } catch (const EmptyDatasetError&) { ++hits; }
+         try { dtwgpu::build_matrix({testing::make_series("a", {1})}, WarpWindow::unlimited(), 0); } catch (const InvalidArgumentsError&) { ++hits; }
+         try { dtwgpu::build_matrix({testing::make_series("a", {1}), testing::make_series("a", {2})}, WarpWindow::unlimited(), 1); } catch (const InvalidSeriesError&) { ++hits; }
+         try { dtwgpu::build_matrix({testing::make_series("a", {1}), testing::make_series("b", {})}, WarpWindow::unlimited(), 1); } catch (const InvalidSeriesError&) { ++hits; }
+         require(hits == 4, "expected 4 typed exceptions, got " + std::to_string(hits));
+         return std::string("Empty/InvalidArguments/InvalidSeries x2 as the reference");
+       }},
+      {"kmedoids: identical ClusterResult and observer trace",
+       [] {
+         const auto ds = walks(5, 120, 100, 160);
+         const DistanceMatrix m = dtwclust::build_matrix(ds, WarpWindow::banded(20), 4, nullptr, true);
+         KMedoidsConfig cfg;
+         cfg.k = 6;
+         cfg.restarts = 5;
+         cfg.seed = 0xDEED;
+         std::vector<double> ta, tb;
+         const ClusterResult a = dtwclust::kmedoids(m, cfg, [&](std::size_t, std::size_t, double c) { ta.push_back(c); });
+         const ClusterResult b = dtwgpu::kmedoids(m, cfg, [&](std::size_t, std::size_t, double c) { tb.push_back(c); });
+         require(a == b, "ClusterResult differs");
+         require(ta == tb, "observer traces differ");
+         return "k=6, 5 restarts: medoids, labels, cost bit-identical; " + std::to_string(ta.size()) + " sweeps";
+       }},
+      {"kmedoids: k == p and invalid configs",
+       [] {
+         SplitMix64 rng(1);
+         const DistanceMatrix d = testing::random_distance_matrix(rng, 6);
+         KMedoidsConfig cfg;
+         cfg.k = 6;
+         cfg.restarts = 2;
+         require(dtwgpu::kmedoids(d, cfg) == dtwclust::kmedoids(d, cfg), "k == p differs");
+         int hits = 0;
+         cfg.k = 7;
+         try { dtwgpu::kmedoids(d, cfg); } catch (const KOutOfRangeError&) { ++hits; }
+         cfg.k = 2;
+         cfg.restarts = 0;
+         try { dtwgpu::kmedoids(d, cfg); } catch (const InvalidArgumentsError&) { ++hits; }
+         require(hits == 2, "typed exceptions missing");
+         return std::string("k == p equal; KOutOfRange, InvalidArguments thrown");
+       }},
+  };
+  int failed = 0;
+  for (const auto& c : checks) {
+    try {
+      const std::string detail = c.body();
+      std::printf("PASS  %s -- %s\n", c.name.c_str(), detail.c_str());
+    } catch (const std::exception& e) {
+      ++failed;
+      std::printf("FAIL  %s -- %s\n", c.name.c_str(), e.what());
+    }
+  }
+  std::printf("%zu/%zu passed\n", checks.size() - failed, checks.size());
+  return failed ? 1 : 0;
+}
