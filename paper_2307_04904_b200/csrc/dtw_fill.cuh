@@ -22,7 +22,14 @@ struct FillArgs {
   double* out;
   double* scratch;         // boundary columns for multi-pass fills (one per group)
   int64_t scratch_stride;  // doubles per group
+  // Band family: the same series, each surrounded by kBandPad +inf samples, so band
+  // columns outside [1, m] (and rows outside [1, n]) load +inf without a range check.
+  const double* bsamples;
+  const float* bsamples32;
+  const int64_t* boffsets;  // start of series i inside bsamples
 };
+
+constexpr int kBandPad = 512;  // >= hw + G + G*R for every band instantiation
 
 enum class Family : int { Full = 0, Band = 1 };
 
@@ -35,6 +42,7 @@ struct KernelCfg {
   bool mask;
   bool fp32;
   int kr = -1;  // Band family: (2hw+1) % R when every pair of the launch shares it, else -1
+  int P = 1;    // Band family: pairs per lane group (independent chains per lane)
 };
 
 // Launches cfg over args on stream with `blocks` CTAs of kThreads threads.

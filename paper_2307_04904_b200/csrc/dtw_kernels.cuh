@@ -77,6 +77,7 @@ struct F64 {
     return __dadd_rn(__dmul_rn(d, d), best);
   }
   static __device__ __forceinline__ const T* base(const FillArgs& A) { return A.samples; }
+  static __device__ __forceinline__ const T* bbase(const FillArgs& A) { return A.bsamples; }
 };
 
 struct F32 {
@@ -88,6 +89,7 @@ struct F32 {
     return __fadd_rn(__fmul_rn(d, d), best);
   }
   static __device__ __forceinline__ const T* base(const FillArgs& A) { return A.samples32; }
+  static __device__ __forceinline__ const T* bbase(const FillArgs& A) { return A.bsamples32; }
 };
 
 struct Pair {
@@ -231,9 +233,9 @@ __global__ void __launch_bounds__(kThreads) dtw_full_kernel(const FillArgs A) {
       const bool use_bnd = gl == 0 && pass > 0;
 
       int r0 = rs - 2 * gl;  // this lane's first row at step 0
-      const int xmax = n - 1;
-      T xa = __ldg(X + min(max(r0 - 1, 0), xmax));
-      T xb = __ldg(X + min(max(r0, 0), xmax));
+      // Rows outside [1, n] read the zero guard around the packed series (never used).
+      T xa = __ldg(X + (r0 - 1));
+      T xb = __ldg(X + r0);
       double ba = Ar::inf(), bb = Ar::inf();
       if (use_bnd) {
         if (r0 <= written_hi) ba = bnd[r0];
@@ -243,8 +245,8 @@ __global__ void __launch_bounds__(kThreads) dtw_full_kernel(const FillArgs A) {
       for (int s = 0; s < nsteps; ++s, r0 += 2) {
         const T x0 = xa, x1 = xb;
         const double b0 = ba, b1 = bb;
-        xa = __ldg(X + min(max(r0 + 1, 0), xmax));
-        xb = __ldg(X + min(max(r0 + 2, 0), xmax));
+        xa = __ldg(X + (r0 + 1));
+        xb = __ldg(X + (r0 + 2));
         if (use_bnd) {
           ba = (r0 + 2 <= written_hi) ? bnd[r0 + 2] : (double)Ar::inf();
           bb = (r0 + 3 <= written_hi) ? bnd[r0 + 3] : (double)Ar::inf();
@@ -356,13 +358,115 @@ __device__ __forceinline__ void kill_cell(T (&pv)[R], int rK, T inf) {
   }
 }
 
-template <class Ar>
-__device__ __forceinline__ typename Ar::T band_y(const typename Ar::T* Y, int m, int j) {
-  return (j >= 1 && j <= m) ? __ldg(Y + j - 1) : Ar::inf();
+// Band family. KR >= 0: K % R known at compile time (static kill position); KR < 0:
+// runtime switch. P pairs per lane group run interleaved (independent chains, ILP P);
+// pairs of one group share the step counter, so each pair's result is captured when
+// its own last row is reached (shared-memory stash, read after the loop). Series are
+// read from the +inf-padded copy (A.bsamples), so no load needs a range check.
+template <int G, int R, int KR, int P, class Ar, bool FILL>
+__device__ __forceinline__ void band_steps(
+    int s0, int& i1, const typename Ar::T* (&xp)[P], const typename Ar::T* (&yp)[P],
+    typename Ar::T (&xq)[P], typename Ar::T (&yq)[P], typename Ar::T (&pv)[P][R],
+    typename Ar::T (&yb)[P][R], typename Ar::T (&send)[P], double (&send_off)[P],
+    double (&off)[P], const int (&n)[P], const int (&lK)[P], const int (&rK)[P],
+    const bool (&hold)[P], int gl, typename Ar::T (*stash)[P][R], double (*stash_off)[P]) {
+  using T = typename Ar::T;
+  constexpr bool kF32 = sizeof(T) == 4;
+  const T INF = Ar::inf();
+  const bool last = gl == G - 1;
+#pragma unroll
+  for (int q = 0; q < R; ++q) {  // phase q: logical y[r] lives in yb[(r + q) % R]
+    T x[P], v0[P], U[P];
+    // Only the first G-1 steps have lanes that have not reached row 1 yet; they keep
+    // the row-0 state. (Lanes past row n compute +inf/garbage rows: harmless, the
+    // result was stashed at row n.)
+    const bool started = FILL ? (i1 >= 1) : true;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      x[p] = xq[p];
+      const T yf = yq[p];
+      xq[p] = __ldg(++xp[p]);
+      yq[p] = __ldg(++yp[p]);
+      // Slide the y window by one: the new last sample is lane l+1's logical y[1]
+      // before its own slide (= y(i + lR + R - 1 - hw)); the last lane loads it.
+      const T ynb = __shfl_down_sync(kFull, yb[p][(1 + q) % R], 1, G);
+      yb[p][q % R] = last ? yf : ynb;  // physical slot of the dropped logical y[0]
+      // From here on logical y[r] = yb[p][(r + q + 1) % R].
+      T L = __shfl_up_sync(kFull, send[p], 1, G);
+      if constexpr (kF32) {
+        const double loff = __shfl_up_sync(kFull, send_off[p], 1, G);
+        L = rebase(L, loff, off[p]);
+      }
+      if (gl == 0) L = INF;  // k = -1 is outside the band
+      // First cell of the strip (k = lR): needs only own previous row + L.
+      T v = Ar::cell(x[p], yb[p][(q + 1) % R], Ar::mn(Ar::mn(pv[p][0], pv[p][1]), L));
+      if (FILL) v = started ? v : pv[p][0];
+      if (KR == 0 || KR < 0) {
+        if (lK[p] == gl && rK[p] == 0) v = INF;  // k == K is this lane's first cell
+      }
+      v0[p] = v;
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      // Up neighbour of the strip's last cell = lane l+1's first cell, previous row.
+      T u = __shfl_down_sync(kFull, v0[p], 1, G);
+      if constexpr (kF32) {
+        const double uoff = __shfl_down_sync(kFull, off[p], 1, G);
+        u = rebase(u, uoff, off[p]);
+      }
+      U[p] = last ? INF : u;
+    }
+    if (started) {
+      T left[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) left[p] = v0[p];
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const T up = (r < R - 1) ? pv[p][r + 1] : U[p];
+          const T v = Ar::cell(x[p], yb[p][(r + q + 1) % R],
+                               Ar::mn(Ar::mn(pv[p][r], up), left[p]));
+          pv[p][r] = v;
+          left[p] = v;
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        pv[p][0] = v0[p];
+        // Cell k == K lies right of the band: keep it at +inf (dtw.hpp:71). Cells
+        // beyond it may hold garbage; only cell K feeds a valid cell (as "up").
+        if constexpr (KR > 0) {
+          if (lK[p] == gl) pv[p][KR] = INF;
+        } else if constexpr (KR < 0) {
+          if (lK[p] == gl && rK[p] != 0) kill_cell<R>(pv[p], rK[p], INF);
+        }
+        if constexpr (kF32) {
+          if (((i1 - 1) & (kRenormSteps - 1)) == kRenormSteps - 1) {
+            T mnv = pv[p][0];
+#pragma unroll
+            for (int r = 1; r < R; ++r) mnv = Ar::mn(mnv, pv[p][r]);
+            if (mnv != INF) {
+#pragma unroll
+              for (int r = 0; r < R; ++r) pv[p][r] = __fsub_rn(pv[p][r], mnv);
+              off[p] += (double)mnv;
+            }
+          }
+          send_off[p] = off[p];
+        }
+        send[p] = pv[p][R - 1];
+        if (hold[p] && i1 == n[p]) {  // the pair's last row: stash its strip
+#pragma unroll
+          for (int r = 0; r < R; ++r) stash[threadIdx.x][p][r] = pv[p][r];
+          if constexpr (kF32) stash_off[threadIdx.x][p] = off[p];
+        }
+      }
+    }
+    ++i1;
+  }
 }
 
-// KR >= 0: K % R known at compile time (static kill position); KR < 0: runtime switch.
-template <int G, int R, int KR, class Ar>
+template <int G, int R, int KR, int P, class Ar>
 __global__ void __launch_bounds__(kThreads) dtw_band_kernel(const FillArgs A) {
   static_assert(R >= 2, "band family needs R >= 2");
   using T = typename Ar::T;
@@ -374,122 +478,82 @@ __global__ void __launch_bounds__(kThreads) dtw_band_kernel(const FillArgs A) {
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const T INF = Ar::inf();
-  const T* S = Ar::base(A);
+  const T* S = Ar::bbase(A);
+  __shared__ T stash[kThreads][P][R];  // pv at the pair's last row (hold lane only)
+  __shared__ double stash_off[kF32 ? kThreads : 1][P];  // fp32: the lane's offset then
 
-  for (int64_t base = warp * GPW; base < A.count; base += nwarps * GPW) {
-    const int64_t item = base + gw;
-    const bool valid = item < A.count;
-    const Pair P = load_pair(A, valid ? item : base);
-    const T* X = S + P.xoff;
-    const T* Y = S + P.yoff;
-    const int n = P.n, m = P.m, hw = P.hw;
-    const int K = 2 * hw + 1;          // band width; k = j - i + hw in [0, K)
-    const int lK = K / R;              // lane holding k == K (first cell right of band)
-    const int rK = KR >= 0 ? KR : K % R;
-    const bool kill_lane = lK == gl;
-    const bool kill0 = kill_lane && rK == 0;
-    const bool killr = kill_lane && rK != 0;
-    const int kres = m - n + hw;       // k of cell (n, m)
-    const bool hold = valid && (kres / R) == gl;
-    const int r_res = kres % R;
-    const int kbase = gl * R;
-
-    T pv[R], yb[R];
-    double off = 0.0;  // fp32 offset of this lane
+  for (int64_t base = warp * GPW * P; base < A.count; base += nwarps * GPW * P) {
+    const T* xp[P];
+    const T* yp[P];
+    const T* Y[P];
+    int n[P], m[P], K[P], lK[P], rK[P], r_res[P];
+    bool hold[P];
+    int64_t slot[P];
+    int nmax = 0;
 #pragma unroll
-    for (int r = 0; r < R; ++r) pv[r] = (kbase + r == hw) ? T(0) : INF;  // row 0: cell (0,0) = 0
-    // y window before step 0 is that of row -gl: yb[r] = y(-gl + kbase + r - hw).
-#pragma unroll
-    for (int r = 0; r < R; ++r) yb[r] = band_y<Ar>(Y, m, -gl + kbase + r - hw);
-
-    T send = INF;
-    double send_off = 0.0;
-    double result = 0.0;
-    const int nsteps = __reduce_max_sync(kFull, n + G - 1);
-    const bool last = gl == G - 1;
-    int i1 = 1 - gl;  // this lane's row at step 0
-    const int xmax = n - 1;
-    const int jfetch = G * R - 1 - hw;  // last lane's new y index = i1 + jfetch
-    T xq = __ldg(X + min(max(i1 - 1, 0), xmax));
-    T yq = last ? band_y<Ar>(Y, m, i1 + jfetch) : T(0);
-
-    for (int s0 = 0; s0 < nsteps; s0 += R) {
-#pragma unroll
-      for (int q = 0; q < R; ++q) {  // phase q: logical y[r] lives in yb[(r + q) % R]
-        if (s0 + q < nsteps) {
-          const T x = xq;
-          const T yf = yq;
-          xq = __ldg(X + min(max(i1, 0), xmax));
-          if (last) yq = band_y<Ar>(Y, m, i1 + 1 + jfetch);
-
-          // Slide the y window by one: the new last sample is lane l+1's logical y[1]
-          // before its own slide (= y(i + lR + R - 1 - hw)); the last lane loads it.
-          const T ynb = __shfl_down_sync(kFull, yb[(1 + q) % R], 1, G);
-          yb[q % R] = last ? yf : ynb;  // physical slot of the dropped logical y[0]
-          // From here on logical y[r] = yb[(r + q + 1) % R].
-
-          T L = __shfl_up_sync(kFull, send, 1, G);
-          double loff = 0.0, uoff = 0.0;
-          if constexpr (kF32) {
-            loff = __shfl_up_sync(kFull, send_off, 1, G);
-            uoff = __shfl_down_sync(kFull, off, 1, G);
-            L = rebase(L, loff, off);
-          }
-          if (gl == 0) L = INF;  // k = -1 is outside the band
-          // Rows 1..n only: before its first row a lane keeps the row-0 state; after
-          // row n it keeps row n (the result is read from pv after the loop).
-          const bool started = i1 >= 1 && i1 <= n;
-
-          // First cell of the strip (k = lR): needs only own previous row + L.
-          T v0 = Ar::cell(x, yb[(q + 1) % R], Ar::mn(Ar::mn(pv[0], pv[1]), L));
-          v0 = started ? v0 : pv[0];
-          if (kill0) v0 = INF;  // k == K is this lane's first cell
-          // Up neighbour of the strip's last cell = lane l+1's first cell, previous row.
-          T U = __shfl_down_sync(kFull, v0, 1, G);
-          if constexpr (kF32) U = rebase(U, uoff, off);
-          if (last) U = INF;
-          if (started) {
-            T left = v0;
-#pragma unroll
-            for (int r = 1; r < R; ++r) {
-              const T up = (r < R - 1) ? pv[r + 1] : U;
-              const T v = Ar::cell(x, yb[(r + q + 1) % R], Ar::mn(Ar::mn(pv[r], up), left));
-              pv[r] = v;
-              left = v;
-            }
-            pv[0] = v0;
-            // Cell k == K lies right of the band: keep it at +inf (dtw.hpp:71). Cells
-            // beyond it may hold garbage; only cell K feeds a valid cell (as "up").
-            if constexpr (KR > 0) {
-              if (kill_lane) pv[KR] = INF;
-            } else if constexpr (KR < 0) {
-              if (killr) kill_cell<R>(pv, rK, INF);
-            }
-            if constexpr (kF32) {
-              if (((i1 - 1) & (kRenormSteps - 1)) == kRenormSteps - 1) {
-                T mnv = pv[0];
-#pragma unroll
-                for (int r = 1; r < R; ++r) mnv = Ar::mn(mnv, pv[r]);
-                if (mnv != INF) {
-#pragma unroll
-                  for (int r = 0; r < R; ++r) pv[r] = __fsub_rn(pv[r], mnv);
-                  off += (double)mnv;
-                }
-              }
-              send_off = off;
-            }
-            send = pv[R - 1];
-          }
-          ++i1;
-        }
-      }
+    for (int p = 0; p < P; ++p) {
+      const int64_t item = base + (int64_t)gw * P + p;
+      const bool valid = item < A.count;
+      const Pair Pp = load_pair(A, valid ? item : base);
+      slot[p] = Pp.slot;
+      // Same pair, addressed in the padded copy (lengths/orientation from load_pair).
+      int64_t a, b;
+      decode_slot(Pp.slot, A.p, a, b);
+      const bool a_rows = (A.offsets[a + 1] - A.offsets[a]) >= (A.offsets[b + 1] - A.offsets[b]);
+      const int64_t xo = A.boffsets[a_rows ? a : b], yo = A.boffsets[a_rows ? b : a];
+      Y[p] = S + yo;
+      xp[p] = S + xo;
+      n[p] = Pp.n;
+      m[p] = Pp.m;
+      K[p] = 2 * Pp.hw + 1;             // band width; k = j - i + hw in [0, K)
+      lK[p] = K[p] / R;                 // lane holding k == K (first cell right of band)
+      rK[p] = KR >= 0 ? KR : K[p] % R;
+      const int kres = m[p] - n[p] + Pp.hw;  // k of cell (n, m)
+      hold[p] = valid && (kres / R) == gl;
+      r_res[p] = kres % R;
+      nmax = max(nmax, n[p]);
     }
-    if (hold) {
-      T rv = pv[0];
+    const int kbase = gl * R;
+    T pv[P][R], yb[P][R];
+    double off[P], send_off[P];
+    T send[P], xq[P], yq[P];
+    int i1 = 1 - gl;  // this lane's row at step 0 (all pairs of the group)
 #pragma unroll
-      for (int r = 1; r < R; ++r) rv = (r == r_res) ? pv[r] : rv;
-      result = (double)rv + (kF32 ? off : 0.0);
-      A.out[P.slot - A.out_base] = result;
+    for (int p = 0; p < P; ++p) {
+      off[p] = 0.0;
+      send_off[p] = 0.0;
+      send[p] = INF;
+      const int hw = (K[p] - 1) / 2;
+#pragma unroll
+      for (int r = 0; r < R; ++r) pv[p][r] = (kbase + r == hw) ? T(0) : INF;  // row 0
+      // y window before step 0 is that of row -gl: yb[r] = y(-gl + kbase + r - hw).
+#pragma unroll
+      for (int r = 0; r < R; ++r) yb[p][r] = __ldg(Y[p] + (-gl + kbase + r - hw - 1));
+      // Streaming pointers: this lane's x (row i1 - 1, 0-based) and the last lane's
+      // next y (index i1 + G*R - 1 - hw), both one step ahead.
+      xp[p] += i1 - 1;
+      xq[p] = __ldg(xp[p]);
+      yp[p] = Y[p] + (i1 + G * R - 1 - hw - 1);
+      yq[p] = __ldg(yp[p]);
+    }
+    // Steps padded to a multiple of R: surplus steps compute rows past n (harmless).
+    const int nsteps = __reduce_max_sync(kFull, nmax + G - 1);
+    const int fill_end = ((G - 1 + R - 1) / R) * R;  // steps with not-yet-started lanes
+    for (int s0 = 0; s0 < nsteps; s0 += R) {
+      if (s0 < fill_end)
+        band_steps<G, R, KR, P, Ar, true>(s0, i1, xp, yp, xq, yq, pv, yb, send, send_off, off,
+                                          n, lK, rK, hold, gl, stash, stash_off);
+      else
+        band_steps<G, R, KR, P, Ar, false>(s0, i1, xp, yp, xq, yq, pv, yb, send, send_off, off,
+                                           n, lK, rK, hold, gl, stash, stash_off);
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      if (hold[p]) {
+        double result = (double)stash[threadIdx.x][p][r_res[p]];
+        if constexpr (kF32) result += stash_off[threadIdx.x][p];
+        A.out[slot[p] - A.out_base] = result;
+      }
     }
   }
 }

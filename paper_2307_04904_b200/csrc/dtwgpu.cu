@@ -35,6 +35,10 @@ using dtwgpu::KernelCfg;
 namespace {
 
 constexpr double kInf = std::numeric_limits<double>::infinity();
+// Zero-filled guard elements before and after the packed series: wavefront lanes that
+// run past a series' ends (rows < 1 or > n, band columns outside [1, m]) read valid
+// memory and never branch; their cells are masked or unused (dtw_kernels.cuh).
+constexpr int64_t kGuard = 4096;
 
 template <class T>
 struct DevBuf {
@@ -113,13 +117,14 @@ int64_t pair_cells(int64_t n, int64_t m, int64_t hw) {
 struct Cand {
   int G, R;
   double rate;  // computed lane-cells / ns
+  int P = 1;    // band family: pairs per lane group
 };
 const Cand kFull[] = {{2, 23, 1845}, {4, 12, 1846}, {8, 8, 1714},   {16, 8, 1700},
                       {16, 16, 2020}, {32, 4, 1300}, {32, 8, 1750}, {32, 12, 1900},
                       {32, 15, 2165}, {32, 16, 2170}};
-const Cand kBand[] = {{16, 7, 1500}, {16, 9, 1600}, {16, 11, 1700}, {16, 13, 1800},
-                      {32, 3, 1000}, {32, 5, 1250}, {32, 7, 1490}, {32, 9, 1500},
-                      {32, 13, 1450}};
+const Cand kBand[] = {{16, 7, 1500},    {16, 9, 1600},    {16, 11, 1700},  {16, 13, 1800},
+                      {32, 3, 1000},    {32, 5, 1250},    {32, 7, 1490},   {32, 9, 1500},
+                      {32, 13, 1450},   {32, 3, 1000, 2}, {32, 5, 1200, 2}, {32, 7, 1550, 2}};
 
 double full_cost(const Shape& s, const Cand& c, bool mask) {
   const int64_t W = (int64_t)c.G * c.R;
@@ -168,7 +173,7 @@ KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out) {
       const double cst = band_cost(s, c);
       if (cst < bc) {
         bc = cst;
-        best = KernelCfg{Family::Band, c.G, c.R, false, fp32, fp32 ? -1 : (int)(K % c.R)};
+        best = KernelCfg{Family::Band, c.G, c.R, false, fp32, fp32 ? -1 : (int)(K % c.R), c.P};
       }
     }
   }
@@ -205,6 +210,11 @@ struct dtwg_ctx {
   DevBuf<int64_t> d_offsets;
   DevBuf<double> d_scratch;
   DevBuf<int64_t> d_list;
+  // +inf-padded copies of the series for the band family (kBandPad each side)
+  DevBuf<double> d_bsamples;
+  DevBuf<float> d_bsamples32;
+  DevBuf<int64_t> d_boffsets;
+  bool have_band64 = false, have_band32 = false;
 
   // resident matrix
   int64_t mat_p = 0;
@@ -245,11 +255,11 @@ namespace {
 KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cost_out) {
   const bool mask = s.hw < s.n - 1;
   if (ctx->force_family >= 0) {
-    KernelCfg f{(Family)ctx->force_family, ctx->force_G, ctx->force_R,
-                ctx->force_family == 0 ? mask : false, fp32,
-                (ctx->force_family == 1 && !fp32 && ctx->force_R > 0)
-                    ? (int)((2 * s.hw + 1) % ctx->force_R)
-                    : -1};
+    const bool band = ctx->force_family >= 1;  // 1: band P=1, 2: band P=2
+    KernelCfg f{band ? Family::Band : Family::Full, ctx->force_G, ctx->force_R,
+                band ? false : mask, fp32,
+                (band && !fp32 && ctx->force_R > 0) ? (int)((2 * s.hw + 1) % ctx->force_R) : -1,
+                ctx->force_family == 2 ? 2 : 1};
     const bool ok = dtwgpu::fill_cfg_supported(f) &&
                     (f.family == Family::Full ||
                      (mask && f.R >= 2 && (int64_t)f.G * f.R >= 2 * s.hw + 1));
@@ -330,7 +340,7 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
     return plan;
   }
   std::map<Shape, int> cls_of_shape;
-  std::map<std::tuple<int, int, int, bool, int>, int> cls_of_cfg;
+  std::map<std::tuple<int, int, int, bool, int, int>, int> cls_of_cfg;
   std::vector<std::vector<std::pair<double, int64_t>>> items;
   int64_t i = 0;
   // decode sb
@@ -351,7 +361,7 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
     if (it == cls_of_shape.end()) {
       double cst = 0;
       const KernelCfg cfg = choose_cfg(ctx, s, fp32, &cst);
-      const auto key = std::make_tuple((int)cfg.family, cfg.G, cfg.R, cfg.mask, cfg.kr);
+      const auto key = std::make_tuple((int)cfg.family, cfg.G, cfg.R, cfg.mask, cfg.kr, cfg.P);
       auto ic = cls_of_cfg.find(key);
       if (ic == cls_of_cfg.end()) {
         PlanClass pc;
@@ -391,12 +401,58 @@ int ensure_fp32(dtwg_ctx* ctx) {
   if (ctx->have32) return DTWG_OK;
   std::vector<float> f(ctx->h_samples.size());
   for (size_t t = 0; t < f.size(); ++t) f[t] = static_cast<float>(ctx->h_samples[t]);
-  CU(ctx->d_samples32.reserve(f.size()), "cudaMalloc samples32");
-  CU(cudaMemcpyAsync(ctx->d_samples32.ptr, f.data(), f.size() * sizeof(float),
+  CU(ctx->d_samples32.reserve(f.size() + 2 * kGuard), "cudaMalloc samples32");
+  CU(cudaMemsetAsync(ctx->d_samples32.ptr, 0, (f.size() + 2 * kGuard) * sizeof(float),
+                     ctx->stream),
+     "memset samples32");
+  CU(cudaMemcpyAsync(ctx->d_samples32.ptr + kGuard, f.data(), f.size() * sizeof(float),
                      cudaMemcpyHostToDevice, ctx->stream),
      "H2D samples32");
   CU(cudaStreamSynchronize(ctx->stream), "sync");
   ctx->have32 = true;
+  return DTWG_OK;
+}
+
+// Band-family copy of the series: each series surrounded by kBandPad +inf samples.
+int ensure_band(dtwg_ctx* ctx, bool fp32) {
+  if (fp32 ? ctx->have_band32 : ctx->have_band64) return DTWG_OK;
+  const int64_t p = ctx->p;
+  const int64_t pad = dtwgpu::kBandPad;
+  std::vector<int64_t> boff(p + 1);
+  int64_t pos = pad;
+  for (int64_t i = 0; i < p; ++i) {
+    boff[i] = pos;
+    pos += ctx->h_len[i] + 2 * pad;
+  }
+  boff[p] = pos;
+  const int64_t total = pos + pad;
+  CU(ctx->d_boffsets.reserve(p + 1), "cudaMalloc boffsets");
+  CU(cudaMemcpyAsync(ctx->d_boffsets.ptr, boff.data(), (p + 1) * 8, cudaMemcpyHostToDevice,
+                     ctx->stream),
+     "H2D boffsets");
+  if (fp32) {
+    std::vector<float> h(total, std::numeric_limits<float>::infinity());
+    for (int64_t i = 0; i < p; ++i)
+      for (int64_t t = 0; t < ctx->h_len[i]; ++t)
+        h[boff[i] + t] = static_cast<float>(ctx->h_samples[ctx->h_offsets[i] + t]);
+    CU(ctx->d_bsamples32.reserve(total), "cudaMalloc bsamples32");
+    CU(cudaMemcpyAsync(ctx->d_bsamples32.ptr, h.data(), total * 4, cudaMemcpyHostToDevice,
+                       ctx->stream),
+       "H2D bsamples32");
+    CU(cudaStreamSynchronize(ctx->stream), "sync");
+    ctx->have_band32 = true;
+  } else {
+    std::vector<double> h(total, kInf);
+    for (int64_t i = 0; i < p; ++i)
+      std::copy(ctx->h_samples.begin() + ctx->h_offsets[i],
+                ctx->h_samples.begin() + ctx->h_offsets[i] + ctx->h_len[i], h.begin() + boff[i]);
+    CU(ctx->d_bsamples.reserve(total), "cudaMalloc bsamples");
+    CU(cudaMemcpyAsync(ctx->d_bsamples.ptr, h.data(), total * 8, cudaMemcpyHostToDevice,
+                       ctx->stream),
+       "H2D bsamples");
+    CU(cudaStreamSynchronize(ctx->stream), "sync");
+    ctx->have_band64 = true;
+  }
   return DTWG_OK;
 }
 
@@ -409,6 +465,13 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
   }
   std::vector<PlanClass> plan = make_plan(ctx, hw, auto_widen, fp32, sb, se);
   ctx->last_plan.clear();
+  for (auto& pc : plan) {
+    if (pc.cfg.family == Family::Band) {
+      const int rc = ensure_band(ctx, fp32);
+      if (rc) return rc;
+      break;
+    }
+  }
   CU(cudaEventRecord(ctx->ev0, ctx->stream), "event");
   // Upload all class lists in one buffer.
   size_t total_list = 0;
@@ -433,12 +496,16 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
     if (count == 0) continue;
     const int bps = dtwgpu::fill_blocks_per_sm(pc.cfg);
     const int64_t groups_per_block = dtwgpu::kThreads / pc.cfg.G;
+    const int64_t items_per_block = groups_per_block * (pc.cfg.family == Family::Band ? pc.cfg.P : 1);
     int64_t blocks = (int64_t)ctx->num_sms * bps;
-    blocks = std::min<int64_t>(blocks, (count + groups_per_block - 1) / groups_per_block);
+    blocks = std::min<int64_t>(blocks, (count + items_per_block - 1) / items_per_block);
     blocks = std::max<int64_t>(blocks, 1);
     FillArgs a{};
-    a.samples = ctx->d_samples.ptr;
-    a.samples32 = fp32 ? ctx->d_samples32.ptr : nullptr;
+    a.samples = ctx->d_samples.ptr + kGuard;
+    a.samples32 = fp32 ? ctx->d_samples32.ptr + kGuard : nullptr;
+    a.bsamples = ctx->have_band64 ? ctx->d_bsamples.ptr : nullptr;
+    a.bsamples32 = ctx->have_band32 ? ctx->d_bsamples32.ptr : nullptr;
+    a.boffsets = (ctx->have_band64 || ctx->have_band32) ? ctx->d_boffsets.ptr : nullptr;
     a.offsets = ctx->d_offsets.ptr;
     a.p = ctx->p;
     a.half_width = hw;
@@ -461,8 +528,10 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
     CU(dtwgpu::launch_fill(pc.cfg, a, (int)blocks, ctx->stream), "fill launch");
     ctx->launches++;
     char buf[160];
-    char krs[16] = "";
-    if (pc.cfg.family == Family::Band && pc.cfg.kr >= 0) snprintf(krs, sizeof(krs), ",kr=%d", pc.cfg.kr);
+    char krs[32] = "";
+    if (pc.cfg.family == Family::Band)
+      snprintf(krs, sizeof(krs), "%s,P=%d", pc.cfg.kr >= 0 ? (",kr=" + std::to_string(pc.cfg.kr)).c_str() : "",
+               pc.cfg.P);
     snprintf(buf, sizeof(buf), "%s%s[G=%d,R=%d%s%s%s] pairs=%lld blocks=%lld(%d/SM)",
              ctx->last_plan.empty() ? "" : "; ", family_name(pc.cfg.family), pc.cfg.G, pc.cfg.R,
              pc.cfg.mask ? ",mask" : "", fp32 ? ",fp32" : "", krs, (long long)count,
@@ -731,6 +800,9 @@ void dtwg_destroy(dtwg_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   ctx->d_samples.release();
   ctx->d_samples32.release();
+  ctx->d_bsamples.release();
+  ctx->d_bsamples32.release();
+  ctx->d_boffsets.release();
   ctx->d_offsets.release();
   ctx->d_scratch.release();
   ctx->d_list.release();
@@ -800,9 +872,13 @@ int dtwg_upload_series(dtwg_ctx* ctx, const double* samples, const int64_t* offs
   const int64_t n = ctx->h_offsets[p];
   ctx->h_samples.assign(samples + base, samples + base + n);
   ctx->have32 = false;
-  CU(ctx->d_samples.reserve(n), "cudaMalloc samples");
+  ctx->have_band64 = ctx->have_band32 = false;
+  CU(ctx->d_samples.reserve(n + 2 * kGuard), "cudaMalloc samples");
   CU(ctx->d_offsets.reserve(p + 1), "cudaMalloc offsets");
-  CU(cudaMemcpyAsync(ctx->d_samples.ptr, ctx->h_samples.data(), n * sizeof(double),
+  CU(cudaMemsetAsync(ctx->d_samples.ptr, 0, kGuard * sizeof(double), ctx->stream), "memset");
+  CU(cudaMemsetAsync(ctx->d_samples.ptr + kGuard + n, 0, kGuard * sizeof(double), ctx->stream),
+     "memset");
+  CU(cudaMemcpyAsync(ctx->d_samples.ptr + kGuard, ctx->h_samples.data(), n * sizeof(double),
                      cudaMemcpyHostToDevice, ctx->stream),
      "H2D samples");
   CU(cudaMemcpyAsync(ctx->d_offsets.ptr, ctx->h_offsets.data(), (p + 1) * sizeof(int64_t),

@@ -7,22 +7,28 @@
 namespace dtwgpu {
 namespace {
 using namespace kern;
-template <int G, int R, int KR>
+template <int G, int R, int KR, int P>
 struct BandTable {
   static const void* get(int kr) {
-    if (kr == KR) return (const void*)dtw_band_kernel<G, R, KR, F64>;
-    if constexpr (KR > 0) return BandTable<G, R, KR - 1>::get(kr);
+    if (kr == KR) return (const void*)dtw_band_kernel<G, R, KR, P, F64>;
+    if constexpr (KR > 0) return BandTable<G, R, KR - 1, P>::get(kr);
     return nullptr;
   }
 };
 }  // namespace
 
-const void* band32_kernel_ptr(int R, int kr, bool fp32) {
+const void* band32_kernel_ptr(int R, int kr, int P, bool fp32) {
 #define DTWG_B(g, r)                                                              \
   if (g == 32 && R == r) {                                                        \
-    if (fp32) return (const void*)dtw_band_kernel<g, r, -1, F32>;                \
-    if (kr < 0) return (const void*)dtw_band_kernel<g, r, -1, F64>;              \
-    return BandTable<g, r, r - 1>::get(kr);                                       \
+    if (P == 2) {                                                                 \
+      if constexpr (r > 7) return nullptr; /* P = 2 only where the code is small */ \
+      if (fp32) return (const void*)dtw_band_kernel<g, r, -1, 2, F32>;           \
+      if (kr < 0) return (const void*)dtw_band_kernel<g, r, -1, 2, F64>;         \
+      return BandTable<g, r, r - 1, 2>::get(kr);                                  \
+    }                                                                             \
+    if (fp32) return (const void*)dtw_band_kernel<g, r, -1, 1, F32>;             \
+    if (kr < 0) return (const void*)dtw_band_kernel<g, r, -1, 1, F64>;           \
+    return BandTable<g, r, r - 1, 1>::get(kr);                                    \
   }
   DTWG_BAND_CFGS_G32(DTWG_B)
 #undef DTWG_B

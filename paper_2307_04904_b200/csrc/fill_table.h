@@ -9,6 +9,6 @@
 
 namespace dtwgpu {
 const void* full_kernel_ptr(int G, int R, bool mask, bool fp32);
-const void* band16_kernel_ptr(int R, int kr, bool fp32);
-const void* band32_kernel_ptr(int R, int kr, bool fp32);
+const void* band16_kernel_ptr(int R, int kr, int P, bool fp32);
+const void* band32_kernel_ptr(int R, int kr, int P, bool fp32);
 }  // namespace dtwgpu

@@ -150,7 +150,8 @@ def test_full_family_every_instantiation(eng, G, R, fp32):
 
 @pytest.mark.parametrize("G,R", BAND)
 @pytest.mark.parametrize("fp32", [False, True])
-def test_band_family_every_instantiation(eng, G, R, fp32):
+@pytest.mark.parametrize("family", [1, 2])  # 2 = two pairs per lane group
+def test_band_family_every_instantiation(eng, G, R, fp32, family):
     rng = np.random.default_rng(G * 1000 + R)
     kmax = G * R
     for hw in sorted({0, 1, (kmax - 1) // 2, max((kmax - 1) // 2 - 3, 0), 7}):
@@ -160,7 +161,7 @@ def test_band_family_every_instantiation(eng, G, R, fp32):
         lengths = [base + int(d) for d in rng.integers(-hw, hw + 1, size=10)]
         lengths = [max(L, 1) for L in lengths]
         samples, offsets = _walks(11 + hw, lengths)
-        eng.force_kernel(1, G, R)
+        eng.force_kernel(family, G, R)
         got = eng.build_condensed(samples, offsets, hw, True, precision=1 if fp32 else 0)
         plan = eng.last_plan()
         want = oracle.build_condensed(samples, offsets, hw, True)

@@ -21,7 +21,7 @@ def main():
     ap.add_argument("--config", type=int, required=True)
     ap.add_argument("--subset", type=int, default=0)
     ap.add_argument("--prec", type=int, default=0)
-    ap.add_argument("--families", default="0,1")
+    ap.add_argument("--families", default="0,1,2")
     a = ap.parse_args()
     ds = gen.make_config(a.config)
     if a.subset:
@@ -37,6 +37,8 @@ def main():
         cands += [(0, g, r) for g, r in FULL]
     if 1 in fams:
         cands += [(1, g, r) for g, r in BAND]
+    if 2 in fams:
+        cands += [(2, g, r) for g, r in BAND]
     ref = None
     for fam, g, r in [(-1, 0, 0)] + cands:
         eng.force_kernel(fam, g, r)
