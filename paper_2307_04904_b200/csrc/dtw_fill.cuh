@@ -43,6 +43,7 @@ struct KernelCfg {
   bool fp32;
   int kr = -1;  // Band family: (2hw+1) % R when every pair of the launch shares it, else -1
   int P = 1;    // Band family: pairs per lane group (independent chains per lane)
+  int TR = 2;   // Full family: rows per step (independent chains per lane)
 };
 
 // Launches cfg over args on stream with `blocks` CTAs of kThreads threads.

@@ -128,52 +128,49 @@ __device__ __forceinline__ float rebase(float v, double from, double to) {
 // ===================================================================================
 // Full family: column strips, two rows per step, multi-pass, optional band mask.
 // ===================================================================================
-template <int R, bool MASK, class Ar>
+template <int R, int NR, bool MASK, class Ar>
 struct FullRows {
   using T = typename Ar::T;
-  // Two rows (a = r0, b = r0+1): a_r needs (pv[r-1]|diag0, pv[r], a_{r-1});
-  // b_r needs (a_{r-1}|L0, a_r, b_{r-1}). pv becomes row b.
-  static __device__ __forceinline__ void two(T (&pv)[R], const T (&yv)[R], T x0, T x1, T diag0,
-                                             T L0, T L1, int jl, int r0, int hw, T& aout,
-                                             T& bout) {
+  // NR consecutive rows r0 .. r0+NR-1 of this lane's R-column strip. Row t's cell at
+  // column r needs (row t-1, col r-1) [diag], (row t-1, col r) [up] and (row t, col r-1)
+  // [left]; row -1 is the previous step's last row, held in pv. The unrolled NR x R
+  // block is a 2-D wavefront, so the compiler interleaves NR independent chains (ILP NR).
+  // In: diag0 = (r0-1, jl-1); L[t] = (r0+t, jl-1) from lane l-1. Out: out[t] = (r0+t,
+  // last column); pv becomes row r0+NR-1.
+  static __device__ __forceinline__ void run(T (&pv)[R], const T (&yv)[R], const T (&x)[NR],
+                                             T diag0, const T (&L)[NR], int jl, int r0, int hw,
+                                             T (&out)[NR]) {
     const T INF = Ar::inf();
-    T ad = diag0, al = L0, bd = L0, bl = L1;
-    const int lo0 = r0 - hw, hi0 = r0 + hw;
+    T d[NR], l[NR];
+#pragma unroll
+    for (int t = 0; t < NR; ++t) {
+      d[t] = t == 0 ? diag0 : L[t - 1];
+      l[t] = L[t];
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const T up = pv[r];
-      T a = Ar::cell(x0, yv[r], Ar::mn(Ar::mn(ad, up), al));
-      if (MASK) a = (jl + r >= lo0 && jl + r <= hi0) ? a : INF;
-      T b = Ar::cell(x1, yv[r], Ar::mn(Ar::mn(bd, a), bl));
-      if (MASK) b = (jl + r >= lo0 + 1 && jl + r <= hi0 + 1) ? b : INF;
-      ad = up;
-      al = a;
-      bd = a;
-      bl = b;
-      pv[r] = b;
-    }
-    aout = al;
-    bout = bl;
-  }
-  static __device__ __forceinline__ void one(T (&pv)[R], const T (&yv)[R], T x0, T diag0, T L0,
-                                             int jl, int r0, int hw, T& aout) {
-    const T INF = Ar::inf();
-    T ad = diag0, al = L0;
-    const int lo0 = r0 - hw, hi0 = r0 + hw;
+      T up = pv[r];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const T up = pv[r];
-      T a = Ar::cell(x0, yv[r], Ar::mn(Ar::mn(ad, up), al));
-      if (MASK) a = (jl + r >= lo0 && jl + r <= hi0) ? a : INF;
-      ad = up;
-      al = a;
-      pv[r] = a;
+      for (int t = 0; t < NR; ++t) {
+        T v = Ar::cell(x[t], yv[r], Ar::mn(Ar::mn(d[t], up), l[t]));
+        if (MASK) {
+          const int j = jl + r, i = r0 + t;
+          v = (j >= i - hw && j <= i + hw) ? v : INF;
+        }
+        d[t] = up;  // (t-1, r) is the diagonal of (t, r+1)
+        l[t] = v;
+        up = v;     // (t, r) is the up neighbour of (t+1, r)
+      }
+      pv[r] = up;
     }
-    aout = al;
+#pragma unroll
+    for (int t = 0; t < NR; ++t) out[t] = l[t];
   }
 };
 
-template <int G, int R, bool MASK, class Ar>
+// Full family. TR rows per step (ILP TR), warp-uniform loops, multi-pass over column
+// strips of width G*R with a per-group boundary column between passes.
+template <int G, int R, int TR, bool MASK, class Ar>
 __global__ void __launch_bounds__(kThreads) dtw_full_kernel(const FillArgs A) {
   using T = typename Ar::T;
   constexpr bool kF32 = sizeof(T) == 4;
@@ -209,7 +206,7 @@ __global__ void __launch_bounds__(kThreads) dtw_full_kernel(const FillArgs A) {
         re = min(n, c0 + W + hw);
       }
       if (!pvalid) re = rs - 1;
-      const int my_steps = pvalid ? ((re - rs + 2) >> 1) + G - 1 : 0;
+      const int my_steps = pvalid ? ((re - rs + TR) / TR) + G - 1 : 0;
       const int nsteps = __reduce_max_sync(kFull, my_steps);
       const int jl = c0 + gl * R + 1;  // 1-based first column of this lane
       T yv[R], pv[R];
@@ -224,7 +221,9 @@ __global__ void __launch_bounds__(kThreads) dtw_full_kernel(const FillArgs A) {
         else if (rs - 1 >= 1 && rs - 1 <= written_hi) diag0 = (T)bnd[rs - 1];
       }
       double off = 0.0;  // fp32: this lane's offset
-      T send0 = INF, send1 = INF;
+      T send[TR];
+#pragma unroll
+      for (int t = 0; t < TR; ++t) send[t] = INF;
       double send_off = 0.0;
       const bool last_pass = pass == npass_g - 1;
       const bool hold = pvalid && last_pass && ((m - 1 - c0) / R) == gl;
@@ -232,65 +231,71 @@ __global__ void __launch_bounds__(kThreads) dtw_full_kernel(const FillArgs A) {
       const bool wb = pvalid && !last_pass && gl == G - 1;
       const bool use_bnd = gl == 0 && pass > 0;
 
-      int r0 = rs - 2 * gl;  // this lane's first row at step 0
+      int r0 = rs - TR * gl;  // this lane's first row at step 0
       // Rows outside [1, n] read the zero guard around the packed series (never used).
-      T xa = __ldg(X + (r0 - 1));
-      T xb = __ldg(X + r0);
-      double ba = Ar::inf(), bb = Ar::inf();
-      if (use_bnd) {
-        if (r0 <= written_hi) ba = bnd[r0];
-        if (r0 + 1 <= written_hi) bb = bnd[r0 + 1];
+      T xq[TR];
+      double bq[TR];
+#pragma unroll
+      for (int t = 0; t < TR; ++t) {
+        xq[t] = __ldg(X + (r0 + t - 1));
+        bq[t] = (use_bnd && r0 + t <= written_hi) ? bnd[r0 + t] : (double)Ar::inf();
       }
 
-      for (int s = 0; s < nsteps; ++s, r0 += 2) {
-        const T x0 = xa, x1 = xb;
-        const double b0 = ba, b1 = bb;
-        xa = __ldg(X + (r0 + 1));
-        xb = __ldg(X + (r0 + 2));
-        if (use_bnd) {
-          ba = (r0 + 2 <= written_hi) ? bnd[r0 + 2] : (double)Ar::inf();
-          bb = (r0 + 3 <= written_hi) ? bnd[r0 + 3] : (double)Ar::inf();
+      for (int s = 0; s < nsteps; ++s, r0 += TR) {
+        T x[TR], L[TR];
+        double b[TR];
+#pragma unroll
+        for (int t = 0; t < TR; ++t) {
+          x[t] = xq[t];
+          b[t] = bq[t];
+          xq[t] = __ldg(X + (r0 + TR + t - 1));
+          if (use_bnd) bq[t] = (r0 + TR + t <= written_hi) ? bnd[r0 + TR + t] : (double)Ar::inf();
+          L[t] = __shfl_up_sync(kFull, send[t], 1, G);
         }
-        T L0 = __shfl_up_sync(kFull, send0, 1, G);
-        T L1 = __shfl_up_sync(kFull, send1, 1, G);
         if constexpr (kF32) {
           const double loff = __shfl_up_sync(kFull, send_off, 1, G);
-          if (gl == 0) {
-            L0 = (b0 == (double)INF) ? INF : (T)(b0 - off);
-            L1 = (b1 == (double)INF) ? INF : (T)(b1 - off);
-          } else {
-            L0 = rebase(L0, loff, off);
-            L1 = rebase(L1, loff, off);
+#pragma unroll
+          for (int t = 0; t < TR; ++t) {
+            if (gl == 0) L[t] = (b[t] == (double)INF) ? INF : (T)(b[t] - off);
+            else L[t] = rebase(L[t], loff, off);
           }
         } else {
           if (gl == 0) {
-            L0 = (T)b0;
-            L1 = (T)b1;
+#pragma unroll
+            for (int t = 0; t < TR; ++t) L[t] = (T)b[t];
           }
         }
         const bool work = s >= gl && r0 <= re;
         bool fast = true;
         if (MASK) {
-          // Rows r0, r0+1 entirely inside |i-j| <= hw for every working lane of the warp?
-          const bool in = (jl >= r0 + 1 - hw) && (jl + R - 1 <= r0 + hw);
+          // All TR rows entirely inside |i-j| <= hw for every working lane of the warp?
+          const bool in = (jl >= r0 + TR - 1 - hw) && (jl + R - 1 <= r0 + hw);
           fast = __all_sync(kFull, in || !work);
         }
         if (work) {
-          T aout, bout;
-          const bool two = r0 + 1 <= re;
-          if (two) {
+          T out[TR];
+          const int nr = min(TR, re - r0 + 1);  // rows of this step inside [rs, re]
+          if (nr == TR) {
             if (!MASK || fast)
-              FullRows<R, false, Ar>::two(pv, yv, x0, x1, diag0, L0, L1, jl, r0, hw, aout, bout);
+              FullRows<R, TR, false, Ar>::run(pv, yv, x, diag0, L, jl, r0, hw, out);
             else
-              FullRows<R, MASK, Ar>::two(pv, yv, x0, x1, diag0, L0, L1, jl, r0, hw, aout, bout);
-            diag0 = L1;
+              FullRows<R, TR, MASK, Ar>::run(pv, yv, x, diag0, L, jl, r0, hw, out);
+            diag0 = L[TR - 1];
           } else {
-            if (!MASK || fast)
-              FullRows<R, false, Ar>::one(pv, yv, x0, diag0, L0, jl, r0, hw, aout);
-            else
-              FullRows<R, MASK, Ar>::one(pv, yv, x0, diag0, L0, jl, r0, hw, aout);
-            bout = aout;
-            diag0 = L0;
+            // Tail of the pass: the remaining rows one at a time.
+#pragma unroll
+            for (int t = 0; t < TR; ++t) {
+              if (t < nr) {
+                const T xt[1] = {x[t]};
+                const T Lt[1] = {L[t]};
+                T ot[1];
+                FullRows<R, 1, MASK, Ar>::run(pv, yv, xt, diag0, Lt, jl, r0 + t, hw, ot);
+                out[t] = ot[0];
+                diag0 = L[t];
+              } else {
+                out[t] = INF;
+              }
+            }
           }
           if constexpr (kF32) {
             if ((s & (kRenormSteps - 1)) == kRenormSteps - 1) {
@@ -301,28 +306,23 @@ __global__ void __launch_bounds__(kThreads) dtw_full_kernel(const FillArgs A) {
 #pragma unroll
                 for (int r = 0; r < R; ++r) pv[r] = __fsub_rn(pv[r], mnv);
                 diag0 = (diag0 == INF) ? INF : __fsub_rn(diag0, mnv);
-                // aout/bout were produced before the shift: re-base them too
-                aout = (aout == INF) ? INF : __fsub_rn(aout, mnv);
-                bout = (bout == INF) ? INF : __fsub_rn(bout, mnv);
+#pragma unroll
+                for (int t = 0; t < TR; ++t) out[t] = (out[t] == INF) ? INF : __fsub_rn(out[t], mnv);
                 off += (double)mnv;
               }
             }
             send_off = off;
           }
-          send0 = aout;
-          send1 = bout;
-          if (wb) {
-            if constexpr (kF32) {
-              bnd[r0] = (aout == INF) ? (double)INF : (double)aout + off;
-              if (two) bnd[r0 + 1] = (bout == INF) ? (double)INF : (double)bout + off;
-            } else {
-              bnd[r0] = aout;
-              if (two) bnd[r0 + 1] = bout;
+#pragma unroll
+          for (int t = 0; t < TR; ++t) {
+            send[t] = out[t];
+            if (wb && t < nr) {
+              if constexpr (kF32) bnd[r0 + t] = (out[t] == INF) ? (double)INF : (double)out[t] + off;
+              else bnd[r0 + t] = out[t];
             }
           }
-          // Row n is always the last row this lane writes into pv (re <= n, so a step
-          // with r0 == n is a single-row step).
-          if (hold && (r0 == n || (two && r0 + 1 == n))) {
+          // pv now holds row r0 + nr - 1; row n is the last row of the last pass (re = n).
+          if (hold && r0 + nr - 1 == n) {
             T rv = pv[0];
 #pragma unroll
             for (int r = 1; r < R; ++r) rv = (r == r_res) ? pv[r] : rv;

@@ -118,10 +118,14 @@ struct Cand {
   int G, R;
   double rate;  // computed lane-cells / ns
   int P = 1;    // band family: pairs per lane group
+  int TR = 2;   // full family: rows per step
 };
-const Cand kFull[] = {{2, 23, 1845}, {4, 12, 1846}, {8, 8, 1714},   {16, 8, 1700},
-                      {16, 16, 2020}, {32, 4, 1300}, {32, 8, 1750}, {32, 12, 1900},
-                      {32, 15, 2165}, {32, 16, 2170}};
+const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026},
+                      {4, 12, 1956, 1, 4},   {8, 8, 1804},         {8, 8, 1700, 1, 4},
+                      {16, 8, 1800},         {16, 16, 1850},       {16, 16, 1850, 1, 4},
+                      {32, 4, 1300},         {32, 8, 1650},        {32, 12, 1950},
+                      {32, 15, 2000},        {32, 15, 2150, 1, 4}, {32, 16, 2100},
+                      {32, 16, 2050, 1, 4}};
 const Cand kBand[] = {{16, 7, 1500},    {16, 9, 1600},    {16, 11, 1700},  {16, 13, 1800},
                       {32, 3, 1000},    {32, 5, 1250},    {32, 7, 1490},   {32, 9, 1500},
                       {32, 13, 1450},   {32, 3, 1000, 2}, {32, 5, 1200, 2}, {32, 7, 1550, 2}};
@@ -137,12 +141,16 @@ double full_cost(const Shape& s, const Cand& c, bool mask) {
       rs = std::max<int64_t>(1, c0 + 1 - s.hw);
       re = std::min<int64_t>(s.n, c0 + W + s.hw);
     }
-    // two rows per step, G-1 steps of wavefront fill/drain
-    cells += double(((re - rs + 2) / 2) * 2 + 2 * (c.G - 1)) * double(W);
+    // TR rows per step, G-1 steps of wavefront fill/drain
+    cells += double(((re - rs + c.TR) / c.TR) * c.TR + c.TR * (c.G - 1)) * double(W);
   }
   double rate = c.rate;
-  if (mask) rate *= 0.75;                       // masked steps (measured on c2 / c5)
-  if (npass > 1 && c.G <= 4) rate *= 0.55;      // boundary column round trips
+  if (mask) rate *= 0.75;  // masked steps (measured on c2 / c5)
+  if (npass > 1) {         // boundary-column round trips per pass (measured on c4)
+    if (c.G == 2) rate *= c.TR == 4 ? 0.68 : 0.59;
+    else if (c.G == 4) rate *= c.TR == 4 ? 0.92 : 0.78;
+    else if (c.G == 8) rate *= c.TR == 4 ? 1.0 : 0.95;
+  }
   return cells / rate;
 }
 
@@ -163,7 +171,7 @@ KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out) {
     const double cst = full_cost(s, c, mask);
     if (cst < bc) {
       bc = cst;
-      best = KernelCfg{Family::Full, c.G, c.R, mask, fp32};
+      best = KernelCfg{Family::Full, c.G, c.R, mask, fp32, -1, 1, c.TR};
     }
   }
   if (mask) {
@@ -191,12 +199,35 @@ struct dtwg_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // Side streams: the kernel classes of a ragged fill run concurrently so one class's
+  // tail wave overlaps the next class's work.
+  static constexpr int kAux = 4;
+  cudaStream_t aux[kAux] = {};
+  cudaEvent_t aux_done[kAux] = {};
+  cudaEvent_t fork = nullptr;
   float last_fill_ms = 0.f;
   uint64_t launches = 0;
   std::string last_error;
   std::string last_plan;
   int64_t err_i = -1, err_j = -1;
   int force_family = -1, force_G = 0, force_R = 0;  // dtwg_force_kernel (tests/diagnostics)
+
+  // cached plan of the last ragged fill (planning 12.5M pairs costs ~1 s of host time)
+  struct PlanKey {
+    int64_t hw, sb, se;
+    int auto_widen;
+    bool fp32;
+    int force_family, force_G, force_R;
+    bool operator==(const PlanKey& o) const {
+      return hw == o.hw && sb == o.sb && se == o.se && auto_widen == o.auto_widen &&
+             fp32 == o.fp32 && force_family == o.force_family && force_G == o.force_G &&
+             force_R == o.force_R;
+    }
+  };
+  bool plan_valid = false;
+  PlanKey plan_key{};
+  std::vector<PlanClass> plan_cache;
+  bool list_uploaded = false;
 
   // series
   int64_t p = 0;
@@ -255,11 +286,12 @@ namespace {
 KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cost_out) {
   const bool mask = s.hw < s.n - 1;
   if (ctx->force_family >= 0) {
-    const bool band = ctx->force_family >= 1;  // 1: band P=1, 2: band P=2
+    // 0: full (2 rows/step), 1: band P=1, 2: band P=2, 3: full (4 rows/step)
+    const bool band = ctx->force_family == 1 || ctx->force_family == 2;
     KernelCfg f{band ? Family::Band : Family::Full, ctx->force_G, ctx->force_R,
                 band ? false : mask, fp32,
                 (band && !fp32 && ctx->force_R > 0) ? (int)((2 * s.hw + 1) % ctx->force_R) : -1,
-                ctx->force_family == 2 ? 2 : 1};
+                ctx->force_family == 2 ? 2 : 1, ctx->force_family == 3 ? 4 : 2};
     const bool ok = dtwgpu::fill_cfg_supported(f) &&
                     (f.family == Family::Full ||
                      (mask && f.R >= 2 && (int64_t)f.G * f.R >= 2 * s.hw + 1));
@@ -339,11 +371,51 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
     plan.push_back(pc);
     return plan;
   }
+  // Ragged dataset: classify every pair by shape (memoised on (n, m)), then bucket the
+  // slots of each class by (passes, rows) with a counting sort -- longest first (LPT),
+  // and pairs of equal pass count and row count adjacent, so the lane groups of one warp
+  // run in lockstep. O(pairs); no comparison sort.
+  int64_t maxlen = 0;
+  for (int64_t t = 0; t < p; ++t) maxlen = std::max(maxlen, ctx->h_len[t]);
+  const int64_t L1 = maxlen + 1;
+  std::vector<int> cls_tab;
+  const bool use_tab = L1 * L1 <= (int64_t)1 << 26;
+  if (use_tab) cls_tab.assign((size_t)(L1 * L1), -1);
   std::map<Shape, int> cls_of_shape;
-  std::map<std::tuple<int, int, int, bool, int, int>, int> cls_of_cfg;
-  std::vector<std::vector<std::pair<double, int64_t>>> items;
-  int64_t i = 0;
-  // decode sb
+  std::map<std::tuple<int, int, int, bool, int, int, int>, int> cls_of_cfg;
+  auto class_of = [&](int64_t a, int64_t b, Shape& s) -> int {
+    s = shape_of(ctx, a, b, hw, auto_widen);
+    int* slotp = use_tab ? &cls_tab[(size_t)(s.n * L1 + s.m)] : nullptr;
+    if (slotp && *slotp >= 0) return *slotp;
+    if (!slotp) {
+      auto it = cls_of_shape.find(s);
+      if (it != cls_of_shape.end()) return it->second;
+    }
+    double cst = 0;
+    const KernelCfg cfg = choose_cfg(ctx, s, fp32, &cst);
+    const auto key = std::make_tuple((int)cfg.family, cfg.G, cfg.R, cfg.mask, cfg.kr, cfg.P, cfg.TR);
+    int cls;
+    auto ic = cls_of_cfg.find(key);
+    if (ic == cls_of_cfg.end()) {
+      PlanClass pc;
+      pc.cfg = cfg;
+      plan.push_back(pc);
+      cls = (int)plan.size() - 1;
+      cls_of_cfg[key] = cls;
+    } else {
+      cls = ic->second;
+    }
+    if (slotp) *slotp = cls;
+    else cls_of_shape[s] = cls;
+    return cls;
+  };
+  auto bucket_of = [&](int cls, const Shape& s) -> int64_t {
+    const KernelCfg& cc = plan[cls].cfg;
+    const int64_t W = (int64_t)cc.G * cc.R;
+    const int64_t npass = cc.family == Family::Full ? (s.m + W - 1) / W : 1;
+    return npass * L1 + s.n;  // larger = earlier
+  };
+  int64_t i0;
   {
     int64_t lo = 0, hi = p - 1;
     while (lo < hi) {
@@ -351,48 +423,52 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
       if (row_off(mid, p) <= sb) lo = mid;
       else hi = mid - 1;
     }
-    i = lo;
+    i0 = lo;
   }
-  int64_t j = i + 1 + (sb - row_off(i, p));
-  for (int64_t slot = sb; slot < se; ++slot) {
-    const Shape s = shape_of(ctx, i, j, hw, auto_widen);
-    auto it = cls_of_shape.find(s);
-    int cls;
-    if (it == cls_of_shape.end()) {
-      double cst = 0;
-      const KernelCfg cfg = choose_cfg(ctx, s, fp32, &cst);
-      const auto key = std::make_tuple((int)cfg.family, cfg.G, cfg.R, cfg.mask, cfg.kr, cfg.P);
-      auto ic = cls_of_cfg.find(key);
-      if (ic == cls_of_cfg.end()) {
-        PlanClass pc;
-        pc.cfg = cfg;
-        plan.push_back(pc);
-        items.emplace_back();
-        cls = (int)plan.size() - 1;
-        cls_of_cfg[key] = cls;
-      } else {
-        cls = ic->second;
+  const int64_t j0 = i0 + 1 + (sb - row_off(i0, p));
+  // pass 1: classes, bucket counts
+  std::vector<std::vector<int64_t>> counts;
+  {
+    int64_t i = i0, j = j0;
+    Shape s;
+    for (int64_t slot = sb; slot < se; ++slot) {
+      const int cls = class_of(i, j, s);
+      if ((int)counts.size() <= cls) counts.resize(cls + 1);
+      const int64_t bk = bucket_of(cls, s);
+      if ((int64_t)counts[cls].size() <= bk) counts[cls].resize(bk + 1, 0);
+      counts[cls][bk]++;
+      plan[cls].max_n = std::max(plan[cls].max_n, s.n);
+      plan[cls].cost += double(s.n) * double(s.m);
+      if (++j == p) {
+        ++i;
+        j = i + 1;
       }
-      cls_of_shape[s] = cls;
-    } else {
-      cls = it->second;
-    }
-    const double cst = double(s.n) * double(s.m);
-    items[cls].emplace_back(cst, slot);
-    plan[cls].cost += cst;
-    plan[cls].max_n = std::max(plan[cls].max_n, s.n);
-    if (++j == p) {
-      ++i;
-      j = i + 1;
     }
   }
+  // descending bucket order -> start offsets
+  std::vector<std::vector<int64_t>> start(plan.size());
   for (size_t c = 0; c < plan.size(); ++c) {
-    auto& v = items[c];
-    // Longest pairs first, so the grid-stride schedule ends on short pairs (LPT).
-    std::stable_sort(v.begin(), v.end(),
-                     [](const auto& x, const auto& y) { return x.first > y.first; });
-    plan[c].slots.reserve(v.size());
-    for (const auto& e : v) plan[c].slots.push_back(e.second);
+    auto& cn = counts[c];
+    start[c].assign(cn.size(), 0);
+    int64_t acc = 0;
+    for (int64_t b = (int64_t)cn.size() - 1; b >= 0; --b) {
+      start[c][b] = acc;
+      acc += cn[b];
+    }
+    plan[c].slots.resize(acc);
+  }
+  // pass 2: place slots
+  {
+    int64_t i = i0, j = j0;
+    Shape s;
+    for (int64_t slot = sb; slot < se; ++slot) {
+      const int cls = class_of(i, j, s);
+      plan[cls].slots[start[cls][bucket_of(cls, s)]++] = slot;
+      if (++j == p) {
+        ++i;
+        j = i + 1;
+      }
+    }
   }
   return plan;
 }
@@ -463,7 +539,15 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
     const int rc = ensure_fp32(ctx);
     if (rc) return rc;
   }
-  std::vector<PlanClass> plan = make_plan(ctx, hw, auto_widen, fp32, sb, se);
+  const dtwg_ctx::PlanKey key{hw, sb, se, auto_widen, fp32, ctx->force_family, ctx->force_G,
+                              ctx->force_R};
+  if (!(ctx->plan_valid && ctx->plan_key == key)) {
+    ctx->plan_cache = make_plan(ctx, hw, auto_widen, fp32, sb, se);
+    ctx->plan_key = key;
+    ctx->plan_valid = true;
+    ctx->list_uploaded = false;
+  }
+  std::vector<PlanClass>& plan = ctx->plan_cache;
   ctx->last_plan.clear();
   for (auto& pc : plan) {
     if (pc.cfg.family == Family::Band) {
@@ -476,7 +560,8 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
   // Upload all class lists in one buffer.
   size_t total_list = 0;
   for (auto& pc : plan) total_list += pc.slots.size();
-  if (total_list) {
+  if (total_list && !ctx->list_uploaded) {
+    ctx->list_uploaded = true;
     CU(ctx->d_list.reserve(total_list), "cudaMalloc list");
     size_t pos = 0;
     for (auto& pc : plan) {
@@ -487,19 +572,52 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
       pos += pc.slots.size();
     }
   }
+  // Per-class scratch (multi-pass Full classes may run concurrently).
+  const bool concurrent = plan.size() > 1;
+  if (concurrent && !ctx->aux[0]) {
+    for (int a = 0; a < dtwg_ctx::kAux; ++a) {
+      CU(cudaStreamCreateWithFlags(&ctx->aux[a], cudaStreamNonBlocking), "aux stream");
+      CU(cudaEventCreateWithFlags(&ctx->aux_done[a], cudaEventDisableTiming), "aux event");
+    }
+    CU(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming), "fork event");
+  }
+  std::vector<int64_t> blocks_of(plan.size()), scratch_off(plan.size(), -1);
+  int64_t scratch_total = 0;
+  for (size_t c = 0; c < plan.size(); ++c) {
+    const PlanClass& pc = plan[c];
+    const int64_t count = ctx->uniform ? (se - sb) : (int64_t)pc.slots.size();
+    const int bps = dtwgpu::fill_blocks_per_sm(pc.cfg);
+    const int64_t groups_per_block = dtwgpu::kThreads / pc.cfg.G;
+    const int64_t items_per_block =
+        groups_per_block * (pc.cfg.family == Family::Band ? pc.cfg.P : 1);
+    int64_t blocks = (int64_t)ctx->num_sms * bps;
+    blocks = std::min<int64_t>(blocks, (count + items_per_block - 1) / items_per_block);
+    blocks_of[c] = std::max<int64_t>(blocks, 1);
+    const int64_t W = (int64_t)pc.cfg.G * pc.cfg.R;
+    const bool multipass = pc.cfg.family == Family::Full &&
+                           (ctx->uniform ? (ctx->h_len[0] > W) : true);
+    if (multipass && count > 0) {
+      scratch_off[c] = scratch_total;
+      scratch_total += (pc.max_n + 2) * blocks_of[c] * groups_per_block;
+    }
+  }
+  if (scratch_total) CU(ctx->d_scratch.reserve((size_t)scratch_total), "cudaMalloc scratch");
+  if (concurrent) {  // fork after the list upload
+    CU(cudaEventRecord(ctx->fork, ctx->stream), "fork event");
+    for (int a = 0; a < dtwg_ctx::kAux; ++a)
+      CU(cudaStreamWaitEvent(ctx->aux[a], ctx->fork, 0), "fork");
+  }
   size_t pos = 0;
-  for (auto& pc : plan) {
+  int next_aux = 0;
+  for (size_t c = 0; c < plan.size(); ++c) {
+    auto& pc = plan[c];
     if (!dtwgpu::fill_cfg_supported(pc.cfg))
       return ctx->fail(DTWG_INTERNAL, "no kernel for %s G=%d R=%d", family_name(pc.cfg.family),
                        pc.cfg.G, pc.cfg.R);
     const int64_t count = ctx->uniform ? (se - sb) : (int64_t)pc.slots.size();
     if (count == 0) continue;
     const int bps = dtwgpu::fill_blocks_per_sm(pc.cfg);
-    const int64_t groups_per_block = dtwgpu::kThreads / pc.cfg.G;
-    const int64_t items_per_block = groups_per_block * (pc.cfg.family == Family::Band ? pc.cfg.P : 1);
-    int64_t blocks = (int64_t)ctx->num_sms * bps;
-    blocks = std::min<int64_t>(blocks, (count + items_per_block - 1) / items_per_block);
-    blocks = std::max<int64_t>(blocks, 1);
+    const int64_t blocks = blocks_of[c];
     FillArgs a{};
     a.samples = ctx->d_samples.ptr + kGuard;
     a.samples32 = fp32 ? ctx->d_samples32.ptr + kGuard : nullptr;
@@ -515,29 +633,31 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
     a.count = count;
     a.out_base = out_base;
     a.out = d_out;
-    const int64_t W = (int64_t)pc.cfg.G * pc.cfg.R;
-    const bool multipass = pc.cfg.family == Family::Full &&
-                           (ctx->uniform ? (ctx->h_len[0] > W) : true);
-    if (multipass) {
-      const int64_t stride = pc.max_n + 2;
-      const int64_t groups = blocks * groups_per_block;
-      CU(ctx->d_scratch.reserve((size_t)(stride * groups)), "cudaMalloc scratch");
-      a.scratch = ctx->d_scratch.ptr;
-      a.scratch_stride = stride;
+    if (scratch_off[c] >= 0) {
+      a.scratch = ctx->d_scratch.ptr + scratch_off[c];
+      a.scratch_stride = pc.max_n + 2;
     }
-    CU(dtwgpu::launch_fill(pc.cfg, a, (int)blocks, ctx->stream), "fill launch");
+    cudaStream_t st = concurrent ? ctx->aux[next_aux++ % dtwg_ctx::kAux] : ctx->stream;
+    CU(dtwgpu::launch_fill(pc.cfg, a, (int)blocks, st), "fill launch");
     ctx->launches++;
     char buf[160];
     char krs[32] = "";
     if (pc.cfg.family == Family::Band)
       snprintf(krs, sizeof(krs), "%s,P=%d", pc.cfg.kr >= 0 ? (",kr=" + std::to_string(pc.cfg.kr)).c_str() : "",
                pc.cfg.P);
+    if (pc.cfg.family == Family::Full) snprintf(krs, sizeof(krs), ",T=%d", pc.cfg.TR);
     snprintf(buf, sizeof(buf), "%s%s[G=%d,R=%d%s%s%s] pairs=%lld blocks=%lld(%d/SM)",
              ctx->last_plan.empty() ? "" : "; ", family_name(pc.cfg.family), pc.cfg.G, pc.cfg.R,
              pc.cfg.mask ? ",mask" : "", fp32 ? ",fp32" : "", krs, (long long)count,
              (long long)blocks, bps);
     ctx->last_plan += buf;
     pos += pc.slots.size();
+  }
+  if (concurrent) {  // join
+    for (int a = 0; a < dtwg_ctx::kAux; ++a) {
+      CU(cudaEventRecord(ctx->aux_done[a], ctx->aux[a]), "join event");
+      CU(cudaStreamWaitEvent(ctx->stream, ctx->aux_done[a], 0), "join");
+    }
   }
   CU(cudaEventRecord(ctx->ev1, ctx->stream), "event");
   CU(cudaEventSynchronize(ctx->ev1), "fill sync");
@@ -818,6 +938,11 @@ void dtwg_destroy(dtwg_ctx* ctx) {
   ctx->d_best_sum.release();
   ctx->d_chosen.release();
   ctx->d_members.release();
+  for (int a = 0; a < dtwg_ctx::kAux; ++a) {
+    if (ctx->aux[a]) cudaStreamDestroy(ctx->aux[a]);
+    if (ctx->aux_done[a]) cudaEventDestroy(ctx->aux_done[a]);
+  }
+  if (ctx->fork) cudaEventDestroy(ctx->fork);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -873,6 +998,7 @@ int dtwg_upload_series(dtwg_ctx* ctx, const double* samples, const int64_t* offs
   ctx->h_samples.assign(samples + base, samples + base + n);
   ctx->have32 = false;
   ctx->have_band64 = ctx->have_band32 = false;
+  ctx->plan_valid = false;
   CU(ctx->d_samples.reserve(n + 2 * kGuard), "cudaMalloc samples");
   CU(ctx->d_offsets.reserve(p + 1), "cudaMalloc offsets");
   CU(cudaMemsetAsync(ctx->d_samples.ptr, 0, kGuard * sizeof(double), ctx->stream), "memset");

@@ -129,18 +129,21 @@ def _walks(seed, lengths):
     return pack(rows)
 
 
-@pytest.mark.parametrize("G,R", FULL)
+FULL4 = [(2, 23), (4, 12), (8, 8), (16, 16), (32, 15), (32, 16)]
+
+
+@pytest.mark.parametrize("G,R,fam", [(g, r, 0) for g, r in FULL] + [(g, r, 3) for g, r in FULL4])
 @pytest.mark.parametrize("fp32", [False, True])
-def test_full_family_every_instantiation(eng, G, R, fp32):
+def test_full_family_every_instantiation(eng, G, R, fam, fp32):
     rng = np.random.default_rng(G * 100 + R)
     lengths = rng.integers(1, 700, size=14)
     lengths[:3] = [1, G * R, G * R + 1]
     samples, offsets = _walks(7 + G + R, lengths)
     for hw, aw in ((-1, False), (40, True), (3, True)):
-        eng.force_kernel(0, G, R)
+        eng.force_kernel(fam, G, R)
         got = eng.build_condensed(samples, offsets, hw, aw, precision=1 if fp32 else 0)
         plan = eng.last_plan()
-        assert f"full[G={G},R={R}" in plan, plan
+        assert f"full[G={G},R={R}" in plan and f"T={4 if fam == 3 else 2}" in plan, plan
         want = oracle.build_condensed(samples, offsets, hw, aw)
         if fp32:
             np.testing.assert_allclose(got, want, rtol=1e-5, atol=0)

@@ -39,6 +39,8 @@ def main():
         cands += [(1, g, r) for g, r in BAND]
     if 2 in fams:
         cands += [(2, g, r) for g, r in BAND]
+    if 3 in fams:
+        cands += [(3, g, r) for g, r in [(2, 23), (4, 12), (8, 8), (16, 16), (32, 15), (32, 16)]]
     ref = None
     for fam, g, r in [(-1, 0, 0)] + cands:
         eng.force_kernel(fam, g, r)
