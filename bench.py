@@ -303,6 +303,39 @@ def run_gpu_arm(a, ds):
                "h2d_bytes_per_step": int(ds.samples.nbytes + ds.offsets.nbytes),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": dt / a.steps * 1e3}
 
+    # k-medoids sweeps over the device-resident matrix (the second hot loop), restarts
+    # sharded over ranks and reduced in restart order.
+    kmed = None
+    if a.kmedoids and ds.k:
+        cond = full[:total] if world > 1 else mine[:total]
+        eng.adopt(None, p, on_device_ptr=cond.data_ptr())
+        eng._p_resident = p
+        eng.km_stats(reset=True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+
+        def run(rb, re_):
+            med, asg, cost, br = eng.kmedoids(p, ds.k, ds.restarts, 100, 0, rb, re_)
+            return (cost, br, med.tolist(), asg.tolist())
+
+        best = dd.kmedoids_restart_sharded(run, ds.restarts, rank, world)
+        km_s = time.perf_counter() - t0
+        st = eng.km_stats()
+        hbm = _hbm_peak()
+        kmed = {"k": ds.k, "restarts": ds.restarts, "seconds": km_s, "sweeps": st["sweeps"],
+                "total_cost": best[0], "best_restart": best[1],
+                "update_kernel": {"ms": st["update_ms"], "algorithmic_bytes": st["update_bytes"],
+                                  "achieved_gbs": st["update_bytes"] / max(st["update_ms"], 1e-9) / 1e6,
+                                  "peak_gbs": hbm[0], "peak_source": hbm[1]},
+                "assign_kernel": {"ms": st["assign_ms"], "algorithmic_bytes": st["assign_bytes"],
+                                  "achieved_gbs": st["assign_bytes"] / max(st["assign_ms"], 1e-9) / 1e6}}
+        if rank == 0 and a.check and p <= 5000:
+            import oracle
+            D = cond.cpu().numpy()
+            med, asg, cost = oracle.kmedoids(D, p, ds.k, ds.restarts, 100, 0)
+            kmed["parity"] = bool(list(med) == list(best[2]) and list(asg) == list(best[3])
+                                  and cost == best[0])
+
     cpu = None
     if rank == 0 and world == 1 and a.cpu_baseline:
         cpu = cpu_reference_sample(ds, a.ref_step_s)
@@ -334,6 +367,7 @@ def run_gpu_arm(a, ds):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
+            "kmedoids": kmed,
             "clocks": clocks,
             "parity": check,
         }
@@ -342,6 +376,15 @@ def run_gpu_arm(a, ds):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def _hbm_peak():
+    """HBM copy bandwidth measured by the driver (MEASURED_PEAKS.json), else the fallback."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(path))["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except (OSError, ValueError, KeyError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def oracle_pair(slot: int, p: int):
@@ -368,6 +411,8 @@ def main():
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-check", dest="check", action="store_false")
+    ap.add_argument("--kmedoids", action="store_true",
+                    help="also run the config's k-medoids over the resident matrix")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 0)
     from paper_2307_04904_b200 import generators as gen

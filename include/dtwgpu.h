@@ -127,6 +127,11 @@ int dtwg_kmedoids(dtwg_ctx* ctx, int64_t k, int64_t restarts, int64_t max_iterat
                   dtwg_observer_fn observer, void* user, int64_t* medoids_out,
                   int64_t* assignment_out, double* cost_out, int64_t* best_restart_out);
 
+/* k-medoids sweep statistics since the last reset: out[0] sweeps, out[1] assignment
+ * kernel ms, out[2] its algorithmic bytes (8 per distance read), out[3] update kernels
+ * ms, out[4] their algorithmic bytes (8 * sum |C|^2 + index traffic). */
+int dtwg_km_stats(dtwg_ctx* ctx, double* out, int reset);
+
 /* One sweep's pieces (cluster_result.hpp:40-72; kmedoids.hpp:48-52, 84-139). */
 int dtwg_km_nearest_update(dtwg_ctx* ctx, int64_t current, const uint8_t* chosen,
                            double* nearest_inout);

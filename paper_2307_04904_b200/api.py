@@ -181,6 +181,13 @@ class Engine:
         self.check(self.L.dtwg_measure_cell_peak(self.h, precision, C.byref(v)))
         return float(v.value)
 
+    def km_stats(self, reset: bool = False) -> dict:
+        """Sweep count and device time / algorithmic bytes of the k-medoids kernels."""
+        out = np.zeros(5, dtype=np.float64)
+        self.check(self.L.dtwg_km_stats(self.h, out, int(reset)))
+        return {"sweeps": int(out[0]), "assign_ms": out[1], "assign_bytes": out[2],
+                "update_ms": out[3], "update_bytes": out[4]}
+
     def last_plan(self) -> str:
         return self.L.dtwg_last_plan(self.h).decode()
 

@@ -255,6 +255,12 @@ struct dtwg_ctx {
   bool square_valid = false;
   DevBuf<int> d_flag;
 
+  // k-medoids sweep statistics (dtwg_km_stats): device time and algorithmic bytes of the
+  // assignment and candidate-sum kernels (8 bytes per distance read).
+  cudaEvent_t km0 = nullptr, km1 = nullptr;
+  double km_assign_ms = 0, km_update_ms = 0, km_assign_bytes = 0, km_update_bytes = 0;
+  int64_t km_sweeps = 0;
+
   // k-medoids scratch
   DevBuf<int64_t> d_medoids, d_assign, d_best_member, d_cb;
   DevBuf<double> d_dist, d_nearest, d_best_sum;
@@ -722,9 +728,11 @@ int km_assign(KmState& S, const std::vector<int64_t>& medoids) {
   CU(cudaMemcpyAsync(ctx->d_medoids.ptr, medoids.data(), medoids.size() * 8,
                      cudaMemcpyHostToDevice, ctx->stream),
      "H2D medoids");
+  CU(cudaEventRecord(ctx->km0, ctx->stream), "event");
   CU(dtwgpu::launch_assign(ctx->d_square.ptr, S.p, ctx->d_medoids.ptr, (int64_t)medoids.size(),
                            ctx->d_assign.ptr, ctx->d_dist.ptr, ctx->stream),
      "assign");
+  CU(cudaEventRecord(ctx->km1, ctx->stream), "event");
   ctx->launches++;
   S.assignment.resize(S.p);
   S.dist.resize(S.p);
@@ -735,6 +743,10 @@ int km_assign(KmState& S, const std::vector<int64_t>& medoids) {
                      ctx->stream),
      "D2H dist");
   CU(cudaStreamSynchronize(ctx->stream), "sync");
+  float ms = 0;
+  CU(cudaEventElapsedTime(&ms, ctx->km0, ctx->km1), "elapsed");
+  ctx->km_assign_ms += ms;
+  ctx->km_assign_bytes += 8.0 * (double)S.p * (double)medoids.size() + 16.0 * (double)S.p;
   return DTWG_OK;
 }
 
@@ -769,15 +781,26 @@ int km_update(KmState& S, const std::vector<int64_t>& medoids, std::vector<int64
      "H2D members");
   CU(cudaMemcpyAsync(ctx->d_cb.ptr, cb.data(), (k + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
      "H2D cb");
+  CU(cudaEventRecord(ctx->km0, ctx->stream), "event");
   CU(dtwgpu::launch_update(ctx->d_square.ptr, p, ctx->d_members.ptr, ctx->d_cb.ptr, k,
                            ctx->d_best_member.ptr, ctx->d_best_sum.ptr, ctx->stream),
      "update");
+  CU(cudaEventRecord(ctx->km1, ctx->stream), "event");
   ctx->launches += 2;
   std::vector<int64_t> best(k);
   CU(cudaMemcpyAsync(best.data(), ctx->d_best_member.ptr, k * 8, cudaMemcpyDeviceToHost,
                      ctx->stream),
      "D2H best");
   CU(cudaStreamSynchronize(ctx->stream), "sync");
+  {
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, ctx->km0, ctx->km1), "elapsed");
+    double sq = 0;
+    for (int64_t c = 0; c < k; ++c) sq += double(cb[c + 1] - cb[c]) * double(cb[c + 1] - cb[c]);
+    ctx->km_update_ms += ms;
+    ctx->km_update_bytes += 8.0 * sq + 12.0 * (double)p;
+    ctx->km_sweeps += 1;
+  }
 
   updated.assign(k, 0);
   for (int64_t c = 0; c < k; ++c) {
@@ -873,6 +896,10 @@ int km_seeds(KmState& S, int64_t k, SplitMix64& rng, std::vector<int64_t>& medoi
 }
 
 int km_reserve(dtwg_ctx* ctx, int64_t p, int64_t k) {
+  if (!ctx->km0) {
+    CU(cudaEventCreate(&ctx->km0), "event");
+    CU(cudaEventCreate(&ctx->km1), "event");
+  }
   CU(ctx->d_medoids.reserve(k), "malloc");
   CU(ctx->d_assign.reserve(p), "malloc");
   CU(ctx->d_dist.reserve(p), "malloc");
@@ -943,6 +970,8 @@ void dtwg_destroy(dtwg_ctx* ctx) {
     if (ctx->aux_done[a]) cudaEventDestroy(ctx->aux_done[a]);
   }
   if (ctx->fork) cudaEventDestroy(ctx->fork);
+  if (ctx->km0) cudaEventDestroy(ctx->km0);
+  if (ctx->km1) cudaEventDestroy(ctx->km1);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -1083,6 +1112,20 @@ int dtwg_measure_cell_peak(dtwg_ctx* ctx, int precision, double* cells_per_s) {
   cudaSetDevice(ctx->device);
   CU(dtwgpu::measure_cell_peak(ctx->stream, ctx->num_sms, precision == DTWG_FP32, cells_per_s),
      "cell peak");
+  return DTWG_OK;
+}
+
+int dtwg_km_stats(dtwg_ctx* ctx, double* out, int reset) {
+  if (!ctx || !out) return DTWG_INVALID_ARGUMENTS;
+  out[0] = (double)ctx->km_sweeps;
+  out[1] = ctx->km_assign_ms;
+  out[2] = ctx->km_assign_bytes;
+  out[3] = ctx->km_update_ms;
+  out[4] = ctx->km_update_bytes;
+  if (reset) {
+    ctx->km_sweeps = 0;
+    ctx->km_assign_ms = ctx->km_update_ms = ctx->km_assign_bytes = ctx->km_update_bytes = 0;
+  }
   return DTWG_OK;
 }
 
