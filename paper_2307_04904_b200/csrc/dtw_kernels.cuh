@@ -120,10 +120,6 @@ __device__ __forceinline__ Pair load_pair(const FillArgs& A, int64_t item) {
   return P;
 }
 
-// Value re-based from a neighbour's fp32 offset to ours (fp32 mode only).
-__device__ __forceinline__ float rebase(float v, double from, double to) {
-  return v == CUDART_INF_F ? v : (float)((double)v + (from - to));
-}
 
 // ===================================================================================
 // Full family: column strips, two rows per step, multi-pass, optional band mask.
@@ -253,11 +249,14 @@ __global__ void __launch_bounds__(kThreads) dtw_full_kernel(const FillArgs A) {
           L[t] = __shfl_up_sync(kFull, send[t], 1, G);
         }
         if constexpr (kF32) {
+          // Neighbour values are relative to its offset: add the (fp32-rounded) offset
+          // difference once per row (inf stays inf). Lane 0 reads absolute fp64 values.
           const double loff = __shfl_up_sync(kFull, send_off, 1, G);
+          const T delta = (T)(loff - off);
 #pragma unroll
           for (int t = 0; t < TR; ++t) {
-            if (gl == 0) L[t] = (b[t] == (double)INF) ? INF : (T)(b[t] - off);
-            else L[t] = rebase(L[t], loff, off);
+            if (gl == 0) L[t] = (T)(b[t] - off);
+            else L[t] = L[t] + delta;
           }
         } else {
           if (gl == 0) {
@@ -395,7 +394,7 @@ __device__ __forceinline__ void band_steps(
       T L = __shfl_up_sync(kFull, send[p], 1, G);
       if constexpr (kF32) {
         const double loff = __shfl_up_sync(kFull, send_off[p], 1, G);
-        L = rebase(L, loff, off[p]);
+        L = L + (T)(loff - off[p]);  // re-base to this lane's offset (inf stays inf)
       }
       if (gl == 0) L = INF;  // k = -1 is outside the band
       // First cell of the strip (k = lR): needs only own previous row + L.
@@ -412,7 +411,7 @@ __device__ __forceinline__ void band_steps(
       T u = __shfl_down_sync(kFull, v0[p], 1, G);
       if constexpr (kF32) {
         const double uoff = __shfl_down_sync(kFull, off[p], 1, G);
-        u = rebase(u, uoff, off[p]);
+        u = u + (T)(uoff - off[p]);
       }
       U[p] = last ? INF : u;
     }

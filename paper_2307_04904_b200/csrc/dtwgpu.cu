@@ -130,7 +130,11 @@ const Cand kBand[] = {{16, 7, 1500},    {16, 9, 1600},    {16, 11, 1700},  {16, 
                       {32, 3, 1000},    {32, 5, 1250},    {32, 7, 1490},   {32, 9, 1500},
                       {32, 13, 1450},   {32, 3, 1000, 2}, {32, 5, 1200, 2}, {32, 7, 1550, 2}};
 
-double full_cost(const Shape& s, const Cand& c, bool mask) {
+// fp32 mode: the cell is FADD FMUL FMNMX3 FADD, so the Full family runs ~2.15x the fp64
+// rate while the Band family (shuffle-heavy per step) gains only ~1.33x (measured, c2-c4).
+constexpr double kFp32Full = 2.15, kFp32Band = 1.33;
+
+double full_cost(const Shape& s, const Cand& c, bool mask, bool fp32) {
   const int64_t W = (int64_t)c.G * c.R;
   const int64_t npass = (s.m + W - 1) / W;
   double cells = 0;
@@ -144,7 +148,7 @@ double full_cost(const Shape& s, const Cand& c, bool mask) {
     // TR rows per step, G-1 steps of wavefront fill/drain
     cells += double(((re - rs + c.TR) / c.TR) * c.TR + c.TR * (c.G - 1)) * double(W);
   }
-  double rate = c.rate;
+  double rate = c.rate * (fp32 ? kFp32Full : 1.0);
   if (mask) rate *= 0.75;  // masked steps (measured on c2 / c5)
   if (npass > 1) {         // boundary-column round trips per pass (measured on c4)
     if (c.G == 2) rate *= c.TR == 4 ? 0.68 : 0.59;
@@ -154,8 +158,8 @@ double full_cost(const Shape& s, const Cand& c, bool mask) {
   return cells / rate;
 }
 
-double band_cost(const Shape& s, const Cand& c) {
-  return double(s.n + c.G - 1) * double(c.G * c.R) / c.rate;
+double band_cost(const Shape& s, const Cand& c, bool fp32) {
+  return double(s.n + c.G - 1) * double(c.G * c.R) / (c.rate * (fp32 ? kFp32Band : 1.0));
 }
 
 KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out);
@@ -168,7 +172,7 @@ KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out) {
   double bc = 1e300;
   const bool mask = s.hw < s.n - 1;  // a band that excludes some cell
   for (const Cand& c : kFull) {
-    const double cst = full_cost(s, c, mask);
+    const double cst = full_cost(s, c, mask, fp32);
     if (cst < bc) {
       bc = cst;
       best = KernelCfg{Family::Full, c.G, c.R, mask, fp32, -1, 1, c.TR};
@@ -178,7 +182,7 @@ KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out) {
     const int64_t K = 2 * s.hw + 1;
     for (const Cand& c : kBand) {
       if ((int64_t)c.G * c.R < K) continue;
-      const double cst = band_cost(s, c);
+      const double cst = band_cost(s, c, fp32);
       if (cst < bc) {
         bc = cst;
         best = KernelCfg{Family::Band, c.G, c.R, false, fp32, fp32 ? -1 : (int)(K % c.R), c.P};
