@@ -362,13 +362,12 @@ __device__ __forceinline__ void kill_cell(T (&pv)[R], int rK, T inf) {
 // pairs of one group share the step counter, so each pair's result is captured when
 // its own last row is reached (shared-memory stash, read after the loop). Series are
 // read from the +inf-padded copy (A.bsamples), so no load needs a range check.
-template <int G, int R, int KR, int P, class Ar, bool FILL>
+template <int G, int R, int KR, int P, class Ar, bool CHECK>
 __device__ __forceinline__ void band_steps(
-    int s0, int& i1, const typename Ar::T* (&xp)[P], const typename Ar::T* (&yp)[P],
+    int& i1, const typename Ar::T* (&xp)[P], const typename Ar::T* (&yp)[P],
     typename Ar::T (&xq)[P], typename Ar::T (&yq)[P], typename Ar::T (&pv)[P][R],
     typename Ar::T (&yb)[P][R], typename Ar::T (&send)[P], double (&send_off)[P],
-    double (&off)[P], const int (&n)[P], const int (&lK)[P], const int (&rK)[P],
-    const bool (&hold)[P], int gl, typename Ar::T (*stash)[P][R], double (*stash_off)[P]) {
+    double (&off)[P], const int (&n)[P], const int (&lK)[P], const int (&rK)[P], int gl) {
   using T = typename Ar::T;
   constexpr bool kF32 = sizeof(T) == 4;
   const T INF = Ar::inf();
@@ -376,10 +375,17 @@ __device__ __forceinline__ void band_steps(
 #pragma unroll
   for (int q = 0; q < R; ++q) {  // phase q: logical y[r] lives in yb[(r + q) % R]
     T x[P], v0[P], U[P];
-    // Only the first G-1 steps have lanes that have not reached row 1 yet; they keep
-    // the row-0 state. (Lanes past row n compute +inf/garbage rows: harmless, the
-    // result was stashed at row n.)
-    const bool started = FILL ? (i1 >= 1) : true;
+    // CHECK blocks (wavefront fill and drain) hold each lane to rows 1..n of each pair:
+    // before row 1 a lane keeps the row-0 state, after row n it keeps row n, which is
+    // read after the loop. Steady-state blocks compute unconditionally.
+    bool act[P];
+    bool any = false, all = true;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      act[p] = CHECK ? (i1 >= 1 && i1 <= n[p]) : true;
+      any |= act[p];
+      all &= act[p];
+    }
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       x[p] = xq[p];
@@ -399,7 +405,7 @@ __device__ __forceinline__ void band_steps(
       if (gl == 0) L = INF;  // k = -1 is outside the band
       // First cell of the strip (k = lR): needs only own previous row + L.
       T v = Ar::cell(x[p], yb[p][(q + 1) % R], Ar::mn(Ar::mn(pv[p][0], pv[p][1]), L));
-      if (FILL) v = started ? v : pv[p][0];
+      if (CHECK) v = act[p] ? v : pv[p][0];
       if (KR == 0 || KR < 0) {
         if (lK[p] == gl && rK[p] == 0) v = INF;  // k == K is this lane's first cell
       }
@@ -415,7 +421,7 @@ __device__ __forceinline__ void band_steps(
       }
       U[p] = last ? INF : u;
     }
-    if (started) {
+    if (any) {
       T left[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) left[p] = v0[p];
@@ -424,14 +430,15 @@ __device__ __forceinline__ void band_steps(
 #pragma unroll
         for (int p = 0; p < P; ++p) {
           const T up = (r < R - 1) ? pv[p][r + 1] : U[p];
-          const T v = Ar::cell(x[p], yb[p][(r + q + 1) % R],
-                               Ar::mn(Ar::mn(pv[p][r], up), left[p]));
+          T v = Ar::cell(x[p], yb[p][(r + q + 1) % R], Ar::mn(Ar::mn(pv[p][r], up), left[p]));
+          if (CHECK && P > 1 && !all) v = act[p] ? v : pv[p][r];
           pv[p][r] = v;
           left[p] = v;
         }
       }
 #pragma unroll
       for (int p = 0; p < P; ++p) {
+        if (CHECK && !act[p]) continue;
         pv[p][0] = v0[p];
         // Cell k == K lies right of the band: keep it at +inf (dtw.hpp:71). Cells
         // beyond it may hold garbage; only cell K feeds a valid cell (as "up").
@@ -454,19 +461,15 @@ __device__ __forceinline__ void band_steps(
           send_off[p] = off[p];
         }
         send[p] = pv[p][R - 1];
-        if (hold[p] && i1 == n[p]) {  // the pair's last row: stash its strip
-#pragma unroll
-          for (int r = 0; r < R; ++r) stash[threadIdx.x][p][r] = pv[p][r];
-          if constexpr (kF32) stash_off[threadIdx.x][p] = off[p];
-        }
       }
     }
     ++i1;
   }
 }
 
+// Register cap: 5 CTAs of 128 threads per SM for the single-pair variants (<= 102 regs).
 template <int G, int R, int KR, int P, class Ar>
-__global__ void __launch_bounds__(kThreads) dtw_band_kernel(const FillArgs A) {
+__global__ void __launch_bounds__(kThreads, P == 1 ? 5 : 3) dtw_band_kernel(const FillArgs A) {
   static_assert(R >= 2, "band family needs R >= 2");
   using T = typename Ar::T;
   constexpr bool kF32 = sizeof(T) == 4;
@@ -478,8 +481,6 @@ __global__ void __launch_bounds__(kThreads) dtw_band_kernel(const FillArgs A) {
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const T INF = Ar::inf();
   const T* S = Ar::bbase(A);
-  __shared__ T stash[kThreads][P][R];  // pv at the pair's last row (hold lane only)
-  __shared__ double stash_off[kF32 ? kThreads : 1][P];  // fp32: the lane's offset then
 
   for (int64_t base = warp * GPW * P; base < A.count; base += nwarps * GPW * P) {
     const T* xp[P];
@@ -488,7 +489,7 @@ __global__ void __launch_bounds__(kThreads) dtw_band_kernel(const FillArgs A) {
     int n[P], m[P], K[P], lK[P], rK[P], r_res[P];
     bool hold[P];
     int64_t slot[P];
-    int nmax = 0;
+    int nmax = 0, nmin = 1 << 30;
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       const int64_t item = base + (int64_t)gw * P + p;
@@ -511,6 +512,7 @@ __global__ void __launch_bounds__(kThreads) dtw_band_kernel(const FillArgs A) {
       hold[p] = valid && (kres / R) == gl;
       r_res[p] = kres % R;
       nmax = max(nmax, n[p]);
+      nmin = min(nmin, n[p]);
     }
     const int kbase = gl * R;
     T pv[P][R], yb[P][R];
@@ -535,22 +537,27 @@ __global__ void __launch_bounds__(kThreads) dtw_band_kernel(const FillArgs A) {
       yp[p] = Y[p] + (i1 + G * R - 1 - hw - 1);
       yq[p] = __ldg(yp[p]);
     }
-    // Steps padded to a multiple of R: surplus steps compute rows past n (harmless).
+    // Steps in blocks of R (the y-rotation period). Blocks with a lane before its row 1
+    // (fill) or past some pair's row n (drain) are checked; the rest run unconditionally.
     const int nsteps = __reduce_max_sync(kFull, nmax + G - 1);
-    const int fill_end = ((G - 1 + R - 1) / R) * R;  // steps with not-yet-started lanes
+    const int fill_end = ((G - 1 + R - 1) / R) * R;
+    const int drain_start = (__reduce_min_sync(kFull, nmin) / R) * R;
     for (int s0 = 0; s0 < nsteps; s0 += R) {
-      if (s0 < fill_end)
-        band_steps<G, R, KR, P, Ar, true>(s0, i1, xp, yp, xq, yq, pv, yb, send, send_off, off,
-                                          n, lK, rK, hold, gl, stash, stash_off);
+      if (s0 < fill_end || s0 >= drain_start)
+        band_steps<G, R, KR, P, Ar, true>(i1, xp, yp, xq, yq, pv, yb, send, send_off, off, n,
+                                          lK, rK, gl);
       else
-        band_steps<G, R, KR, P, Ar, false>(s0, i1, xp, yp, xq, yq, pv, yb, send, send_off, off,
-                                           n, lK, rK, hold, gl, stash, stash_off);
+        band_steps<G, R, KR, P, Ar, false>(i1, xp, yp, xq, yq, pv, yb, send, send_off, off, n,
+                                           lK, rK, gl);
     }
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-      if (hold[p]) {
-        double result = (double)stash[threadIdx.x][p][r_res[p]];
-        if constexpr (kF32) result += stash_off[threadIdx.x][p];
+      if (hold[p]) {  // pv holds row n
+        T rv = pv[p][0];
+#pragma unroll
+        for (int r = 1; r < R; ++r) rv = (r == r_res[p]) ? pv[p][r] : rv;
+        double result = (double)rv;
+        if constexpr (kF32) result += off[p];
         A.out[slot[p] - A.out_base] = result;
       }
     }

@@ -128,7 +128,7 @@ const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026}
                       {32, 16, 2050, 1, 4}};
 const Cand kBand[] = {{16, 7, 1500},    {16, 9, 1600},    {16, 11, 1700},  {16, 13, 1800},
                       {32, 3, 1000},    {32, 5, 1250},    {32, 7, 1490},   {32, 9, 1500},
-                      {32, 13, 1450},   {32, 3, 1000, 2}, {32, 5, 1200, 2}, {32, 7, 1550, 2}};
+                      {32, 13, 1450},   {32, 3, 600, 2},  {32, 5, 600, 2},  {32, 7, 700, 2}};
 
 // fp32 mode: the cell is FADD FMUL FMNMX3 FADD, so the Full family runs ~2.15x the fp64
 // rate while the Band family (shuffle-heavy per step) gains only ~1.33x (measured, c2-c4).

@@ -265,3 +265,21 @@ def test_memory_scale_long_pair(eng):
     samples, offsets = pack([x, y])
     got = eng.build_condensed(samples, offsets, -1)
     assert got[0] == oracle.dtw(x, y, -1)
+
+
+@pytest.mark.slow
+def test_config4_fp32_full_matrix_error_histogram(eng):
+    """fp32 mode on ALL 499,500 pairs of c4 (L=2844) against the bit-exact
+    fp64 fill (itself equal to the reference): max relative error <= 1e-5."""
+    import torch
+    ds = gen.config4()
+    eng.upload(ds.samples, ds.offsets)
+    total = ds.p * (ds.p - 1) // 2
+    a = torch.empty(total, dtype=torch.float64, device="cuda")
+    b = torch.empty(total, dtype=torch.float64, device="cuda")
+    eng.fill_slots(-1, False, 0, 0, total, a.data_ptr())
+    eng.fill_slots(-1, False, 1, 0, total, b.data_ptr())
+    rel = ((b - a).abs() / a.abs()).cpu().numpy()
+    hist = np.histogram(np.log10(np.maximum(rel, 1e-16)), bins=[-16, -9, -8, -7, -6, -5.5, -5, 0])
+    print("fp32 rel-error histogram (log10 bins):", hist[0].tolist(), "max", rel.max())
+    assert rel.max() <= 1e-5, rel.max()
