@@ -29,7 +29,7 @@ struct FillArgs {
   const int64_t* boffsets;  // start of series i inside bsamples
 };
 
-constexpr int kBandPad = 512;  // >= hw + G + G*R for every band instantiation
+constexpr int kBandPad = 640;  // >= hw + G + G*R (+3 ring chunks) for every band instantiation
 
 enum class Family : int { Full = 0, Band = 1 };
 
@@ -44,6 +44,7 @@ struct KernelCfg {
   int kr = -1;  // Band family: (2hw+1) % R when every pair of the launch shares it, else -1
   int P = 1;    // Band family: pairs per lane group (independent chains per lane)
   int TR = 2;   // Full family: rows per step (independent chains per lane)
+  bool ring = false;  // Band family: y window in a shared-memory ring instead of registers
 };
 
 // Launches cfg over args on stream with `blocks` CTAs of kThreads threads.

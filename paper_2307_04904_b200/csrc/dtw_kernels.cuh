@@ -343,6 +343,7 @@ __global__ void __launch_bounds__(kThreads) dtw_full_kernel(const FillArgs A) {
 // pv[rK] = inf for a uniform runtime rK: one jump-table branch instead of R selects.
 template <int R, class T>
 __device__ __forceinline__ void kill_cell(T (&pv)[R], int rK, T inf) {
+  static_assert(R <= 32, "kill_cell handles R <= 32");
   switch (rK) {
 #define DTWG_KILL(c) \
   case c:            \
@@ -350,7 +351,9 @@ __device__ __forceinline__ void kill_cell(T (&pv)[R], int rK, T inf) {
     break;
     DTWG_KILL(1) DTWG_KILL(2) DTWG_KILL(3) DTWG_KILL(4) DTWG_KILL(5) DTWG_KILL(6) DTWG_KILL(7)
     DTWG_KILL(8) DTWG_KILL(9) DTWG_KILL(10) DTWG_KILL(11) DTWG_KILL(12) DTWG_KILL(13)
-    DTWG_KILL(14) DTWG_KILL(15)
+    DTWG_KILL(14) DTWG_KILL(15) DTWG_KILL(16) DTWG_KILL(17) DTWG_KILL(18) DTWG_KILL(19)
+    DTWG_KILL(20) DTWG_KILL(21) DTWG_KILL(22) DTWG_KILL(23) DTWG_KILL(24) DTWG_KILL(25)
+    DTWG_KILL(26) DTWG_KILL(27) DTWG_KILL(28) DTWG_KILL(29) DTWG_KILL(30) DTWG_KILL(31)
 #undef DTWG_KILL
     default:
       break;
@@ -561,6 +564,178 @@ __global__ void __launch_bounds__(kThreads, P == 1 ? 5 : 3) dtw_band_kernel(cons
         A.out[slot[p] - A.out_base] = result;
       }
     }
+  }
+}
+
+// ===================================================================================
+// Band family, shared-memory y variant ("ring"): same sheared coordinates and cell
+// dependencies as dtw_band_kernel, but the sliding y window lives in a per-group ring
+// in shared memory (read with immediate offsets, one LDS per cell) instead of rotating
+// through R registers. That frees 2R registers (more resident warps to cover the
+// 29-cycle cell chain) and removes the R-fold unrolled loop body (I-cache).
+// Ring: 256 slots (+R duplicated so a lane's R reads never wrap), refilled 32 samples at
+// a time from the +inf-padded series, one chunk ahead.
+// ===================================================================================
+constexpr int kRing = 256;
+
+template <int G, int R, int KR, class Ar, bool CHECK>
+__device__ __forceinline__ void ring_steps(int nst, int& i1, const typename Ar::T*& xp,
+                                           typename Ar::T& xq, int& b, const typename Ar::T* ring,
+                                           typename Ar::T (&pv)[R], typename Ar::T& send,
+                                           double& send_off, double& off, int n, int lK, int rK,
+                                           int gl) {
+  using T = typename Ar::T;
+  constexpr bool kF32 = sizeof(T) == 4;
+  const T INF = Ar::inf();
+  const bool last = gl == G - 1;
+#pragma unroll 2
+  for (int q = 0; q < nst; ++q) {
+    const bool act = CHECK ? (i1 >= 1 && i1 <= n) : true;
+    const T x = xq;
+    xq = __ldg(++xp);
+    const T* yr = ring + b;
+    T L = __shfl_up_sync(kFull, send, 1, G);
+    if constexpr (kF32) {
+      const double loff = __shfl_up_sync(kFull, send_off, 1, G);
+      L = L + (T)(loff - off);
+    }
+    if (gl == 0) L = INF;
+    T v0 = Ar::cell(x, yr[0], Ar::mn(Ar::mn(pv[0], pv[1]), L));
+    if (CHECK) v0 = act ? v0 : pv[0];
+    if (KR == 0 || KR < 0) {
+      if (lK == gl && rK == 0) v0 = INF;
+    }
+    T U = __shfl_down_sync(kFull, v0, 1, G);
+    if constexpr (kF32) {
+      const double uoff = __shfl_down_sync(kFull, off, 1, G);
+      U = U + (T)(uoff - off);
+    }
+    U = last ? INF : U;
+    if (act) {
+      T left = v0;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const T up = (r < R - 1) ? pv[r + 1] : U;
+        const T v = Ar::cell(x, yr[r], Ar::mn(Ar::mn(pv[r], up), left));
+        pv[r] = v;
+        left = v;
+      }
+      pv[0] = v0;
+      if constexpr (KR > 0) {
+        if (lK == gl) pv[KR] = INF;
+      } else if constexpr (KR < 0) {
+        if (lK == gl && rK != 0) kill_cell<R>(pv, rK, INF);
+      }
+      if constexpr (kF32) {
+        if (((i1 - 1) & (kRenormSteps - 1)) == kRenormSteps - 1) {
+          T mnv = pv[0];
+#pragma unroll
+          for (int r = 1; r < R; ++r) mnv = Ar::mn(mnv, pv[r]);
+          if (mnv != INF) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) pv[r] = __fsub_rn(pv[r], mnv);
+            off += (double)mnv;
+          }
+        }
+        send_off = off;
+      }
+      send = pv[R - 1];
+    }
+    b = (b + 1) & (kRing - 1);
+    ++i1;
+  }
+}
+
+template <int G, int R, int KR, class Ar>
+__global__ void __launch_bounds__(kThreads) dtw_bandring_kernel(const FillArgs A) {
+  static_assert(R >= 2, "band family needs R >= 2");
+  static_assert(G * R - G <= kRing - 33, "ring too small for this band width");
+  // Lane l's window starts l*(R-1) slots after lane 0's: with R-1 odd the 8-byte reads
+  // of a warp hit distinct bank pairs (conflict-free); even R-1 would serialise them.
+  static_assert((R - 1) % 2 == 1, "ring variant needs even R (bank-conflict-free reads)");
+  using T = typename Ar::T;
+  constexpr int GPW = 32 / G;
+  constexpr int C = 32;           // samples per refill chunk (= steps per chunk)
+  constexpr int PER = C / G;      // chunk samples loaded by each lane
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % G;
+  const int gw = lane / G;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const T INF = Ar::inf();
+  const T* S = Ar::bbase(A);
+  __shared__ T rings[kThreads / G][kRing + R];
+  T* ring = rings[threadIdx.x / G];
+  constexpr int JOFF = 4 * kRing;  // keeps ring indices of j >= 1 - hw - G non-negative
+
+  for (int64_t base = warp * GPW; base < A.count; base += nwarps * GPW) {
+    const int64_t item = base + gw;
+    const bool valid = item < A.count;
+    const Pair Pp = load_pair(A, valid ? item : base);
+    int64_t a, bb;
+    decode_slot(Pp.slot, A.p, a, bb);
+    const bool a_rows =
+        (A.offsets[a + 1] - A.offsets[a]) >= (A.offsets[bb + 1] - A.offsets[bb]);
+    const T* Y = S + A.boffsets[a_rows ? bb : a];
+    const T* xp = S + A.boffsets[a_rows ? a : bb];
+    const int n = Pp.n, m = Pp.m, hw = Pp.hw;
+    const int K = 2 * hw + 1;
+    const int lK = K / R;
+    const int rK = KR >= 0 ? KR : K % R;
+    const int kres = m - n + hw;
+    const bool hold = valid && (kres / R) == gl;
+    const int r_res = kres % R;
+    const int kbase = gl * R;
+    const int D = G * R - G + 2 - hw;  // first sample index of the chunk written at step 0
+
+    // Ring prologue: samples j in [1 - hw, D) before step 0; chunk c (j in [32c + D,
+    // 32c + D + 32)) is written at step 32c from registers loaded one chunk ahead.
+    auto put = [&](int j, T v) {
+      const int slot = (j + JOFF) & (kRing - 1);
+      ring[slot] = v;
+      if (slot < R) ring[slot + kRing] = v;
+    };
+    for (int j = 1 - hw + gl; j < D; j += G) put(j, __ldg(Y + (j - 1)));
+    T chunk[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) chunk[u] = __ldg(Y + (D + gl + u * G - 1));
+
+    T pv[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) pv[r] = (kbase + r == hw) ? T(0) : INF;  // row 0
+    T send = INF;
+    double off = 0.0, send_off = 0.0;
+    int i1 = 1 - gl;
+    xp += i1 - 1;
+    T xq = __ldg(xp);
+    int b = (i1 + kbase - hw + JOFF) & (kRing - 1);
+    const int nsteps = __reduce_max_sync(kFull, n + G - 1);
+    const int fill_end = ((G - 1 + C - 1) / C) * C;
+    const int drain_start = (__reduce_min_sync(kFull, n) / C) * C;
+    for (int s0 = 0; s0 < nsteps; s0 += C) {
+      // write chunk s0/C, prefetch the next one
+#pragma unroll
+      for (int u = 0; u < PER; ++u) put(s0 + D + gl + u * G, chunk[u]);
+#pragma unroll
+      for (int u = 0; u < PER; ++u) chunk[u] = __ldg(Y + (s0 + C + D + gl + u * G - 1));
+      __syncwarp();
+      if (s0 < fill_end || s0 >= drain_start)
+        ring_steps<G, R, KR, Ar, true>(C, i1, xp, xq, b, ring, pv, send, send_off, off, n, lK, rK,
+                                       gl);
+      else
+        ring_steps<G, R, KR, Ar, false>(C, i1, xp, xq, b, ring, pv, send, send_off, off, n, lK,
+                                        rK, gl);
+      __syncwarp();
+    }
+    if (hold) {
+      T rv = pv[0];
+#pragma unroll
+      for (int r = 1; r < R; ++r) rv = (r == r_res) ? pv[r] : rv;
+      double result = (double)rv;
+      if constexpr (sizeof(T) == 4) result += off;
+      A.out[Pp.slot - A.out_base] = result;
+    }
+    __syncwarp();
   }
 }
 

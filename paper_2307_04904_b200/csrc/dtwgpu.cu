@@ -119,6 +119,7 @@ struct Cand {
   double rate;  // computed lane-cells / ns
   int P = 1;    // band family: pairs per lane group
   int TR = 2;   // full family: rows per step
+  bool ring = false;  // band family: shared-memory y ring
 };
 const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026},
                       {4, 12, 1956, 1, 4},   {8, 8, 1804},         {8, 8, 1700, 1, 4},
@@ -128,7 +129,10 @@ const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026}
                       {32, 16, 2050, 1, 4}};
 const Cand kBand[] = {{16, 7, 1500},    {16, 9, 1600},    {16, 11, 1700},  {16, 13, 1800},
                       {32, 3, 1000},    {32, 5, 1250},    {32, 7, 1490},   {32, 9, 1500},
-                      {32, 13, 1450},   {32, 3, 600, 2},  {32, 5, 600, 2},  {32, 7, 700, 2}};
+                      {32, 13, 1450},   {32, 3, 600, 2},  {32, 5, 600, 2},  {32, 7, 700, 2},
+                      {8, 16, 1900, 1, 2, true},  {8, 26, 2130, 1, 2, true},
+                      {16, 8, 1500, 1, 2, true},  {16, 14, 1900, 1, 2, true},
+                      {32, 6, 1300, 1, 2, true}};
 
 // fp32 mode: the cell is FADD FMUL FMNMX3 FADD, so the Full family runs ~2.15x the fp64
 // rate while the Band family (shuffle-heavy per step) gains only ~1.33x (measured, c2-c4).
@@ -159,7 +163,9 @@ double full_cost(const Shape& s, const Cand& c, bool mask, bool fp32) {
 }
 
 double band_cost(const Shape& s, const Cand& c, bool fp32) {
-  return double(s.n + c.G - 1) * double(c.G * c.R) / (c.rate * (fp32 ? kFp32Band : 1.0));
+  // the smem-ring variant keeps more of the fp32 gain (fewer registers, ~1.5x measured)
+  const double f32 = c.ring ? 1.5 : kFp32Band;
+  return double(s.n + c.G - 1) * double(c.G * c.R) / (c.rate * (fp32 ? f32 : 1.0));
 }
 
 KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out);
@@ -185,7 +191,8 @@ KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out) {
       const double cst = band_cost(s, c, fp32);
       if (cst < bc) {
         bc = cst;
-        best = KernelCfg{Family::Band, c.G, c.R, false, fp32, fp32 ? -1 : (int)(K % c.R), c.P};
+        best = KernelCfg{Family::Band, c.G, c.R, false, fp32, fp32 ? -1 : (int)(K % c.R), c.P,
+                         2, c.ring};
       }
     }
   }
@@ -296,12 +303,13 @@ namespace {
 KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cost_out) {
   const bool mask = s.hw < s.n - 1;
   if (ctx->force_family >= 0) {
-    // 0: full (2 rows/step), 1: band P=1, 2: band P=2, 3: full (4 rows/step)
-    const bool band = ctx->force_family == 1 || ctx->force_family == 2;
+    // 0: full (2 rows/step), 1: band P=1, 2: band P=2, 3: full (4 rows/step), 4: band ring
+    const bool band = ctx->force_family == 1 || ctx->force_family == 2 || ctx->force_family == 4;
     KernelCfg f{band ? Family::Band : Family::Full, ctx->force_G, ctx->force_R,
                 band ? false : mask, fp32,
                 (band && !fp32 && ctx->force_R > 0) ? (int)((2 * s.hw + 1) % ctx->force_R) : -1,
-                ctx->force_family == 2 ? 2 : 1, ctx->force_family == 3 ? 4 : 2};
+                ctx->force_family == 2 ? 2 : 1, ctx->force_family == 3 ? 4 : 2,
+                ctx->force_family == 4};
     const bool ok = dtwgpu::fill_cfg_supported(f) &&
                     (f.family == Family::Full ||
                      (mask && f.R >= 2 && (int64_t)f.G * f.R >= 2 * s.hw + 1));
@@ -403,7 +411,8 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
     }
     double cst = 0;
     const KernelCfg cfg = choose_cfg(ctx, s, fp32, &cst);
-    const auto key = std::make_tuple((int)cfg.family, cfg.G, cfg.R, cfg.mask, cfg.kr, cfg.P, cfg.TR);
+    const auto key = std::make_tuple((int)cfg.family * 2 + (int)cfg.ring, cfg.G, cfg.R, cfg.mask,
+                                     cfg.kr, cfg.P, cfg.TR);
     int cls;
     auto ic = cls_of_cfg.find(key);
     if (ic == cls_of_cfg.end()) {
@@ -653,8 +662,9 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
     char buf[160];
     char krs[32] = "";
     if (pc.cfg.family == Family::Band)
-      snprintf(krs, sizeof(krs), "%s,P=%d", pc.cfg.kr >= 0 ? (",kr=" + std::to_string(pc.cfg.kr)).c_str() : "",
-               pc.cfg.P);
+      snprintf(krs, sizeof(krs), "%s,P=%d%s",
+               pc.cfg.kr >= 0 ? (",kr=" + std::to_string(pc.cfg.kr)).c_str() : "", pc.cfg.P,
+               pc.cfg.ring ? ",ring" : "");
     if (pc.cfg.family == Family::Full) snprintf(krs, sizeof(krs), ",T=%d", pc.cfg.TR);
     snprintf(buf, sizeof(buf), "%s%s[G=%d,R=%d%s%s%s] pairs=%lld blocks=%lld(%d/SM)",
              ctx->last_plan.empty() ? "" : "; ", family_name(pc.cfg.family), pc.cfg.G, pc.cfg.R,

@@ -8,6 +8,7 @@ namespace dtwgpu {
 
 static const void* kernel_ptr(const KernelCfg& c) {
   if (c.family == Family::Full) return full_kernel_ptr(c.G, c.R, c.TR, c.mask, c.fp32);
+  if (c.ring) return c.P == 1 ? ring_kernel_ptr(c.G, c.R, c.kr, c.fp32) : nullptr;
   if (c.G == 16) return band16_kernel_ptr(c.R, c.kr, c.P, c.fp32);
   if (c.G == 32) return band32_kernel_ptr(c.R, c.kr, c.P, c.fp32);
   return nullptr;

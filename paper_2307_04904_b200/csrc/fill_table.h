@@ -8,9 +8,12 @@
   X(32, 15, 4) X(32, 16, 4)
 #define DTWG_BAND_CFGS_G16(X) X(16, 7) X(16, 9) X(16, 11) X(16, 13)
 #define DTWG_BAND_CFGS_G32(X) X(32, 3) X(32, 5) X(32, 7) X(32, 9) X(32, 13)
+// Band family, shared-memory y ring variant
+#define DTWG_RING_CFGS(X) X(8, 16) X(8, 26) X(16, 8) X(16, 14) X(32, 6)
 
 namespace dtwgpu {
 const void* full_kernel_ptr(int G, int R, int TR, bool mask, bool fp32);
 const void* band16_kernel_ptr(int R, int kr, int P, bool fp32);
 const void* band32_kernel_ptr(int R, int kr, int P, bool fp32);
+const void* ring_kernel_ptr(int G, int R, int kr, bool fp32);
 }  // namespace dtwgpu

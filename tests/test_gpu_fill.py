@@ -151,9 +151,12 @@ def test_full_family_every_instantiation(eng, G, R, fam, fp32):
             assert_bitwise(got, want, f"full G={G} R={R} hw={hw}")
 
 
-@pytest.mark.parametrize("G,R", BAND)
+RING = [(8, 16), (8, 26), (16, 8), (16, 14), (32, 6)]
+
+
+@pytest.mark.parametrize("G,R,family", [(g, r, f) for g, r in BAND for f in (1, 2)] +
+                         [(g, r, 4) for g, r in RING])  # 2: two pairs/group, 4: smem ring
 @pytest.mark.parametrize("fp32", [False, True])
-@pytest.mark.parametrize("family", [1, 2])  # 2 = two pairs per lane group
 def test_band_family_every_instantiation(eng, G, R, fp32, family):
     rng = np.random.default_rng(G * 1000 + R)
     kmax = G * R

@@ -39,6 +39,8 @@ def main():
         cands += [(1, g, r) for g, r in BAND]
     if 2 in fams:
         cands += [(2, g, r) for g, r in BAND]
+    if 4 in fams:
+        cands += [(4, g, r) for g, r in [(8, 16), (8, 26), (16, 8), (16, 14), (32, 6)]]
     if 3 in fams:
         cands += [(3, g, r) for g, r in [(2, 23), (4, 12), (8, 8), (16, 16), (32, 15), (32, 16)]]
     ref = None
