@@ -175,8 +175,16 @@ def run_gpu_arm(a, ds):
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
+    # --dist-backend gloo (diagnostic): several ranks may then share one GPU; slices are
+    # all-gathered through host memory. The product path is NCCL, one GPU per rank.
+    gloo = a.dist_backend == "gloo"
+    if gloo and world > 1:
+        local = local % max(torch.cuda.device_count(), 1)
     if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)  # a real stream: fill, all-gather and events share it
@@ -201,7 +209,18 @@ def run_gpu_arm(a, ds):
         if e > b:
             eng.fill_slots(ds.half_width, ds.auto_widen, prec, b, e, mine.data_ptr())
         if world > 1:
-            dist.all_gather_into_tensor(full, mine)
+            if gloo:
+                host = full.cpu()
+                dist.all_gather_into_tensor(host, host[rank * width:(rank + 1) * width].clone())
+                full.copy_(host)
+            else:
+                dist.all_gather_into_tensor(full, mine)
+
+    def assembled():
+        """The gathered slices in condensed order (ragged shards are padded to `width`)."""
+        if world == 1:
+            return mine[:total]
+        return torch.cat([full[r * width:r * width + (ee - bb)] for r, (bb, ee) in enumerate(bounds)])
 
     for _ in range(max(a.warmup, 0)):
         step()
@@ -231,7 +250,7 @@ def run_gpu_arm(a, ds):
     step_ms = [s.elapsed_time(t) for s, t in evs]
     launches = eng.launch_count() - launches0
     my_ms = sum(step_ms)
-    t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([my_ms], dtype=torch.float64, device="cpu" if gloo else dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
@@ -241,17 +260,20 @@ def run_gpu_arm(a, ds):
     check = None
     if rank == 0 and a.check:
         import oracle
-        got = full[:width].cpu().numpy() if world > 1 else mine[: e - b].cpu().numpy()
+        # world > 1: check the assembled (all-gathered) matrix; else this rank's slice
+        lo, hi = (0, total) if world > 1 else (b, e)
+        got_all = assembled() if world > 1 else mine[: e - b]
+        got = got_all.cpu().numpy()
         rng = np.random.default_rng(0)
-        picks = rng.choice(max(min(e - b, width), 1), size=min(8, max(e - b, 1)), replace=False)
+        picks = rng.choice(max(hi - lo, 1), size=min(8, max(hi - lo, 1)), replace=False)
         ok = 0
         for s_ in picks:
-            s_ = int(s_) + b
+            s_ = int(s_) + lo
             i, j = oracle_pair(s_, p)
             want = oracle.dtw(ds.series(i), ds.series(j),
                               int(gen.effective_half_width(ds.lengths[i], ds.lengths[j],
                                                            ds.half_width, ds.auto_widen)))
-            g = got[s_ - b]
+            g = got[s_ - lo]
             ok += int(g == want if prec == 0 else abs(g - want) <= 1e-5 * abs(want))
         check = f"{ok}/{len(picks)} sampled pairs match the oracle"
 
@@ -295,7 +317,7 @@ def run_gpu_arm(a, ds):
                 host[: e - b].copy_(mine[: e - b], non_blocking=True)
                 torch.cuda.synchronize()
             dt = time.perf_counter() - t0
-            tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+            tt = torch.tensor([dt], dtype=torch.float64, device="cpu" if gloo else dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             dt = float(tt.item())
             d2h = (e - b) * 8
@@ -307,7 +329,7 @@ def run_gpu_arm(a, ds):
     # sharded over ranks and reduced in restart order.
     kmed = None
     if a.kmedoids and ds.k:
-        cond = full[:total] if world > 1 else mine[:total]
+        cond = assembled().contiguous()
         eng.adopt(None, p, on_device_ptr=cond.data_ptr())
         eng._p_resident = p
         eng.km_stats(reset=True)
@@ -411,12 +433,18 @@ def main():
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-check", dest="check", action="store_false")
+    ap.add_argument("--subset", type=int, default=0,
+                    help="diagnostics: only the first N series of the config")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: diagnostic multi-rank run (ranks may share a GPU)")
     ap.add_argument("--kmedoids", action="store_true",
                     help="also run the config's k-medoids over the resident matrix")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 0)
     from paper_2307_04904_b200 import generators as gen
     ds = gen.make_config(a.config)
+    if a.subset:
+        ds = ds.subset(a.subset)
     if a.impl == "reference":
         return run_reference_arm(a, ds)
     return run_gpu_arm(a, ds)

@@ -664,7 +664,11 @@ __global__ void __launch_bounds__(kThreads) dtw_bandring_kernel(const FillArgs A
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const T INF = Ar::inf();
   const T* S = Ar::bbase(A);
-  __shared__ T rings[kThreads / G][kRing + R];
+  // Ring stride = 8 (mod 16) slots: lane l of group g reads slot base + g*stride + l*(R-1)
+  // (+r); with R-1 odd one group covers 8 of the 16 bank pairs and the next group (shifted
+  // by 8) the other 8, so a half-warp of 8-byte reads is conflict-free.
+  constexpr int kStride = ((kRing + R + 7) / 16) * 16 + 8;
+  __shared__ T rings[kThreads / G][kStride];
   T* ring = rings[threadIdx.x / G];
   constexpr int JOFF = 4 * kRing;  // keeps ring indices of j >= 1 - hw - G non-negative
 

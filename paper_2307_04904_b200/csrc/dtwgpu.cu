@@ -237,6 +237,7 @@ struct dtwg_ctx {
   };
   bool plan_valid = false;
   PlanKey plan_key{};
+  std::vector<int64_t> plan_lens;
   std::vector<PlanClass> plan_cache;
   bool list_uploaded = false;
 
@@ -244,7 +245,6 @@ struct dtwg_ctx {
   int64_t p = 0;
   std::vector<int64_t> h_offsets;
   std::vector<int64_t> h_len;
-  std::vector<double> h_samples;  // kept for fp32 conversion
   bool uniform = true;
   DevBuf<double> d_samples;
   DevBuf<float> d_samples32;
@@ -494,21 +494,18 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
 
 int ensure_fp32(dtwg_ctx* ctx) {
   if (ctx->have32) return DTWG_OK;
-  std::vector<float> f(ctx->h_samples.size());
-  for (size_t t = 0; t < f.size(); ++t) f[t] = static_cast<float>(ctx->h_samples[t]);
-  CU(ctx->d_samples32.reserve(f.size() + 2 * kGuard), "cudaMalloc samples32");
-  CU(cudaMemsetAsync(ctx->d_samples32.ptr, 0, (f.size() + 2 * kGuard) * sizeof(float),
-                     ctx->stream),
-     "memset samples32");
-  CU(cudaMemcpyAsync(ctx->d_samples32.ptr + kGuard, f.data(), f.size() * sizeof(float),
-                     cudaMemcpyHostToDevice, ctx->stream),
-     "H2D samples32");
-  CU(cudaStreamSynchronize(ctx->stream), "sync");
+  // the whole guarded buffer, guards included (zeros stay zeros)
+  const int64_t total = ctx->h_offsets[ctx->p] + 2 * kGuard;
+  CU(ctx->d_samples32.reserve(total), "cudaMalloc samples32");
+  CU(dtwgpu::launch_to_f32(ctx->d_samples.ptr, total, ctx->d_samples32.ptr, ctx->stream),
+     "to f32");
+  ctx->launches++;
   ctx->have32 = true;
   return DTWG_OK;
 }
 
-// Band-family copy of the series: each series surrounded by kBandPad +inf samples.
+// Band-family copy of the series: each series surrounded by kBandPad +inf samples,
+// scattered on the device from the packed (guarded) series.
 int ensure_band(dtwg_ctx* ctx, bool fp32) {
   if (fp32 ? ctx->have_band32 : ctx->have_band64) return DTWG_OK;
   const int64_t p = ctx->p;
@@ -525,29 +522,19 @@ int ensure_band(dtwg_ctx* ctx, bool fp32) {
   CU(cudaMemcpyAsync(ctx->d_boffsets.ptr, boff.data(), (p + 1) * 8, cudaMemcpyHostToDevice,
                      ctx->stream),
      "H2D boffsets");
+  void* out;
   if (fp32) {
-    std::vector<float> h(total, std::numeric_limits<float>::infinity());
-    for (int64_t i = 0; i < p; ++i)
-      for (int64_t t = 0; t < ctx->h_len[i]; ++t)
-        h[boff[i] + t] = static_cast<float>(ctx->h_samples[ctx->h_offsets[i] + t]);
     CU(ctx->d_bsamples32.reserve(total), "cudaMalloc bsamples32");
-    CU(cudaMemcpyAsync(ctx->d_bsamples32.ptr, h.data(), total * 4, cudaMemcpyHostToDevice,
-                       ctx->stream),
-       "H2D bsamples32");
-    CU(cudaStreamSynchronize(ctx->stream), "sync");
-    ctx->have_band32 = true;
+    out = ctx->d_bsamples32.ptr;
   } else {
-    std::vector<double> h(total, kInf);
-    for (int64_t i = 0; i < p; ++i)
-      std::copy(ctx->h_samples.begin() + ctx->h_offsets[i],
-                ctx->h_samples.begin() + ctx->h_offsets[i] + ctx->h_len[i], h.begin() + boff[i]);
     CU(ctx->d_bsamples.reserve(total), "cudaMalloc bsamples");
-    CU(cudaMemcpyAsync(ctx->d_bsamples.ptr, h.data(), total * 8, cudaMemcpyHostToDevice,
-                       ctx->stream),
-       "H2D bsamples");
-    CU(cudaStreamSynchronize(ctx->stream), "sync");
-    ctx->have_band64 = true;
+    out = ctx->d_bsamples.ptr;
   }
+  CU(dtwgpu::launch_band_pad(ctx->d_samples.ptr + kGuard, ctx->d_offsets.ptr, ctx->d_boffsets.ptr,
+                             p, pad, out, fp32, ctx->stream),
+     "band pad");
+  ctx->launches++;
+  (fp32 ? ctx->have_band32 : ctx->have_band64) = true;
   return DTWG_OK;
 }
 
@@ -1038,16 +1025,18 @@ int dtwg_upload_series(dtwg_ctx* ctx, const double* samples, const int64_t* offs
     if (ctx->h_len[i] != ctx->h_len[0]) ctx->uniform = false;
   }
   const int64_t n = ctx->h_offsets[p];
-  ctx->h_samples.assign(samples + base, samples + base + n);
   ctx->have32 = false;
   ctx->have_band64 = ctx->have_band32 = false;
-  ctx->plan_valid = false;
+  // The plan depends only on the series lengths (and window/precision/range): keep it
+  // when a new upload has the same lengths.
+  if (ctx->plan_valid && ctx->plan_lens != ctx->h_len) ctx->plan_valid = false;
+  if (!ctx->plan_valid) ctx->plan_lens = ctx->h_len;
   CU(ctx->d_samples.reserve(n + 2 * kGuard), "cudaMalloc samples");
   CU(ctx->d_offsets.reserve(p + 1), "cudaMalloc offsets");
   CU(cudaMemsetAsync(ctx->d_samples.ptr, 0, kGuard * sizeof(double), ctx->stream), "memset");
   CU(cudaMemsetAsync(ctx->d_samples.ptr + kGuard + n, 0, kGuard * sizeof(double), ctx->stream),
      "memset");
-  CU(cudaMemcpyAsync(ctx->d_samples.ptr + kGuard, ctx->h_samples.data(), n * sizeof(double),
+  CU(cudaMemcpyAsync(ctx->d_samples.ptr + kGuard, samples + base, n * sizeof(double),
                      cudaMemcpyHostToDevice, ctx->stream),
      "H2D samples");
   CU(cudaMemcpyAsync(ctx->d_offsets.ptr, ctx->h_offsets.data(), (p + 1) * sizeof(int64_t),

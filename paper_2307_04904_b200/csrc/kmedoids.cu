@@ -180,6 +180,28 @@ __global__ void cluster_argmin_kernel(const int32_t* __restrict__ members,
   }
 }
 
+// Band-family series copy: series i at bsamples[boff[i] .. + len), surrounded by pad
+// +inf samples (built on the device from the packed series).
+template <class T>
+__global__ void band_pad_kernel(const double* __restrict__ samples, const int64_t* __restrict__ off,
+                                const int64_t* __restrict__ boff, int64_t p, int64_t pad,
+                                T* __restrict__ out) {
+  const T inf = (T)CUDART_INF;
+  for (int64_t i = blockIdx.x; i < p; i += gridDim.x) {
+    const int64_t s0 = off[i], len = off[i + 1] - s0, d0 = boff[i];
+    for (int64_t t = threadIdx.x; t < len + 2 * pad; t += blockDim.x) {
+      const int64_t k = t - pad;
+      out[d0 - pad + t] = (k >= 0 && k < len) ? (T)samples[s0 + k] : inf;
+    }
+  }
+}
+
+__global__ void to_f32_kernel(const double* __restrict__ in, int64_t n, float* __restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = (float)in[t];
+}
+
 int grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   if (g > 148 * 32) g = 148 * 32;
@@ -187,6 +209,21 @@ int grid_for(int64_t n, int threads) {
 }
 
 }  // namespace
+
+cudaError_t launch_band_pad(const double* samples, const int64_t* off, const int64_t* boff,
+                            int64_t p, int64_t pad, void* out, bool fp32, cudaStream_t s) {
+  const unsigned blocks = (unsigned)(p < 148 * 16 ? p : 148 * 16);
+  if (fp32)
+    band_pad_kernel<float><<<blocks, 256, 0, s>>>(samples, off, boff, p, pad, (float*)out);
+  else
+    band_pad_kernel<double><<<blocks, 256, 0, s>>>(samples, off, boff, p, pad, (double*)out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_to_f32(const double* in, int64_t n, float* out, cudaStream_t s) {
+  to_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(in, n, out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_expand_square(const double* condensed, int64_t p, double* square,
                                  cudaStream_t s) {
