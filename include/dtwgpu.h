@@ -38,6 +38,7 @@ enum {
   DTWG_K_OUT_OF_RANGE = 10,
   DTWG_DISTANCE_MATRIX_INVALID = 11,
   DTWG_INDEX_OUT_OF_RANGE = 12,
+  DTWG_SINGLE_CLUSTER_UNDEFINED = 13,
   DTWG_CUDA_ERROR = 100,
   DTWG_NO_DEVICE = 101,
   DTWG_INTERNAL = 102
@@ -131,6 +132,15 @@ int dtwg_kmedoids(dtwg_ctx* ctx, int64_t k, int64_t restarts, int64_t max_iterat
  * kernel ms, out[2] its algorithmic bytes (8 per distance read), out[3] update kernels
  * ms, out[4] their algorithmic bytes (8 * sum |C|^2 + index traffic). */
 int dtwg_km_stats(dtwg_ctx* ctx, double* out, int reset);
+
+/*
+ * Replaces dtwclust::silhouette_scores (validation.hpp:30-79) over the resident matrix:
+ * silhouette_out[p] per series and *mean_out, bit-identical to the reference (same
+ * ascending-member summation order). Errors: InvalidArguments (p_assign != p, or a series
+ * assigned to a non-medoid), 13 = SingleClusterUndefined (k < 2).
+ */
+int dtwg_silhouette(dtwg_ctx* ctx, const int64_t* medoids, int64_t k, const int64_t* assignment,
+                    int64_t p_assign, double* silhouette_out, double* mean_out);
 
 /* One sweep's pieces (cluster_result.hpp:40-72; kmedoids.hpp:48-52, 84-139). */
 int dtwg_km_nearest_update(dtwg_ctx* ctx, int64_t current, const uint8_t* chosen,

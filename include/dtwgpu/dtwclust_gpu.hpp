@@ -24,6 +24,7 @@
 #include <dtwclust/kmedoids.hpp>
 #include <dtwclust/pairwise.hpp>
 #include <dtwclust/time_series.hpp>
+#include <dtwclust/validation.hpp>
 #include <dtwclust/warp_window.hpp>
 
 #include "../dtwgpu.h"
@@ -89,6 +90,8 @@ namespace detail {
     }
     case DTWG_DISTANCE_MATRIX_INVALID:
       throw dtwclust::DistanceMatrixInvalidError(msg);
+    case DTWG_SINGLE_CLUSTER_UNDEFINED:
+      throw dtwclust::SingleClusterUndefinedError();
     default:
       throw DeviceError(rc, msg);
   }
@@ -168,5 +171,66 @@ inline dtwclust::ClusterResult kmedoids(const dtwclust::DistanceMatrix& source,
   result.certificate = dtwclust::Certificate::LocalHeuristic;
   return result;
 }
+
+/// validation.hpp:30-79 on the GPU: per-series silhouettes and their mean, bit-identical.
+inline dtwclust::ScoreReport silhouette_scores(const dtwclust::DistanceMatrix& distances,
+                                               const dtwclust::ClusterResult& result) {
+  const std::size_t p = distances.size();
+  if (result.assignment.size() != p) {
+    throw dtwclust::InvalidArgumentsError("clustering covers " +
+                                          std::to_string(result.assignment.size()) +
+                                          " series, matrix has " + std::to_string(p));
+  }
+  if (result.medoids.size() < 2) throw dtwclust::SingleClusterUndefinedError();
+  dtwg_ctx* ctx = thread_context().get();
+  const auto& cond = distances.condensed();
+  int rc = dtwg_adopt_condensed(ctx, cond.empty() ? nullptr : cond.data(),
+                                static_cast<std::int64_t>(p), 0);
+  if (rc != DTWG_OK) detail::rethrow(ctx, rc, nullptr, 0);
+  std::vector<std::int64_t> med(result.medoids.begin(), result.medoids.end());
+  std::vector<std::int64_t> asg(result.assignment.begin(), result.assignment.end());
+  dtwclust::ScoreReport report;
+  report.silhouette.resize(p);
+  rc = dtwg_silhouette(ctx, med.data(), static_cast<std::int64_t>(med.size()), asg.data(),
+                       static_cast<std::int64_t>(asg.size()), report.silhouette.data(),
+                       &report.mean_silhouette);
+  if (rc != DTWG_OK) detail::rethrow(ctx, rc, nullptr, 0);
+  return report;
+}
+
+/// Drop-in for dtwclust::LazyDistanceSource (pairwise.hpp:133-188) on the k-medoids path
+/// (runner.hpp:187-189, 211): instead of computing pairs on demand on the host, the first
+/// use fills the whole matrix on the GPU. Satisfies the DistanceSource concept
+/// (cluster_result.hpp:13-17); every distance is identical, so kmedoids returns the same
+/// ClusterResult -- only computed_pairs() reports p(p-1)/2.
+class GpuDistanceSource {
+ public:
+  GpuDistanceSource(const std::vector<dtwclust::TimeSeries>& dataset,
+                    const dtwclust::WarpWindow& w, bool auto_widen = false)
+      : dataset_(&dataset), window_(w), auto_widen_(auto_widen) {
+    if (dataset.empty()) throw dtwclust::EmptyDatasetError();
+    dtwclust::validate_dataset(dataset);
+  }
+  std::size_t size() const noexcept { return dataset_->size(); }
+  double distance(std::size_t i, std::size_t j) {
+    if (!matrix_) {
+      dtwclust::BuildStats stats;
+      matrix_ = std::make_unique<dtwclust::DistanceMatrix>(
+          dtwgpu::build_matrix(*dataset_, window_, 1, &stats, auto_widen_));
+      computed_ = stats.evaluations;
+    }
+    return matrix_->distance(i, j);
+  }
+  std::uint64_t computed_pairs() const { return computed_; }
+  /// The filled matrix (after the first distance() call), e.g. for kmedoids on the GPU.
+  const dtwclust::DistanceMatrix* matrix() const { return matrix_.get(); }
+
+ private:
+  const std::vector<dtwclust::TimeSeries>* dataset_;
+  dtwclust::WarpWindow window_;
+  bool auto_widen_;
+  std::unique_ptr<dtwclust::DistanceMatrix> matrix_;
+  std::uint64_t computed_ = 0;
+};
 
 }  // namespace dtwgpu

@@ -59,6 +59,8 @@ def lib():
                                         OBSERVER, C.c_void_p, _ip, _ip, C.POINTER(C.c_double),
                                         C.POINTER(_i64)]
     L.oracle_kmedoids_range.restype = C.c_int
+    L.oracle_silhouette.argtypes = [_dp, _i64, _ip, _i64, _ip, _i64, _dp, C.POINTER(C.c_double)]
+    L.oracle_silhouette.restype = C.c_int
     L.oracle_splitmix_next.argtypes = [C.POINTER(C.c_uint64)]
     L.oracle_splitmix_next.restype = C.c_uint64
     return L
@@ -90,6 +92,8 @@ def ref():
     L.ref_kmedoids.restype = C.c_int
     L.ref_sweep.argtypes = [_dp, _i64, _ip, _i64, _ip, C.POINTER(C.c_double), _ip]
     L.ref_sweep.restype = C.c_int
+    L.ref_silhouette.argtypes = [_dp, _i64, _ip, _i64, _ip, _i64, _dp, C.POINTER(C.c_double)]
+    L.ref_silhouette.restype = C.c_int
     return L
 
 
@@ -180,6 +184,18 @@ def kmedoids_range(D, p, k, restarts, max_iterations, seed, rb, re):
     return med[:k], asg, cost.value, int(br.value)
 
 
+def silhouette(D, p, medoids, assignment):
+    """validation.hpp:30-79 restated; returns (per-series silhouettes, mean)."""
+    asg = _i64a(assignment)
+    out = np.zeros(max(p, 1), dtype=np.float64)
+    mean = C.c_double()
+    rc = lib().oracle_silhouette(_f64(D), p, _i64a(medoids), len(medoids), asg, len(asg), out,
+                                 C.byref(mean))
+    if rc:
+        raise RuntimeError(f"oracle_silhouette error code {rc}")
+    return out[:p], mean.value
+
+
 # ---------------------------------------------------------------- reference itself
 class RefError(Exception):
     def __init__(self, code, message, pair=None):
@@ -244,3 +260,12 @@ def ref_sweep(D, p, medoids):
     cost = C.c_double()
     _ref_check(ref().ref_sweep(_f64(D), p, _i64a(medoids), k, asg, C.byref(cost), upd))
     return asg, cost.value, upd
+
+
+def ref_silhouette(D, p, medoids, assignment):
+    asg = _i64a(assignment)
+    out = np.zeros(max(p, 1), dtype=np.float64)
+    mean = C.c_double()
+    _ref_check(ref().ref_silhouette(_f64(D), p, _i64a(medoids), len(medoids), asg, len(asg), out,
+                                    C.byref(mean)))
+    return out[:p], mean.value

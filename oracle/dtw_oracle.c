@@ -457,3 +457,66 @@ int oracle_kmedoids_range(const double* D, int64_t p, int64_t k, int64_t restart
   free(asg);
   return 0;
 }
+
+/*
+ * validation.hpp:30-79 silhouette_scores over a condensed matrix. Returns 0, or the
+ * reference error code: 2 (size mismatch / non-medoid assignment), 13 (k < 2).
+ */
+int oracle_silhouette(const double* D, int64_t p, const int64_t* medoids, int64_t k,
+                      const int64_t* assignment, int64_t p_assign, double* sil, double* mean) {
+  if (p_assign != p) return 2;
+  if (k < 2) return 13;
+  int64_t* cls = (int64_t*)malloc(sizeof(int64_t) * (size_t)p);
+  int64_t* cnt = (int64_t*)calloc((size_t)k + 1, sizeof(int64_t));
+  for (int64_t j = 0; j < p; ++j) {
+    int64_t lo = 0, hi = k;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (medoids[mid] < assignment[j]) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo == k || medoids[lo] != assignment[j]) {
+      free(cls);
+      free(cnt);
+      return 2;
+    }
+    cls[j] = lo;
+    cnt[lo + 1]++;
+  }
+  for (int64_t c = 0; c < k; ++c) cnt[c + 1] += cnt[c];
+  int64_t* mem = (int64_t*)malloc(sizeof(int64_t) * (size_t)p);
+  int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * (size_t)k);
+  for (int64_t c = 0; c < k; ++c) fill[c] = cnt[c];
+  for (int64_t j = 0; j < p; ++j) mem[fill[cls[j]]++] = j;
+  for (int64_t j = 0; j < p; ++j) sil[j] = 0.0;
+  double sum = 0.0;
+  for (int64_t c = 0; c < k; ++c) {
+    const int64_t nc = cnt[c + 1] - cnt[c];
+    for (int64_t q = cnt[c]; q < cnt[c + 1]; ++q) {
+      const int64_t t = mem[q];
+      if (nc == 1) continue;
+      double own = 0.0;
+      for (int64_t u = cnt[c]; u < cnt[c + 1]; ++u)
+        if (mem[u] != t) own += dist(D, p, t, mem[u]);
+      const double a = own / (double)(nc - 1);
+      double b = ORACLE_INF;
+      for (int64_t o = 0; o < k; ++o) {
+        const int64_t no = cnt[o + 1] - cnt[o];
+        if (o == c || no == 0) continue;
+        double across = 0.0;
+        for (int64_t u = cnt[o]; u < cnt[o + 1]; ++u) across += dist(D, p, t, mem[u]);
+        b = min2(b, across / (double)no);
+      }
+      const double denom = a < b ? b : a;
+      const double s = denom > 0.0 ? (b - a) / denom : 0.0;
+      sil[t] = s;
+      sum += s;
+    }
+  }
+  *mean = sum / (double)p;
+  free(cls);
+  free(cnt);
+  free(mem);
+  free(fill);
+  return 0;
+}

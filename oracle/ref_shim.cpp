@@ -22,6 +22,7 @@
 #include <dtwclust/errors.hpp>
 #include <dtwclust/kmedoids.hpp>
 #include <dtwclust/pairwise.hpp>
+#include <dtwclust/validation.hpp>
 
 #include "support/oracles.hpp"
 
@@ -173,6 +174,23 @@ int ref_sweep(const double* condensed, std::int64_t p, const std::int64_t* medoi
     const auto upd = dtwclust::detail::update_medoids(m, med, asg);
     for (std::size_t t = 0; t < asg.size(); ++t) assignment_out[t] = static_cast<std::int64_t>(asg[t]);
     for (std::size_t t = 0; t < upd.size(); ++t) updated_out[t] = static_cast<std::int64_t>(upd[t]);
+  });
+}
+
+// dtwclust::silhouette_scores (validation.hpp:30-79).
+int ref_silhouette(const double* condensed, std::int64_t p, const std::int64_t* medoids,
+                   std::int64_t k, const std::int64_t* assignment, std::int64_t p_assign,
+                   double* sil_out, double* mean_out) {
+  return guarded([&] {
+    const std::size_t total = dtwclust::DistanceMatrix::condensed_size(static_cast<std::size_t>(p));
+    auto m = dtwclust::DistanceMatrix::from_condensed(
+        static_cast<std::size_t>(p), std::vector<double>(condensed, condensed + total));
+    dtwclust::ClusterResult r;
+    r.medoids.assign(medoids, medoids + k);
+    r.assignment.assign(assignment, assignment + p_assign);
+    const dtwclust::ScoreReport rep = dtwclust::silhouette_scores(m, r);
+    for (std::size_t t = 0; t < rep.silhouette.size(); ++t) sil_out[t] = rep.silhouette[t];
+    *mean_out = rep.mean_silhouette;
   });
 }
 

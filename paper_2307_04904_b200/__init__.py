@@ -8,7 +8,8 @@ seeded synthetic workloads (generators.py).
 from .api import (  # noqa: F401
     FP32, FP64, BandInfeasibleError, BuildStats, ClusterResult, DeviceError, DistanceMatrix,
     DistanceMatrixInvalidError, EmptyDatasetError, Engine, Error, IndexOutOfRangeError,
-    InvalidArgumentsError, InvalidSeriesError, KMedoidsConfig, KOutOfRangeError, TimeSeries,
-    WarpWindow, assign_to_medoids, assignment_cost, build_matrix, build_matrix_packed,
-    engine, kmedoids, update_medoids, validate, validate_dataset,
+    InvalidArgumentsError, InvalidSeriesError, KMedoidsConfig, KOutOfRangeError, ScoreReport,
+    SingleClusterUndefinedError, TimeSeries, WarpWindow, assign_to_medoids, assignment_cost,
+    build_matrix, build_matrix_packed, engine, kmedoids, silhouette_scores, update_medoids,
+    validate, validate_dataset,
 )

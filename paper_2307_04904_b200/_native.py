@@ -27,7 +27,7 @@ EXPORTS = [
     "dtwg_synchronize", "dtwg_build_matrix", "dtwg_upload_series", "dtwg_fill_slots",
     "dtwg_count_cells", "dtwg_last_fill_ms", "dtwg_launch_count", "dtwg_last_plan",
     "dtwg_adopt_condensed", "dtwg_download_condensed", "dtwg_kmedoids", "dtwg_km_nearest_update",
-    "dtwg_km_assign", "dtwg_km_update", "dtwg_force_kernel", "dtwg_measure_cell_peak", "dtwg_km_stats",
+    "dtwg_km_assign", "dtwg_km_update", "dtwg_force_kernel", "dtwg_measure_cell_peak", "dtwg_km_stats", "dtwg_silhouette",
 ]
 
 
@@ -78,6 +78,7 @@ def lib() -> C.CDLL:
     L.dtwg_force_kernel.argtypes = [_vp, C.c_int, C.c_int, C.c_int]
     L.dtwg_measure_cell_peak.argtypes = [_vp, C.c_int, P(C.c_double)]
     L.dtwg_km_stats.argtypes = [_vp, _dp, C.c_int]
+    L.dtwg_silhouette.argtypes = [_vp, _ip, _i64, _ip, _i64, _dp, P(C.c_double)]
     for name in EXPORTS:
         fn = getattr(L, name)
         if fn.restype is C.c_int or name in ("dtwg_set_stream", "dtwg_synchronize",
@@ -87,6 +88,7 @@ def lib() -> C.CDLL:
                                               "dtwg_download_condensed", "dtwg_kmedoids",
                                               "dtwg_km_nearest_update", "dtwg_km_assign",
                                               "dtwg_km_update", "dtwg_force_kernel",
-                                              "dtwg_measure_cell_peak", "dtwg_km_stats"):
+                                              "dtwg_measure_cell_peak", "dtwg_km_stats",
+                                              "dtwg_silhouette"):
             fn.restype = C.c_int
     return L

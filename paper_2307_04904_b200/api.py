@@ -84,12 +84,20 @@ class IndexOutOfRangeError(Error):
         super().__init__(f"index {index} is outside [0, {p})")
 
 
+class SingleClusterUndefinedError(Error):
+    code = 13
+
+    def __init__(self, message: str = "silhouette scores are undefined for a single cluster; "
+                                      "request k >= 2"):
+        super().__init__(message)
+
+
 class DeviceError(Error):
     code = 100
 
 
 _BY_CODE = {2: InvalidArgumentsError, 7: EmptyDatasetError, 10: KOutOfRangeError,
-            11: DistanceMatrixInvalidError}
+            11: DistanceMatrixInvalidError, 13: SingleClusterUndefinedError}
 
 
 # ----------------------------------------------------------------------------- engine
@@ -241,6 +249,15 @@ class Engine:
         if errors:
             raise errors[0]
         return med[:k].copy(), asg[:p].copy(), float(cost.value), int(best_r.value)
+
+    def silhouette(self, medoids, assignment):
+        medoids = np.ascontiguousarray(medoids, dtype=np.int64)
+        assignment = np.ascontiguousarray(assignment, dtype=np.int64)
+        out = np.zeros(max(len(assignment), 1), dtype=np.float64)
+        mean = C.c_double()
+        self.check(self.L.dtwg_silhouette(self.h, medoids, len(medoids), assignment,
+                                          len(assignment), out, C.byref(mean)))
+        return out[: len(assignment)], float(mean.value)
 
     def km_assign(self, medoids):
         medoids = np.ascontiguousarray(medoids, dtype=np.int64)
@@ -551,3 +568,19 @@ def update_medoids(source: DistanceMatrix, medoids, assignment) -> list:
     """kmedoids.hpp:84-139 (detail::update_medoids) on the GPU."""
     eng = _resident(source)
     return [int(v) for v in eng.km_update(medoids, assignment)]
+
+
+# ----------------------------------------------------------------------------- scores
+@dataclass
+class ScoreReport:
+    """validation.hpp:20-24."""
+    silhouette: list = field(default_factory=list)
+    mean_silhouette: float = 0.0
+    elbow: list = field(default_factory=list)
+
+
+def silhouette_scores(distances: DistanceMatrix, result: ClusterResult) -> ScoreReport:
+    """validation.hpp:30-79 over the GPU-resident matrix, bit-identical to the reference."""
+    eng = _resident(distances)
+    sil, mean = eng.silhouette(result.medoids, result.assignment)
+    return ScoreReport([float(v) for v in sil], mean)

@@ -61,6 +61,9 @@ constexpr int kThreads = 128;
 cudaError_t measure_cell_peak(cudaStream_t st, int sms, bool fp32, double* cells_per_s);
 
 // ---- k-medoids sweep kernels (kmedoids.cu) -------------------------------------
+cudaError_t launch_silhouette(const double* square, int64_t p, const int32_t* members,
+                              const int64_t* cluster_begin, const int32_t* cls, int64_t k,
+                              double* sil, cudaStream_t s);
 cudaError_t launch_to_f32(const double* in, int64_t n, float* out, cudaStream_t s);
 cudaError_t launch_band_pad(const double* samples, const int64_t* off, const int64_t* boff,
                             int64_t p, int64_t pad, void* out, bool fp32, cudaStream_t s);

@@ -277,6 +277,7 @@ struct dtwg_ctx {
   DevBuf<double> d_dist, d_nearest, d_best_sum;
   DevBuf<uint8_t> d_chosen;
   DevBuf<int32_t> d_members;
+  DevBuf<int32_t> d_sil_cls;
 
   int fail(int code, const char* fmt, ...) {
     char buf[512];
@@ -966,6 +967,7 @@ void dtwg_destroy(dtwg_ctx* ctx) {
   ctx->d_best_sum.release();
   ctx->d_chosen.release();
   ctx->d_members.release();
+  ctx->d_sil_cls.release();
   for (int a = 0; a < dtwg_ctx::kAux; ++a) {
     if (ctx->aux[a]) cudaStreamDestroy(ctx->aux[a]);
     if (ctx->aux_done[a]) cudaEventDestroy(ctx->aux_done[a]);
@@ -1115,6 +1117,65 @@ int dtwg_measure_cell_peak(dtwg_ctx* ctx, int precision, double* cells_per_s) {
   cudaSetDevice(ctx->device);
   CU(dtwgpu::measure_cell_peak(ctx->stream, ctx->num_sms, precision == DTWG_FP32, cells_per_s),
      "cell peak");
+  return DTWG_OK;
+}
+
+int dtwg_silhouette(dtwg_ctx* ctx, const int64_t* medoids, int64_t k, const int64_t* assignment,
+                    int64_t p_assign, double* silhouette_out, double* mean_out) {
+  if (!ctx || !medoids || !assignment) return DTWG_INVALID_ARGUMENTS;
+  cudaSetDevice(ctx->device);
+  if (!ctx->cond_valid) return ctx->fail(DTWG_INVALID_ARGUMENTS, "no resident distance matrix");
+  const int64_t p = ctx->mat_p;
+  // validation.hpp:33-49, in the reference's order
+  if (p_assign != p)
+    return ctx->fail(DTWG_INVALID_ARGUMENTS, "clustering covers %lld series, matrix has %lld",
+                     (long long)p_assign, (long long)p);
+  if (k < 2)
+    return ctx->fail(DTWG_SINGLE_CLUSTER_UNDEFINED, "silhouette scores are undefined for a single cluster; request k >= 2");
+  std::vector<int64_t> cb(k + 1, 0);
+  std::vector<int32_t> cls(p);
+  for (int64_t j = 0; j < p; ++j) {
+    const int64_t* it = std::lower_bound(medoids, medoids + k, assignment[j]);
+    if (it == medoids + k || *it != assignment[j])
+      return ctx->fail(DTWG_INVALID_ARGUMENTS, "series %lld is assigned to a non-medoid",
+                       (long long)j);
+    cls[j] = (int32_t)(it - medoids);
+    cb[cls[j] + 1]++;
+  }
+  for (int64_t c = 0; c < k; ++c) cb[c + 1] += cb[c];
+  std::vector<int32_t> members(p);
+  {
+    std::vector<int64_t> fill(cb.begin(), cb.end() - 1);
+    for (int64_t j = 0; j < p; ++j) members[fill[cls[j]]++] = (int32_t)j;
+  }
+  int rc = ensure_square(ctx);
+  if (rc) return rc;
+  rc = km_reserve(ctx, p, k);
+  if (rc) return rc;
+  CU(ctx->d_sil_cls.reserve(p), "malloc");
+  CU(cudaMemcpyAsync(ctx->d_members.ptr, members.data(), p * 4, cudaMemcpyHostToDevice, ctx->stream),
+     "H2D members");
+  CU(cudaMemcpyAsync(ctx->d_cb.ptr, cb.data(), (k + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
+     "H2D cb");
+  CU(cudaMemcpyAsync(ctx->d_sil_cls.ptr, cls.data(), p * 4, cudaMemcpyHostToDevice, ctx->stream),
+     "H2D cls");
+  CU(dtwgpu::launch_silhouette(ctx->d_square.ptr, p, ctx->d_members.ptr, ctx->d_cb.ptr,
+                               ctx->d_sil_cls.ptr, k, ctx->d_dist.ptr, ctx->stream),
+     "silhouette");
+  ctx->launches++;
+  std::vector<double> sil(p);
+  CU(cudaMemcpyAsync(sil.data(), ctx->d_dist.ptr, p * 8, cudaMemcpyDeviceToHost, ctx->stream),
+     "D2H silhouette");
+  CU(cudaStreamSynchronize(ctx->stream), "sync");
+  // validation.hpp:54-77: the mean sums cluster by cluster, members ascending, singletons
+  // skipped (adding their 0 would not change the bits anyway).
+  double sum = 0.0;
+  for (int64_t c = 0; c < k; ++c) {
+    if (cb[c + 1] - cb[c] == 1) continue;
+    for (int64_t q = cb[c]; q < cb[c + 1]; ++q) sum += sil[members[q]];
+  }
+  if (silhouette_out) std::copy(sil.begin(), sil.end(), silhouette_out);
+  if (mean_out) *mean_out = sum / (double)p;
   return DTWG_OK;
 }
 

@@ -202,6 +202,43 @@ __global__ void to_f32_kernel(const double* __restrict__ in, int64_t n, float* _
     out[t] = (float)in[t];
 }
 
+// validation.hpp:30-79 silhouette, per series t: a = mean distance to the other members
+// of its own cluster, b = smallest mean distance to another non-empty cluster, s =
+// (b - a) / max(a, b) (0 when that is 0; singletons score 0). Every sum runs over the
+// members in ascending order, as the reference does, reading D(m, t) = D(t, m) so a warp
+// of consecutive t reads one coalesced row segment per member m.
+__global__ void silhouette_kernel(const double* __restrict__ sq, int64_t p,
+                                  const int32_t* __restrict__ members,
+                                  const int64_t* __restrict__ cb, const int32_t* __restrict__ cls,
+                                  int64_t k, double* __restrict__ sil) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < p;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = cls[t];
+    const int64_t own_n = cb[c + 1] - cb[c];
+    if (own_n == 1) {
+      sil[t] = 0.0;
+      continue;
+    }
+    double own = 0.0;
+    for (int64_t q = cb[c]; q < cb[c + 1]; ++q) {
+      const int64_t m = members[q];
+      if (m != t) own = __dadd_rn(own, sq[m * p + t]);
+    }
+    const double a = __ddiv_rn(own, (double)(own_n - 1));
+    double b = CUDART_INF;
+    for (int64_t o = 0; o < k; ++o) {
+      const int64_t n_o = cb[o + 1] - cb[o];
+      if (o == c || n_o == 0) continue;
+      double across = 0.0;
+      for (int64_t q = cb[o]; q < cb[o + 1]; ++q) across = __dadd_rn(across, sq[(int64_t)members[q] * p + t]);
+      const double mean = __ddiv_rn(across, (double)n_o);
+      b = mean < b ? mean : b;  // std::min(b, mean)
+    }
+    const double denom = a < b ? b : a;  // std::max(a, b)
+    sil[t] = denom > 0.0 ? __ddiv_rn(__dsub_rn(b, a), denom) : 0.0;
+  }
+}
+
 int grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   if (g > 148 * 32) g = 148 * 32;
@@ -222,6 +259,14 @@ cudaError_t launch_band_pad(const double* samples, const int64_t* off, const int
 
 cudaError_t launch_to_f32(const double* in, int64_t n, float* out, cudaStream_t s) {
   to_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(in, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_silhouette(const double* square, int64_t p, const int32_t* members,
+                              const int64_t* cluster_begin, const int32_t* cls, int64_t k,
+                              double* sil, cudaStream_t s) {
+  silhouette_kernel<<<grid_for(p, 128), 128, 0, s>>>(square, p, members, cluster_begin, cls, k,
+                                                      sil);
   return cudaGetLastError();
 }
 

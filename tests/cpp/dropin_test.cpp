@@ -117,6 +117,36 @@ int main() {
          require(hits == 2, "typed exceptions missing");
          return std::string("k == p equal; KOutOfRange, InvalidArguments thrown");
        }},
+      {"silhouette: identical ScoreReport",
+       [] {
+         const auto ds = walks(6, 150, 80, 120);
+         const DistanceMatrix m = dtwclust::build_matrix(ds, WarpWindow::unlimited(), 4);
+         KMedoidsConfig cfg;
+         cfg.k = 5;
+         const ClusterResult r = dtwclust::kmedoids(m, cfg);
+         const ScoreReport a = dtwclust::silhouette_scores(m, r);
+         const ScoreReport b = dtwgpu::silhouette_scores(m, r);
+         require(a.silhouette == b.silhouette, "silhouettes differ");
+         require(a.mean_silhouette == b.mean_silhouette, "mean differs");
+         ClusterResult one = r;
+         one.medoids = {r.medoids[0]};
+         try { dtwgpu::silhouette_scores(m, one); } catch (const SingleClusterUndefinedError&) {
+           return "150 series, k=5: bit-identical; k=1 -> SingleClusterUndefinedError";
+         }
+         throw std::runtime_error("k=1 accepted");
+       }},
+      {"lazy source: GPU-backed DistanceSource gives the same clustering",
+       [] {
+         const auto ds = walks(7, 60, 40, 90);
+         dtwclust::LazyDistanceSource lazy(ds, WarpWindow::banded(10), true);
+         dtwgpu::GpuDistanceSource gpu(ds, WarpWindow::banded(10), true);
+         KMedoidsConfig cfg;
+         cfg.k = 3;
+         cfg.seed = 2024;
+         require(dtwclust::kmedoids(lazy, cfg) == dtwclust::kmedoids(gpu, cfg), "results differ");
+         require(gpu.computed_pairs() == 60 * 59 / 2, "computed_pairs");
+         return "kmedoids(lazy) == kmedoids(GpuDistanceSource); computed_pairs = p(p-1)/2";
+       }},
   };
   int failed = 0;
   for (const auto& c : checks) {

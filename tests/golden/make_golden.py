@@ -44,6 +44,10 @@ def main():
             arrays[f"c{c}_km_medoids"] = med
             arrays[f"c{c}_km_assignment"] = asg
             arrays[f"c{c}_km_cost"] = np.array([cost])
+            if k >= 2:
+                sil, mean = oracle.ref_silhouette(cond, ds.p, med, asg)
+                arrays[f"c{c}_silhouette"] = sil
+                arrays[f"c{c}_silhouette_mean"] = np.array([mean])
             meta["kmedoids"][f"c{c}"] = {"k": k, "restarts": 3, "max_iterations": 100, "seed": 0}
     # test_dtw.cpp:80-95 pairs (seed 20240601), reference distances and brute force.
     rng = ScalarRng(20240601)

@@ -125,3 +125,38 @@ def test_config_pipeline_matches_reference(eng, cfgno, q):
     got = kmedoids(m, cfg)
     med, asg, cost = kref(m.condensed(), ds.p, cfg)
     assert got.medoids == list(med) and got.assignment == list(asg) and got.total_cost == cost
+
+
+# ---------------------------------------------------------------- silhouette (validation.hpp)
+def sref(D, p, med, asg):
+    return (oracle.ref_silhouette if oracle.have_ref() else oracle.silhouette)(D, p, med, asg)
+
+
+@pytest.mark.parametrize("cfgno,q", [(1, 100), (3, 800), (5, 200)])
+def test_silhouette_matches_reference(cfgno, q):
+    ds = gen.make_config(cfgno).subset(q)
+    m = api.build_matrix_packed(ds.samples, ds.offsets,
+                                WarpWindow(None if ds.half_width < 0 else ds.half_width),
+                                ds.auto_widen)
+    res = kmedoids(m, KMedoidsConfig(k=ds.k, restarts=2))
+    rep = api.silhouette_scores(m, res)
+    sil, mean = sref(m.condensed(), ds.p, res.medoids, res.assignment)
+    assert np.array_equal(np.array(rep.silhouette).view(np.uint64), sil.view(np.uint64))
+    assert rep.mean_silhouette == mean
+
+
+def test_silhouette_singletons_and_errors():
+    D = random_condensed(ScalarRng(12), 12)
+    m = DistanceMatrix.from_condensed(12, D)
+    res = kmedoids(m, KMedoidsConfig(k=6, restarts=2))   # k large: singleton clusters likely
+    rep = api.silhouette_scores(m, res)
+    sil, mean = sref(D, 12, res.medoids, res.assignment)
+    assert np.array_equal(np.array(rep.silhouette), sil) and rep.mean_silhouette == mean
+    with pytest.raises(api.SingleClusterUndefinedError):
+        api.silhouette_scores(m, api.ClusterResult([res.medoids[0]], [res.medoids[0]] * 12, 0.0))
+    with pytest.raises(InvalidArgumentsError):
+        api.silhouette_scores(m, api.ClusterResult(res.medoids, res.assignment[:-1], 0.0))
+    bad = list(res.assignment)
+    bad[0] = next(j for j in range(12) if j not in res.medoids)
+    with pytest.raises(InvalidArgumentsError):
+        api.silhouette_scores(m, api.ClusterResult(res.medoids, bad, 0.0))

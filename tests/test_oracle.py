@@ -163,3 +163,13 @@ def test_generators_shapes():
     # z-normalised: mean 0, population std 1
     s = gen.config2(n=3).series(1)
     assert abs(s.mean()) < 1e-12 and abs(s.std() - 1) < 1e-12
+
+
+@pytest.mark.parametrize("c", [1, 3, 5])
+def test_golden_silhouette(c):
+    """validation.hpp:30-79 restated, against the reference's own ScoreReport."""
+    p = META["configs"][f"c{c}"]["series"]
+    sil, mean = oracle.silhouette(GOLD[f"c{c}_condensed"], p, GOLD[f"c{c}_km_medoids"],
+                                  GOLD[f"c{c}_km_assignment"])
+    assert_bitwise(sil, GOLD[f"c{c}_silhouette"], f"c{c} silhouette")
+    assert mean == GOLD[f"c{c}_silhouette_mean"][0]
