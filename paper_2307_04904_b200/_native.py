@@ -12,7 +12,8 @@ from functools import lru_cache
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdtwgpu.so")
+# DTWGPU_LIB: load an alternative build (kernel-variant experiments in tools/).
+LIB_PATH = os.environ.get("DTWGPU_LIB") or os.path.join(HERE, "libdtwgpu.so")
 
 _dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
 _ip = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")

@@ -27,11 +27,18 @@ struct FillArgs {
   const double* bsamples;
   const float* bsamples32;
   const int64_t* boffsets;  // start of series i inside bsamples
+  // Strip family (long pairs; column strips of one pair pipelined over many warps):
+  const int64_t* strip_base;     // count + 1 prefix sums of strips per pair (nullptr: uniform)
+  int strips_per_pair;           // uniform mode
+  unsigned long long* work;      // item counter (zeroed before the launch)
+  int* prog;                     // per strip item: last row published (zeroed before the launch)
+  double* cols;                  // two boundary columns per pair, col_stride doubles each
+  int64_t col_stride;
 };
 
 constexpr int kBandPad = 640;  // >= hw + G + G*R (+3 ring chunks) for every band instantiation
 
-enum class Family : int { Full = 0, Band = 1 };
+enum class Family : int { Full = 0, Band = 1, Strip = 2 };
 
 // One kernel configuration: family, lanes per pair (G), DP cells per lane per row (R),
 // and whether per-cell band masking may be needed (Full family only).
@@ -45,6 +52,7 @@ struct KernelCfg {
   int P = 1;    // Band family: pairs per lane group (independent chains per lane)
   int TR = 2;   // Full family: rows per step (independent chains per lane)
   bool ring = false;  // Band family: y window in a shared-memory ring instead of registers
+  int U = 1;          // ring variant: units per lane (independent cell chains per lane)
 };
 
 // Launches cfg over args on stream with `blocks` CTAs of kThreads threads.

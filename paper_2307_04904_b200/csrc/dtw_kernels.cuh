@@ -338,6 +338,225 @@ __global__ void __launch_bounds__(kThreads) dtw_full_kernel(const FillArgs A) {
 }
 
 // ===================================================================================
+// Strip family: long pairs. The Full family's column strips of ONE pair are spread over
+// many warps (all SMs) instead of being run as sequential passes by one group: strip s
+// of a pair is a work item taken (in order, from a global counter) by any warp of a
+// persistent grid; it trails strip s-1 through the boundary column strip s-1 writes
+// (global memory, read through L2) and a per-strip progress counter published with
+// release/acquire ordering every few steps. Items are handed out in dependency order
+// and a warp finishes its item before taking the next, so every wait is on an item that
+// a running warp holds: no deadlock, whatever the residency. Two boundary columns per
+// pair suffice: strip s+2 overwrites row r of strip s's column only after strip s+1 has
+// published row r, i.e. after it has read it.
+// ===================================================================================
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int R, int TR, bool MASK, class Ar>
+__global__ void __launch_bounds__(kThreads) dtw_strip_kernel(const FillArgs A) {
+  using T = typename Ar::T;
+  constexpr bool kF32 = sizeof(T) == 4;
+  constexpr int G = 32;
+  constexpr int W = G * R;
+  constexpr int kPublish = 8;  // steps between progress publications
+  const int gl = threadIdx.x & 31;
+  const T INF = Ar::inf();
+  const T* S = Ar::base(A);
+  const int64_t total =
+      A.strip_base ? A.strip_base[A.count] : A.count * (int64_t)A.strips_per_pair;
+
+  for (;;) {
+    unsigned long long it0 = 0;
+    if (gl == 0) it0 = atomicAdd(A.work, 1ull);
+    const int64_t it = (int64_t)__shfl_sync(kFull, it0, 0);
+    if (it >= total) break;
+    int64_t q;
+    int s, nstrip;
+    if (A.strip_base) {
+      int64_t lo = 0, hi = A.count;  // strip_base[lo] <= it < strip_base[hi]
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (A.strip_base[mid] <= it) lo = mid;
+        else hi = mid;
+      }
+      q = lo;
+      s = (int)(it - A.strip_base[q]);
+      nstrip = (int)(A.strip_base[q + 1] - A.strip_base[q]);
+    } else {
+      q = it / A.strips_per_pair;
+      s = (int)(it - q * A.strips_per_pair);
+      nstrip = A.strips_per_pair;
+    }
+    const Pair P = load_pair(A, q);
+    const T* X = S + P.xoff;
+    const T* Y = S + P.yoff;
+    const int n = P.n, m = P.m, hw = P.hw;
+    double* colq = A.cols + q * 2 * A.col_stride;
+    const double* bin = s > 0 ? colq + ((s - 1) & 1) * A.col_stride : nullptr;
+    double* bout = s < nstrip - 1 ? colq + (s & 1) * A.col_stride : nullptr;
+    const int* pin = s > 0 ? A.prog + (it - 1) : nullptr;
+    int* pout = A.prog + it;
+
+    const int c0 = s * W;
+    int rs = 1, re = n;
+    if (MASK) {
+      rs = max(1, c0 + 1 - hw);
+      re = min(n, c0 + W + hw);
+    }
+    const int written_hi = s > 0 ? (MASK ? min(n, c0 + hw) : n) : 0;  // strip s-1's last row
+    int avail = 0;  // rows of the boundary column published so far (warp-uniform)
+    // Block until strip s-1 has published every row <= need that it writes.
+    auto wait_rows = [&](int need) {
+      need = min(need, written_hi);
+      if (need <= avail) return;
+      int v = 0;
+      for (;;) {
+        if (gl == 0) v = ld_acquire_gpu(pin);
+        v = __shfl_sync(kFull, v, 0);
+        if (v >= need) break;
+        __nanosleep(100);
+      }
+      avail = v;
+    };
+
+    const int nsteps = ((re - rs + TR) / TR) + G - 1;
+    const int jl = c0 + gl * R + 1;  // 1-based first column of this lane
+    T yv[R], pv[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      yv[r] = (jl + r <= m) ? __ldg(Y + jl + r - 1) : T(0);
+      pv[r] = INF;
+    }
+    const bool use_bnd = gl == 0 && s > 0;
+    wait_rows(rs + 2 * TR - 1);
+    T diag0 = INF;  // cell (r0-1, jl-1)
+    if (gl == 0) {
+      if (s == 0) diag0 = (rs == 1) ? T(0) : INF;
+      else if (rs - 1 >= 1 && rs - 1 <= written_hi) diag0 = (T)__ldcg(bin + rs - 1);
+    }
+    double off = 0.0;
+    T send[TR];
+#pragma unroll
+    for (int t = 0; t < TR; ++t) send[t] = INF;
+    double send_off = 0.0;
+    const bool hold = s == nstrip - 1 && ((m - 1 - c0) / R) == gl;
+    const int r_res = hold ? (m - 1 - c0) % R : -1;
+    const bool wb = bout != nullptr && gl == G - 1;
+    double result = 0.0;
+
+    int r0 = rs - TR * gl;
+    T xq[TR];
+    double bq[TR];
+#pragma unroll
+    for (int t = 0; t < TR; ++t) {
+      xq[t] = __ldg(X + (r0 + t - 1));
+      bq[t] = (use_bnd && r0 + t <= written_hi) ? __ldcg(bin + r0 + t) : (double)Ar::inf();
+    }
+    int last_written = 0;
+    for (int st = 0; st < nsteps; ++st, r0 += TR) {
+      wait_rows(rs + TR * (st + 2) - 1);  // lane 0's prefetch below
+      T x[TR], L[TR];
+      double b[TR];
+#pragma unroll
+      for (int t = 0; t < TR; ++t) {
+        x[t] = xq[t];
+        b[t] = bq[t];
+        xq[t] = __ldg(X + (r0 + TR + t - 1));
+        if (use_bnd)
+          bq[t] = (r0 + TR + t <= written_hi) ? __ldcg(bin + r0 + TR + t) : (double)Ar::inf();
+        L[t] = __shfl_up_sync(kFull, send[t], 1, G);
+      }
+      if constexpr (kF32) {
+        const double loff = __shfl_up_sync(kFull, send_off, 1, G);
+        const T delta = (T)(loff - off);
+#pragma unroll
+        for (int t = 0; t < TR; ++t) {
+          if (gl == 0) L[t] = (T)(b[t] - off);
+          else L[t] = L[t] + delta;
+        }
+      } else {
+        if (gl == 0) {
+#pragma unroll
+          for (int t = 0; t < TR; ++t) L[t] = (T)b[t];
+        }
+      }
+      const bool work = st >= gl && r0 <= re;
+      bool fast = true;
+      if (MASK) {
+        const bool in = (jl >= r0 + TR - 1 - hw) && (jl + R - 1 <= r0 + hw);
+        fast = __all_sync(kFull, in || !work);
+      }
+      if (work) {
+        T out[TR];
+        const int nr = min(TR, re - r0 + 1);
+        if (nr == TR) {
+          if (!MASK || fast)
+            FullRows<R, TR, false, Ar>::run(pv, yv, x, diag0, L, jl, r0, hw, out);
+          else
+            FullRows<R, TR, MASK, Ar>::run(pv, yv, x, diag0, L, jl, r0, hw, out);
+          diag0 = L[TR - 1];
+        } else {
+#pragma unroll
+          for (int t = 0; t < TR; ++t) {
+            if (t < nr) {
+              const T xt[1] = {x[t]};
+              const T Lt[1] = {L[t]};
+              T ot[1];
+              FullRows<R, 1, MASK, Ar>::run(pv, yv, xt, diag0, Lt, jl, r0 + t, hw, ot);
+              out[t] = ot[0];
+              diag0 = L[t];
+            } else {
+              out[t] = INF;
+            }
+          }
+        }
+        if constexpr (kF32) {
+          if ((st & (kRenormSteps - 1)) == kRenormSteps - 1) {
+            T mnv = pv[0];
+#pragma unroll
+            for (int r = 1; r < R; ++r) mnv = Ar::mn(mnv, pv[r]);
+            if (mnv != INF) {
+#pragma unroll
+              for (int r = 0; r < R; ++r) pv[r] = __fsub_rn(pv[r], mnv);
+              diag0 = (diag0 == INF) ? INF : __fsub_rn(diag0, mnv);
+#pragma unroll
+              for (int t = 0; t < TR; ++t) out[t] = (out[t] == INF) ? INF : __fsub_rn(out[t], mnv);
+              off += (double)mnv;
+            }
+          }
+          send_off = off;
+        }
+#pragma unroll
+        for (int t = 0; t < TR; ++t) {
+          send[t] = out[t];
+          if (wb && t < nr) {
+            if constexpr (kF32) bout[r0 + t] = (out[t] == INF) ? (double)INF : (double)out[t] + off;
+            else bout[r0 + t] = out[t];
+          }
+        }
+        if (wb) last_written = r0 + nr - 1;
+        if (hold && r0 + nr - 1 == n) {
+          T rv = pv[0];
+#pragma unroll
+          for (int r = 1; r < R; ++r) rv = (r == r_res) ? pv[r] : rv;
+          result = (double)rv + (kF32 ? off : 0.0);
+        }
+      }
+      if (wb && (st % kPublish) == kPublish - 1 && last_written > 0) st_release_gpu(pout, last_written);
+    }
+    if (wb) st_release_gpu(pout, 1 << 30);  // strip done
+    if (hold) A.out[P.slot - A.out_base] = result;
+    __syncwarp();
+  }
+}
+
+// ===================================================================================
 // Band family: sheared band coordinates, one group covers the whole band.
 // ===================================================================================
 // pv[rK] = inf for a uniform runtime rK: one jump-table branch instead of R selects.
@@ -646,8 +865,11 @@ __device__ __forceinline__ void ring_steps(int nst, int& i1, const typename Ar::
   }
 }
 
+#ifndef DTWG_RING_MINB
+#define DTWG_RING_MINB 1
+#endif
 template <int G, int R, int KR, class Ar>
-__global__ void __launch_bounds__(kThreads) dtw_bandring_kernel(const FillArgs A) {
+__global__ void __launch_bounds__(kThreads, DTWG_RING_MINB) dtw_bandring_kernel(const FillArgs A) {
   static_assert(R >= 2, "band family needs R >= 2");
   static_assert(G * R - G <= kRing - 33, "ring too small for this band width");
   // Lane l's window starts l*(R-1) slots after lane 0's: with R-1 odd the 8-byte reads
@@ -729,6 +951,218 @@ __global__ void __launch_bounds__(kThreads) dtw_bandring_kernel(const FillArgs A
       else
         ring_steps<G, R, KR, Ar, false>(C, i1, xp, xq, b, ring, pv, send, send_off, off, n, lK,
                                         rK, gl);
+      __syncwarp();
+    }
+    if (hold) {
+      T rv = pv[0];
+#pragma unroll
+      for (int r = 1; r < R; ++r) rv = (r == r_res) ? pv[r] : rv;
+      double result = (double)rv;
+      if constexpr (sizeof(T) == 4) result += off;
+      A.out[Pp.slot - A.out_base] = result;
+    }
+    __syncwarp();
+  }
+}
+
+// ===================================================================================
+// Band family, ring variant with U units per lane ("unit" kernel). The lane's R band
+// columns are split into U consecutive units; unit h of lane l is unit u = l*U + h of
+// the group and runs one row behind unit u-1 (the wavefront skew moves inside the lane).
+// Per step, unit h of a lane works on row i1 - h:
+//   * its first cell's left neighbour is unit h-1's last column, same row, computed by
+//     unit h-1 in the PREVIOUS step (register; for h = 0: lane l-1, shfl_up);
+//   * its last cell's up neighbour is unit h+1's first cell of row i-1, computed in THIS
+//     step (v0 of unit h+1; for h = U-1: lane l+1's v0 of unit 0, shfl_down).
+// So after the U first cells (v0) of a step are done, the U cell chains are mutually
+// independent: ILP U with chains of R/U cells, at the register cost of the U=1 kernel.
+// Unit h's y window starts h*(width-1) samples into the lane's, so all reads are
+// immediate offsets from one ring pointer; lanes are R-U samples apart, which must be
+// odd for conflict-free 8-byte reads (cf. dtw_bandring_kernel).
+// ===================================================================================
+template <int R, int U>
+struct Units {
+  static constexpr int width(int h) { return R / U + (h < R % U ? 1 : 0); }
+  static constexpr int start(int h) { return h * (R / U) + (h < R % U ? h : R % U); }
+  static constexpr int maxw() { return R / U + (R % U ? 1 : 0); }
+};
+
+template <int G, int R, int U, int KR, class Ar, bool CHECK>
+__device__ __forceinline__ void unit_steps(int nst, int& i1, const typename Ar::T*& xp,
+                                           typename Ar::T& xq, typename Ar::T (&xs)[U], int& b,
+                                           const typename Ar::T* ring, typename Ar::T (&pv)[R],
+                                           typename Ar::T& send, double& send_off, double& off,
+                                           int n, int lK, int rK, int gl) {
+  using T = typename Ar::T;
+  using Un = Units<R, U>;
+  constexpr bool kF32 = sizeof(T) == 4;
+  const T INF = Ar::inf();
+  const bool last = gl == G - 1;
+#pragma unroll 2
+  for (int q = 0; q < nst; ++q) {
+    bool act[U];
+#pragma unroll
+    for (int h = 0; h < U; ++h) act[h] = CHECK ? (i1 - h >= 1 && i1 - h <= n) : true;
+#pragma unroll
+    for (int h = U - 1; h > 0; --h) xs[h] = xs[h - 1];
+    xs[0] = xq;
+    xq = __ldg(++xp);
+    const T* yr = ring + b;
+    T L = __shfl_up_sync(kFull, send, 1, G);
+    if constexpr (kF32) {
+      const double loff = __shfl_up_sync(kFull, send_off, 1, G);
+      L = L + (T)(loff - off);
+    }
+    if (gl == 0) L = INF;
+    // First cells of the units (their left inputs are previous-step values).
+    T v0[U];
+#pragma unroll
+    for (int h = 0; h < U; ++h) {
+      const int s0 = Un::start(h);
+      const T left = h == 0 ? L : pv[s0 - 1];
+      T v = Ar::cell(xs[h], yr[s0 - h], Ar::mn(Ar::mn(pv[s0], pv[s0 + 1]), left));
+      if (CHECK) v = act[h] ? v : pv[s0];
+      if (KR < 0 || KR == s0) {
+        if (lK == gl && rK == s0) v = INF;  // k == K is this unit's first cell
+      }
+      v0[h] = v;
+    }
+    T Ud = __shfl_down_sync(kFull, v0[0], 1, G);
+    if constexpr (kF32) {
+      const double uoff = __shfl_down_sync(kFull, off, 1, G);
+      Ud = Ud + (T)(uoff - off);
+    }
+    Ud = last ? INF : Ud;
+    // Chains, interleaved across units (independent).
+    T left[U];
+#pragma unroll
+    for (int h = 0; h < U; ++h) left[h] = v0[h];
+#pragma unroll
+    for (int c = 1; c < Un::maxw(); ++c) {
+#pragma unroll
+      for (int h = 0; h < U; ++h) {
+        if (c < Un::width(h)) {
+          const int r = Un::start(h) + c;
+          const bool lastc = c == Un::width(h) - 1;
+          const T up = !lastc ? pv[r + 1] : (h == U - 1 ? Ud : v0[h + 1]);
+          T v = Ar::cell(xs[h], yr[r - h], Ar::mn(Ar::mn(pv[r], up), left[h]));
+          if (CHECK) v = act[h] ? v : pv[r];
+          pv[r] = v;
+          left[h] = v;
+        }
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < U; ++h) pv[Un::start(h)] = v0[h];
+    // Cell k == K stays +inf (dtw.hpp:71); first-cell positions were handled above.
+    if constexpr (KR > 0) {
+      if (lK == gl) pv[KR] = INF;
+    } else if constexpr (KR < 0) {
+      if (lK == gl && rK != 0) kill_cell<R>(pv, rK, INF);
+    }
+    if constexpr (kF32) {
+      if (((i1 - 1) & (kRenormSteps - 1)) == kRenormSteps - 1) {
+        T mnv = pv[0];
+#pragma unroll
+        for (int r = 1; r < R; ++r) mnv = Ar::mn(mnv, pv[r]);
+        if (mnv != INF) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) pv[r] = __fsub_rn(pv[r], mnv);
+          off += (double)mnv;
+        }
+      }
+      send_off = off;
+    }
+    send = pv[R - 1];
+    b = (b + 1) & (kRing - 1);
+    ++i1;
+  }
+}
+
+// Resident CTAs the register allocation is capped for (ILP U needs fewer warps; wide R
+// keeps 4 CTAs without spills, narrower ones fit 5).
+#ifndef DTWG_UNIT_MINB
+#define DTWG_UNIT_MINB(R) ((R) >= 20 ? 4 : 5)
+#endif
+template <int G, int R, int U, int KR, class Ar>
+__global__ void __launch_bounds__(kThreads, DTWG_UNIT_MINB(R)) dtw_bandunit_kernel(const FillArgs A) {
+  static_assert(U >= 1 && R / U >= 2, "units need >= 2 columns");
+  static_assert(G * (R - U) <= kRing - 33, "ring too small for this band width");
+  static_assert((R - U) % 2 == 1, "unit variant needs odd R-U (bank-conflict-free reads)");
+  using T = typename Ar::T;
+  constexpr int GPW = 32 / G;
+  constexpr int C = 32;
+  constexpr int PER = C / G;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % G;
+  const int gw = lane / G;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const T INF = Ar::inf();
+  const T* S = Ar::bbase(A);
+  constexpr int kStride = ((kRing + R + 7) / 16) * 16 + 8;
+  __shared__ T rings[kThreads / G][kStride];
+  T* ring = rings[threadIdx.x / G];
+  constexpr int JOFF = 4 * kRing;
+
+  for (int64_t base = warp * GPW; base < A.count; base += nwarps * GPW) {
+    const int64_t item = base + gw;
+    const bool valid = item < A.count;
+    const Pair Pp = load_pair(A, valid ? item : base);
+    int64_t a, bb;
+    decode_slot(Pp.slot, A.p, a, bb);
+    const bool a_rows =
+        (A.offsets[a + 1] - A.offsets[a]) >= (A.offsets[bb + 1] - A.offsets[bb]);
+    const T* Y = S + A.boffsets[a_rows ? bb : a];
+    const T* xp = S + A.boffsets[a_rows ? a : bb];
+    const int n = Pp.n, m = Pp.m, hw = Pp.hw;
+    const int K = 2 * hw + 1;
+    const int lK = K / R;
+    const int rK = KR >= 0 ? KR : K % R;
+    const int kres = m - n + hw;
+    const bool hold = valid && (kres / R) == gl;
+    const int r_res = kres % R;
+    const int kbase = gl * R;
+    const int D = G * (R - U) + 2 - hw;  // first sample index of the chunk written at step 0
+
+    auto put = [&](int j, T v) {
+      const int slot = (j + JOFF) & (kRing - 1);
+      ring[slot] = v;
+      if (slot < R) ring[slot + kRing] = v;
+    };
+    for (int j = 1 - hw + gl; j < D; j += G) put(j, __ldg(Y + (j - 1)));
+    T chunk[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) chunk[u] = __ldg(Y + (D + gl + u * G - 1));
+
+    T pv[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) pv[r] = (kbase + r == hw) ? T(0) : INF;  // row 0
+    T send = INF;
+    double off = 0.0, send_off = 0.0;
+    int i1 = 1 - gl * U;  // row of unit 0 at step 0
+    xp += i1 - 1;
+    T xq = __ldg(xp);
+    T xs[U];
+#pragma unroll
+    for (int h = 0; h < U - 1; ++h) xs[h] = __ldg(xp - 1 - h);  // shifted in at step 0
+    xs[U - 1] = INF;
+    int b = (i1 + kbase - hw + JOFF) & (kRing - 1);
+    const int nsteps = __reduce_max_sync(kFull, n + G * U - 1);
+    const int fill_end = ((G * U - 1 + C - 1) / C) * C;
+    const int drain_start = (__reduce_min_sync(kFull, n) / C) * C;
+    for (int s0 = 0; s0 < nsteps; s0 += C) {
+#pragma unroll
+      for (int u = 0; u < PER; ++u) put(s0 + D + gl + u * G, chunk[u]);
+#pragma unroll
+      for (int u = 0; u < PER; ++u) chunk[u] = __ldg(Y + (s0 + C + D + gl + u * G - 1));
+      __syncwarp();
+      if (s0 < fill_end || s0 >= drain_start)
+        unit_steps<G, R, U, KR, Ar, true>(C, i1, xp, xq, xs, b, ring, pv, send, send_off, off, n,
+                                          lK, rK, gl);
+      else
+        unit_steps<G, R, U, KR, Ar, false>(C, i1, xp, xq, xs, b, ring, pv, send, send_off, off,
+                                           n, lK, rK, gl);
       __syncwarp();
     }
     if (hold) {

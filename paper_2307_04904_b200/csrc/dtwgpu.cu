@@ -94,6 +94,9 @@ struct PlanClass {
   std::vector<int64_t> slots;  // empty + range mode when uniform
   double cost = 0;
   int64_t max_n = 0;
+  // Strip family: strips per pair (uniform) or prefix sums over `slots` (ragged)
+  int strips_per_pair = 0;
+  std::vector<int64_t> strip_base;
 };
 
 int64_t row_off(int64_t i, int64_t p) { return i * p - i * (i + 1) / 2; }
@@ -120,6 +123,7 @@ struct Cand {
   int P = 1;    // band family: pairs per lane group
   int TR = 2;   // full family: rows per step
   bool ring = false;  // band family: shared-memory y ring
+  int U = 1;          // ring variant: units per lane
 };
 const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026},
                       {4, 12, 1956, 1, 4},   {8, 8, 1804},         {8, 8, 1700, 1, 4},
@@ -130,9 +134,12 @@ const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026}
 const Cand kBand[] = {{16, 7, 1500},    {16, 9, 1600},    {16, 11, 1700},  {16, 13, 1800},
                       {32, 3, 1000},    {32, 5, 1250},    {32, 7, 1490},   {32, 9, 1500},
                       {32, 13, 1450},   {32, 3, 600, 2},  {32, 5, 600, 2},  {32, 7, 700, 2},
-                      {8, 16, 1900, 1, 2, true},  {8, 26, 2130, 1, 2, true},
-                      {16, 8, 1500, 1, 2, true},  {16, 14, 1900, 1, 2, true},
-                      {32, 6, 1300, 1, 2, true}};
+                      {8, 16, 1900, 1, 2, true},  {8, 26, 2221, 1, 2, true},
+                      {16, 8, 1500, 1, 2, true},  {16, 14, 2105, 1, 2, true},
+                      {32, 6, 1300, 1, 2, true},
+                      // ring with U units per lane (c2 sweep, round 1)
+                      {8, 26, 2286, 1, 2, true, 3}, {8, 26, 2198, 1, 2, true, 5},
+                      {16, 14, 2166, 1, 2, true, 3}, {16, 13, 2128, 1, 2, true, 2}};
 
 // fp32 mode: the cell is FADD FMUL FMNMX3 FADD, so the Full family runs ~2.15x the fp64
 // rate while the Band family (shuffle-heavy per step) gains only ~1.33x (measured, c2-c4).
@@ -163,9 +170,11 @@ double full_cost(const Shape& s, const Cand& c, bool mask, bool fp32) {
 }
 
 double band_cost(const Shape& s, const Cand& c, bool fp32) {
-  // the smem-ring variant keeps more of the fp32 gain (fewer registers, ~1.5x measured)
-  const double f32 = c.ring ? 1.5 : kFp32Band;
-  return double(s.n + c.G - 1) * double(c.G * c.R) / (c.rate * (fp32 ? f32 : 1.0));
+  // the smem-ring variants keep more of the fp32 gain (fewer registers; 1.39x / 1.46x
+  // measured on c2 for U = 1 / U = 3)
+  const double f32 = c.ring ? (c.U > 1 ? 1.46 : 1.39) : kFp32Band;
+  // wavefront fill/drain: one step per unit of the group
+  return double(s.n + c.G * c.U - 1) * double(c.G * c.R) / (c.rate * (fp32 ? f32 : 1.0));
 }
 
 KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out);
@@ -192,7 +201,7 @@ KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out) {
       if (cst < bc) {
         bc = cst;
         best = KernelCfg{Family::Band, c.G, c.R, false, fp32, fp32 ? -1 : (int)(K % c.R), c.P,
-                         2, c.ring};
+                         2, c.ring, c.U};
       }
     }
   }
@@ -200,7 +209,9 @@ KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out) {
   return best;
 }
 
-const char* family_name(Family f) { return f == Family::Full ? "full" : "band"; }
+const char* family_name(Family f) {
+  return f == Family::Full ? "full" : (f == Family::Band ? "band" : "strip");
+}
 
 }  // namespace
 
@@ -252,6 +263,11 @@ struct dtwg_ctx {
   DevBuf<int64_t> d_offsets;
   DevBuf<double> d_scratch;
   DevBuf<int64_t> d_list;
+  // Strip family: strip prefix sums, progress counters, item counters, boundary columns
+  DevBuf<int64_t> d_strip_base;
+  DevBuf<int> d_prog;
+  DevBuf<unsigned long long> d_work;
+  DevBuf<double> d_cols;
   // +inf-padded copies of the series for the band family (kBandPad each side)
   DevBuf<double> d_bsamples;
   DevBuf<float> d_bsamples32;
@@ -304,13 +320,21 @@ namespace {
 KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cost_out) {
   const bool mask = s.hw < s.n - 1;
   if (ctx->force_family >= 0) {
-    // 0: full (2 rows/step), 1: band P=1, 2: band P=2, 3: full (4 rows/step), 4: band ring
-    const bool band = ctx->force_family == 1 || ctx->force_family == 2 || ctx->force_family == 4;
+    // 0: full (2 rows/step), 1: band P=1, 2: band P=2, 3: full (4 rows/step), 4: band ring,
+    // 10 + U: band ring with U units per lane
+    const int ff = ctx->force_family;
+    if (ff == 5) {  // strip family (long pairs spread over warps), G = 32, 4 rows per step
+      KernelCfg f{Family::Strip, 32, ctx->force_R, mask, fp32, -1, 1, 4};
+      if (dtwgpu::fill_cfg_supported(f)) {
+        if (cost_out) *cost_out = 1.0;
+        return f;
+      }
+    }
+    const bool band = ff == 1 || ff == 2 || ff == 4 || ff > 10;
     KernelCfg f{band ? Family::Band : Family::Full, ctx->force_G, ctx->force_R,
                 band ? false : mask, fp32,
                 (band && !fp32 && ctx->force_R > 0) ? (int)((2 * s.hw + 1) % ctx->force_R) : -1,
-                ctx->force_family == 2 ? 2 : 1, ctx->force_family == 3 ? 4 : 2,
-                ctx->force_family == 4};
+                ff == 2 ? 2 : 1, ff == 3 ? 4 : 2, ff == 4 || ff > 10, ff > 10 ? ff - 10 : 1};
     const bool ok = dtwgpu::fill_cfg_supported(f) &&
                     (f.family == Family::Full ||
                      (mask && f.R >= 2 && (int64_t)f.G * f.R >= 2 * s.hw + 1));
@@ -377,6 +401,50 @@ Shape shape_of(const dtwg_ctx* ctx, int64_t a, int64_t b, int64_t hw, int auto_w
   return s;
 }
 
+// A Full-family class of few, long pairs leaves most of the GPU idle (one lane group per
+// pair, passes in sequence). Such classes become Strip classes: every column strip of
+// every pair is a work item for a full warp, pipelined along the pair (dtw_strip_kernel).
+// Rule: fewer pairs than half the warps the Full configuration keeps resident, and on
+// average at least two strips per pair. m_uniform < 0: ragged class (lengths per slot).
+constexpr int kStripR = 15;
+void maybe_strip(dtwg_ctx* ctx, PlanClass& pc, int64_t count, int64_t m_uniform) {
+  if (count <= 0) return;
+  const bool forced = pc.cfg.family == Family::Strip;  // dtwg_force_kernel(5, ., R)
+  KernelCfg sc = pc.cfg;
+  if (!forced) {
+    if (pc.cfg.family != Family::Full || ctx->force_family >= 0) return;
+    const int64_t resident_groups = (int64_t)ctx->num_sms * dtwgpu::fill_blocks_per_sm(pc.cfg) *
+                                    (dtwgpu::kThreads / pc.cfg.G);
+    if (count * 2 > resident_groups) return;  // enough pairs to fill the GPU already
+    sc = KernelCfg{Family::Strip, 32, kStripR, pc.cfg.mask, pc.cfg.fp32, -1, 1, 4};
+    if (!dtwgpu::fill_cfg_supported(sc)) return;
+  }
+  const int64_t W = 32 * (int64_t)sc.R;
+  if (m_uniform >= 0) {
+    const int64_t S = (m_uniform + W - 1) / W;
+    if (S < 2 && !forced) return;
+    pc.strips_per_pair = (int)S;
+  } else {
+    std::vector<int64_t> base(count + 1, 0);
+    const int64_t p = ctx->p;
+    for (int64_t q = 0; q < count; ++q) {
+      const int64_t slot = pc.slots[q];
+      int64_t lo = 0, hi = p - 1;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) / 2;
+        if (row_off(mid, p) <= slot) lo = mid;
+        else hi = mid - 1;
+      }
+      const int64_t i = lo, j = i + 1 + (slot - row_off(i, p));
+      const int64_t m = std::min(ctx->h_len[i], ctx->h_len[j]);
+      base[q + 1] = base[q] + (m + W - 1) / W;
+    }
+    if (base[count] < 2 * count && !forced) return;
+    pc.strip_base = std::move(base);
+  }
+  pc.cfg = sc;
+}
+
 std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool fp32,
                                  int64_t sb, int64_t se) {
   std::vector<PlanClass> plan;
@@ -388,6 +456,7 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
     pc.cfg = choose_cfg(ctx, s, fp32, &pc.cost);
     pc.max_n = s.n;
     plan.push_back(pc);
+    maybe_strip(ctx, plan[0], se - sb, s.m);
     return plan;
   }
   // Ragged dataset: classify every pair by shape (memoised on (n, m)), then bucket the
@@ -412,7 +481,7 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
     }
     double cst = 0;
     const KernelCfg cfg = choose_cfg(ctx, s, fp32, &cst);
-    const auto key = std::make_tuple((int)cfg.family * 2 + (int)cfg.ring, cfg.G, cfg.R, cfg.mask,
+    const auto key = std::make_tuple((int)cfg.family * 2 + (int)cfg.ring + 4 * cfg.U, cfg.G, cfg.R, cfg.mask,
                                      cfg.kr, cfg.P, cfg.TR);
     int cls;
     auto ic = cls_of_cfg.find(key);
@@ -490,6 +559,7 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
       }
     }
   }
+  for (auto& pc : plan) maybe_strip(ctx, pc, (int64_t)pc.slots.size(), -1);
   return plan;
 }
 
@@ -590,6 +660,10 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
   }
   std::vector<int64_t> blocks_of(plan.size()), scratch_off(plan.size(), -1);
   int64_t scratch_total = 0;
+  // Strip classes: offsets into the strip buffers
+  std::vector<int64_t> sb_off(plan.size(), -1), prog_off(plan.size(), 0), cols_off(plan.size(), 0);
+  int64_t sb_total = 0, prog_total = 0, cols_total = 0;
+  int n_strip_cls = 0;
   for (size_t c = 0; c < plan.size(); ++c) {
     const PlanClass& pc = plan[c];
     const int64_t count = ctx->uniform ? (se - sb) : (int64_t)pc.slots.size();
@@ -600,6 +674,21 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
     int64_t blocks = (int64_t)ctx->num_sms * bps;
     blocks = std::min<int64_t>(blocks, (count + items_per_block - 1) / items_per_block);
     blocks_of[c] = std::max<int64_t>(blocks, 1);
+    if (pc.cfg.family == Family::Strip && count > 0) {
+      blocks_of[c] = (int64_t)ctx->num_sms * bps;  // persistent: items are strips
+      const int64_t strips =
+          pc.strip_base.empty() ? count * pc.strips_per_pair : pc.strip_base[count];
+      if (!pc.strip_base.empty()) {
+        sb_off[c] = sb_total;
+        sb_total += count + 1;
+      }
+      prog_off[c] = prog_total;
+      prog_total += strips;
+      cols_off[c] = cols_total;
+      cols_total += count * 2 * (pc.max_n + 2);
+      ++n_strip_cls;
+      continue;
+    }
     const int64_t W = (int64_t)pc.cfg.G * pc.cfg.R;
     const bool multipass = pc.cfg.family == Family::Full &&
                            (ctx->uniform ? (ctx->h_len[0] > W) : true);
@@ -609,6 +698,22 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
     }
   }
   if (scratch_total) CU(ctx->d_scratch.reserve((size_t)scratch_total), "cudaMalloc scratch");
+  if (n_strip_cls) {
+    CU(ctx->d_prog.reserve((size_t)prog_total), "cudaMalloc prog");
+    CU(ctx->d_cols.reserve((size_t)cols_total), "cudaMalloc cols");
+    CU(ctx->d_work.reserve((size_t)plan.size()), "cudaMalloc work");
+    CU(cudaMemsetAsync(ctx->d_prog.ptr, 0, prog_total * sizeof(int), ctx->stream), "memset prog");
+    CU(cudaMemsetAsync(ctx->d_work.ptr, 0, plan.size() * sizeof(unsigned long long), ctx->stream),
+       "memset work");
+    if (sb_total) {
+      CU(ctx->d_strip_base.reserve((size_t)sb_total), "cudaMalloc strip_base");
+      for (size_t c = 0; c < plan.size(); ++c)
+        if (sb_off[c] >= 0)
+          CU(cudaMemcpyAsync(ctx->d_strip_base.ptr + sb_off[c], plan[c].strip_base.data(),
+                             plan[c].strip_base.size() * 8, cudaMemcpyHostToDevice, ctx->stream),
+             "H2D strip_base");
+    }
+  }
   if (concurrent) {  // fork after the list upload
     CU(cudaEventRecord(ctx->fork, ctx->stream), "fork event");
     for (int a = 0; a < dtwg_ctx::kAux; ++a)
@@ -644,16 +749,25 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
       a.scratch = ctx->d_scratch.ptr + scratch_off[c];
       a.scratch_stride = pc.max_n + 2;
     }
+    if (pc.cfg.family == Family::Strip) {
+      a.strip_base = sb_off[c] >= 0 ? ctx->d_strip_base.ptr + sb_off[c] : nullptr;
+      a.strips_per_pair = pc.strips_per_pair;
+      a.work = ctx->d_work.ptr + c;
+      a.prog = ctx->d_prog.ptr + prog_off[c];
+      a.cols = ctx->d_cols.ptr + cols_off[c];
+      a.col_stride = pc.max_n + 2;
+    }
     cudaStream_t st = concurrent ? ctx->aux[next_aux++ % dtwg_ctx::kAux] : ctx->stream;
     CU(dtwgpu::launch_fill(pc.cfg, a, (int)blocks, st), "fill launch");
     ctx->launches++;
     char buf[160];
     char krs[32] = "";
     if (pc.cfg.family == Family::Band)
-      snprintf(krs, sizeof(krs), "%s,P=%d%s",
+      snprintf(krs, sizeof(krs), "%s,P=%d%s%s",
                pc.cfg.kr >= 0 ? (",kr=" + std::to_string(pc.cfg.kr)).c_str() : "", pc.cfg.P,
-               pc.cfg.ring ? ",ring" : "");
-    if (pc.cfg.family == Family::Full) snprintf(krs, sizeof(krs), ",T=%d", pc.cfg.TR);
+               pc.cfg.ring ? ",ring" : "",
+               pc.cfg.U > 1 ? (",U=" + std::to_string(pc.cfg.U)).c_str() : "");
+    if (pc.cfg.family != Family::Band) snprintf(krs, sizeof(krs), ",T=%d", pc.cfg.TR);
     snprintf(buf, sizeof(buf), "%s%s[G=%d,R=%d%s%s%s] pairs=%lld blocks=%lld(%d/SM)",
              ctx->last_plan.empty() ? "" : "; ", family_name(pc.cfg.family), pc.cfg.G, pc.cfg.R,
              pc.cfg.mask ? ",mask" : "", fp32 ? ",fp32" : "", krs, (long long)count,

@@ -10,10 +10,16 @@
 #define DTWG_BAND_CFGS_G32(X) X(32, 3) X(32, 5) X(32, 7) X(32, 9) X(32, 13)
 // Band family, shared-memory y ring variant
 #define DTWG_RING_CFGS(X) X(8, 16) X(8, 26) X(16, 8) X(16, 14) X(32, 6)
+// Band family, ring variant with U units per lane: (G, R, U), R - U odd
+// Strip family (G = 32): (R, rows per step)
+#define DTWG_STRIP_CFGS(X) X(15, 4) X(8, 4)
+#define DTWG_UNIT_CFGS(X) X(8, 26, 3) X(8, 26, 5) X(16, 14, 3) X(16, 13, 2)
 
 namespace dtwgpu {
 const void* full_kernel_ptr(int G, int R, int TR, bool mask, bool fp32);
 const void* band16_kernel_ptr(int R, int kr, int P, bool fp32);
 const void* band32_kernel_ptr(int R, int kr, int P, bool fp32);
 const void* ring_kernel_ptr(int G, int R, int kr, bool fp32);
+const void* unit_kernel_ptr(int G, int R, int U, int kr, bool fp32);
+const void* strip_kernel_ptr(int R, int TR, bool mask, bool fp32);
 }  // namespace dtwgpu

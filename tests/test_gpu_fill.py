@@ -152,10 +152,12 @@ def test_full_family_every_instantiation(eng, G, R, fam, fp32):
 
 
 RING = [(8, 16), (8, 26), (16, 8), (16, 14), (32, 6)]
+UNIT = [(8, 26, 3), (8, 26, 5), (16, 14, 3), (16, 13, 2)]  # ring with U units per lane
 
 
 @pytest.mark.parametrize("G,R,family", [(g, r, f) for g, r in BAND for f in (1, 2)] +
-                         [(g, r, 4) for g, r in RING])  # 2: two pairs/group, 4: smem ring
+                         [(g, r, 4) for g, r in RING] +  # 2: two pairs/group, 4: smem ring
+                         [(g, r, 10 + u) for g, r, u in UNIT])
 @pytest.mark.parametrize("fp32", [False, True])
 def test_band_family_every_instantiation(eng, G, R, fp32, family):
     rng = np.random.default_rng(G * 1000 + R)
@@ -175,6 +177,42 @@ def test_band_family_every_instantiation(eng, G, R, fp32, family):
             np.testing.assert_allclose(got, want, rtol=1e-5, atol=0)
         else:
             assert_bitwise(got, want, f"band G={G} R={R} hw={hw} plan={plan}")
+
+
+STRIP = [15, 8]
+
+
+@pytest.mark.parametrize("R", STRIP)
+@pytest.mark.parametrize("fp32", [False, True])
+def test_strip_family_every_instantiation(eng, R, fp32):
+    """Long-pair family: column strips of one pair pipelined over warps (forced here on
+    ragged pairs of 1..6 strips, unlimited, widened and narrow bands)."""
+    rng = np.random.default_rng(R)
+    lengths = rng.integers(1, 1500, size=12)
+    lengths[:3] = [1, 32 * R, 32 * R + 1]
+    samples, offsets = _walks(5 + R, lengths)
+    for hw, aw in ((-1, False), (40, True), (3, True), (700, True)):
+        eng.force_kernel(5, 32, R)
+        got = eng.build_condensed(samples, offsets, hw, aw, precision=1 if fp32 else 0)
+        plan = eng.last_plan()
+        assert f"strip[G=32,R={R}" in plan, plan
+        want = oracle.build_condensed(samples, offsets, hw, aw)
+        if fp32:
+            np.testing.assert_allclose(got, want, rtol=1e-5, atol=0)
+        else:
+            assert_bitwise(got, want, f"strip R={R} hw={hw}")
+
+
+@pytest.mark.parametrize("lengths,hw", [([6000, 5000, 7000], -1), ([100000, 99000], 300),
+                                        ([3000] * 5, -1)])
+def test_few_long_pairs_use_the_strip_pipeline(eng, lengths, hw):
+    """Few long pairs (the reference's 1e5-sample case, acceptance_main.cpp:153-187):
+    the planner spreads each pair's strips over the GPU; bit-identical to the oracle."""
+    samples, offsets = _walks(0x5771 + len(lengths), lengths)
+    got = eng.build_condensed(samples, offsets, hw, True)
+    assert "strip[" in eng.last_plan(), eng.last_plan()
+    want = oracle.build_condensed(samples, offsets, hw, True)
+    assert_bitwise(got, want, f"plan={eng.last_plan()}")
 
 
 # ---------------------------------------------------------------- configs (oracle-sized)

@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--subset", type=int, default=0)
     ap.add_argument("--prec", type=int, default=0)
     ap.add_argument("--families", default="0,1,2")
+    ap.add_argument("--cands", default="")  # explicit "family:G:R,..." (overrides --families)
+    ap.add_argument("--reps", type=int, default=1)
     a = ap.parse_args()
     ds = gen.make_config(a.config)
     if a.subset:
@@ -43,6 +45,8 @@ def main():
         cands += [(4, g, r) for g, r in [(8, 16), (8, 26), (16, 8), (16, 14), (32, 6)]]
     if 3 in fams:
         cands += [(3, g, r) for g, r in [(2, 23), (4, 12), (8, 8), (16, 16), (32, 15), (32, 16)]]
+    if a.cands:
+        cands = [tuple(int(v) for v in c.split(":")) for c in a.cands.split(",")]
     ref = None
     for fam, g, r in [(-1, 0, 0)] + cands:
         eng.force_kernel(fam, g, r)
@@ -53,6 +57,9 @@ def main():
             print(json.dumps({"force": [fam, g, r], "error": str(e)}), flush=True)
             continue
         ms = eng.last_fill_ms()
+        for _ in range(a.reps - 1):
+            eng.fill_slots(ds.half_width, ds.auto_widen, a.prec, 0, total, out.data_ptr())
+            ms = min(ms, eng.last_fill_ms())
         plan = eng.last_plan()
         if ref is None:
             ref = out.clone()
