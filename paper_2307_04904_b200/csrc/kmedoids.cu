@@ -4,15 +4,19 @@
 // k-medoids: the nearest-distance refresh of spread seeding
 // (kmedoids.hpp:48-52), nearest-medoid assignment (cluster_result.hpp:40-61) and the
 // per-candidate member sums of the medoid update (kmedoids.hpp:111-121). Every
-// floating-point reduction keeps the reference's order: per-candidate sums are one
-// thread's ascending-member sequential loop (never a tree), comparisons are strict
-// with the lowest index winning. Sequential scalar sums over p (assignment_cost,
-// seeding weights) stay on the host, exactly as written in the reference.
+// floating-point result that decides an outcome keeps the reference's order: the
+// winning candidate's sum (and any candidate that could tie it) is one thread's
+// ascending-member sequential loop; warp-tree sums only rule candidates out, with a
+// rigorous error bound (see tree_sum_kernel). Comparisons are strict with the lowest
+// index winning. Sequential scalar sums over p (assignment_cost, seeding weights) stay
+// on the host, exactly as written in the reference.
 //
 // The matrix is expanded once from condensed to a dense p x p square so every sweep
 // reads contiguous rows (D is symmetric and D[i][j], D[j][i] are the same stored
 // double, so reading the transposed entry is bit-identical).
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <math_constants.h>
 
 #include <cstdint>
@@ -112,12 +116,26 @@ __global__ void assign_kernel(const double* __restrict__ sq, int64_t p,
 
 // kmedoids.hpp:113-120: one thread per candidate; sequential ascending-member sum.
 // members: all clusters concatenated, each ascending; cluster c = [cb[c], cb[c+1]).
-__global__ void candidate_sum_kernel(const double* __restrict__ sq, int64_t p,
-                                     const int32_t* __restrict__ members,
-                                     const int64_t* __restrict__ cb, int64_t k,
-                                     double* __restrict__ sums) {
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < p;
-       q += (int64_t)gridDim.x * blockDim.x) {
+// ---- medoid update (kmedoids.hpp:84-139) -------------------------------------------
+// The reference sums each candidate's distances to its cluster sequentially, in
+// ascending member order, and keeps the first candidate with the strictly smallest sum.
+// Only that argmin (and its sum) matters, so the sums are computed in two passes:
+//  1. tree_sum_kernel: one warp per candidate, lanes stride over the members and the
+//     warp reduces with shuffles -- full parallelism and bandwidth, any summation order.
+//  2. cluster_select_kernel: one block per cluster. With n = |C| non-negative terms, any
+//     order of the n-1 roundings is within gamma_{n-1} * S of the exact sum S (Higham,
+//     Accuracy and Stability, sec. 4.2), for the tree sum and the reference's sequential
+//     sum alike. So a candidate whose tree sum exceeds min_tree * ((1+g)/(1-g))^2 cannot
+//     have the smallest sequential sum; the remaining "contenders" (normally just one)
+//     get the reference's exact sequential sum, and the (sum, position) minimum over
+//     them is the reference's choice, bit for bit.
+__global__ void tree_sum_kernel(const double* __restrict__ sq, int64_t p,
+                                const int32_t* __restrict__ members,
+                                const int64_t* __restrict__ cb, int64_t k,
+                                double* __restrict__ tsum) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < p; q += nw) {
     int64_t lo = 0, hi = k - 1;  // cluster c with cb[c] <= q < cb[c+1]
     while (lo < hi) {
       const int64_t mid = (lo + hi + 1) / 2;
@@ -125,40 +143,66 @@ __global__ void candidate_sum_kernel(const double* __restrict__ sq, int64_t p,
       else hi = mid - 1;
     }
     const int64_t b = __ldg(cb + lo), e = __ldg(cb + lo + 1);
-    const int64_t a = members[q];
+    const double* row = sq + (int64_t)__ldg(members + q) * p;  // D[a][.] == D[.][a]
+    double acc = 0.0;
+    int64_t t = b + lane;
+    for (; t + 96 < e; t += 128) {  // 4 loads in flight per lane
+      const double v0 = row[__ldg(members + t)], v1 = row[__ldg(members + t + 32)];
+      const double v2 = row[__ldg(members + t + 64)], v3 = row[__ldg(members + t + 96)];
+      acc = __dadd_rn(__dadd_rn(acc, v0), __dadd_rn(__dadd_rn(v1, v2), v3));
+    }
+    for (; t < e; t += 32) acc = __dadd_rn(acc, row[__ldg(members + t)]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    if (lane == 0) tsum[q] = acc;
+  }
+}
+
+__global__ void cluster_select_kernel(const double* __restrict__ sq, int64_t p,
+                                      const int32_t* __restrict__ members,
+                                      const int64_t* __restrict__ cb,
+                                      const double* __restrict__ tsum, int64_t* best_member,
+                                      double* best_sum) {
+  const int64_t c = blockIdx.x;
+  const int64_t b = cb[c], e = cb[c + 1];
+  __shared__ double sv[256];
+  __shared__ int64_t sq_[256];
+  // (1) minimum tree sum
+  double mn = CUDART_INF;
+  for (int64_t q = b + threadIdx.x; q < e; q += blockDim.x) mn = fmin(mn, tsum[q]);
+  sv[threadIdx.x] = mn;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sv[threadIdx.x] = fmin(sv[threadIdx.x], sv[threadIdx.x + w]);
+    __syncthreads();
+  }
+  mn = sv[0];
+  __syncthreads();
+  // (2) contenders: exact sequential sums (ascending members, kmedoids.hpp:111-121)
+  const double n = (double)(e - b);
+  const double u = 1.1102230246251565e-16;  // 2^-53
+  const double g = n * u / (1.0 - n * u);
+  const double thr = mn * (1.0 + 8.0 * g) * (1.0 + 4.0 * u);
+  double bv = CUDART_INF;
+  int64_t bq = -1;
+  for (int64_t q = b + threadIdx.x; q < e; q += blockDim.x) {
+    if (!(tsum[q] <= thr)) continue;
+    const double* row = sq + (int64_t)members[q] * p;
     double sum = 0.0;
     int64_t t = b;
     for (; t + 8 <= e; t += 8) {  // loads batched, additions kept in order
       double v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = sq[(int64_t)__ldg(members + t + u) * p + a];
+      for (int uu = 0; uu < 8; ++uu) v[uu] = row[__ldg(members + t + uu)];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) sum = __dadd_rn(sum, v[u]);
+      for (int uu = 0; uu < 8; ++uu) sum = __dadd_rn(sum, v[uu]);
     }
-    for (; t < e; ++t) sum = __dadd_rn(sum, sq[(int64_t)__ldg(members + t) * p + a]);
-    sums[q] = sum;
-  }
-}
-
-// kmedoids.hpp:111-121 selection: first candidate (ascending) with the smallest sum,
-// i.e. lexicographic (sum, position) minimum -- exact in any reduction order.
-__global__ void cluster_argmin_kernel(const int32_t* __restrict__ members,
-                                      const int64_t* __restrict__ cb,
-                                      const double* __restrict__ sums, int64_t* best_member,
-                                      double* best_sum) {
-  const int64_t c = blockIdx.x;
-  const int64_t b = cb[c], e = cb[c + 1];
-  double bv = CUDART_INF;
-  int64_t bq = -1;
-  for (int64_t q = b + threadIdx.x; q < e; q += blockDim.x) {
-    const double v = sums[q];
-    if (bq < 0 || v < bv) {  // q ascending per thread: strict < keeps the first minimum
-      bv = v;
+    for (; t < e; ++t) sum = __dadd_rn(sum, row[__ldg(members + t)]);
+    if (bq < 0 || sum < bv) {  // q ascending per thread: strict < keeps the first minimum
+      bv = sum;
       bq = q;
     }
   }
-  __shared__ double sv[256];
-  __shared__ int64_t sq_[256];
   sv[threadIdx.x] = bv;
   sq_[threadIdx.x] = bq;
   __syncthreads();
@@ -300,12 +344,13 @@ cudaError_t launch_update(const double* square, int64_t p, const int32_t* member
                           double* best_sum, cudaStream_t s) {
   // sums scratch lives right after best_sum (k doubles) -- caller allocates p more.
   double* sums = best_sum + k;
-  candidate_sum_kernel<<<grid_for(p, 128), 128, 0, s>>>(square, p, members, cluster_begin, k,
-                                                         sums);
+  const int64_t warps = std::min<int64_t>(p, 148 * 64);
+  tree_sum_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(square, p, members, cluster_begin,
+                                                               k, sums);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  cluster_argmin_kernel<<<(unsigned)k, 256, 0, s>>>(members, cluster_begin, sums, best_member,
-                                                    best_sum);
+  cluster_select_kernel<<<(unsigned)k, 256, 0, s>>>(square, p, members, cluster_begin, sums,
+                                                    best_member, best_sum);
   return cudaGetLastError();
 }
 

@@ -160,3 +160,23 @@ def test_silhouette_singletons_and_errors():
     bad[0] = next(j for j in range(12) if j not in res.medoids)
     with pytest.raises(InvalidArgumentsError):
         api.silhouette_scores(m, api.ClusterResult(res.medoids, bad, 0.0))
+
+
+@pytest.mark.parametrize("spread", [0.0, 1e-16, 1e-15, 1e-13])
+def test_update_near_ties_match_reference(spread):
+    """Candidate sums equal up to rounding: the warp-tree sums only pre-filter, the
+    reference's sequential sums decide (ties and last-ulp differences included)."""
+    p = 300
+    rng = np.random.default_rng(int(spread * 1e17) + 1)
+    D = 1.0 + spread * rng.integers(0, 8, size=p * (p - 1) // 2).astype(np.float64)
+    D[::7] *= 3.0  # a few larger terms so summation order matters
+    m = DistanceMatrix.from_condensed(p, D)
+    for medoids in ([0], [3, 150, 299], list(range(0, 300, 30))):
+        asg = api.assign_to_medoids(m, medoids)
+        got = api.update_medoids(m, medoids, asg)
+        if oracle.have_ref():
+            asg_ref, _, upd_ref = oracle.ref_sweep(D, p, medoids)
+            assert asg == list(asg_ref)
+            assert got == list(upd_ref), (spread, medoids)
+        cfg = KMedoidsConfig(k=len(medoids), restarts=2, seed=7)
+        check_same(D, p, cfg)
