@@ -17,10 +17,12 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <unordered_map>
 #include <vector>
@@ -268,6 +270,10 @@ struct dtwg_ctx {
   DevBuf<int> d_prog;
   DevBuf<unsigned long long> d_work;
   DevBuf<double> d_cols;
+  // streamed build (large outputs): copy stream, two pinned staging buffers
+  cudaStream_t copy_stream = nullptr;
+  double* h_stage[2] = {nullptr, nullptr};
+  size_t stage_elems = 0;
   // +inf-padded copies of the series for the band family (kBandPad each side)
   DevBuf<double> d_bsamples;
   DevBuf<float> d_bsamples32;
@@ -610,7 +616,7 @@ int ensure_band(dtwg_ctx* ctx, bool fp32) {
 }
 
 int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t sb, int64_t se,
-             double* d_out, int64_t out_base) {
+             double* d_out, int64_t out_base, bool sync = true) {
   const bool fp32 = precision == DTWG_FP32;
   if (fp32) {
     const int rc = ensure_fp32(ctx);
@@ -782,6 +788,7 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
     }
   }
   CU(cudaEventRecord(ctx->ev1, ctx->stream), "event");
+  if (!sync) return DTWG_OK;
   CU(cudaEventSynchronize(ctx->ev1), "fill sync");
   CU(cudaEventElapsedTime(&ctx->last_fill_ms, ctx->ev0, ctx->ev1), "elapsed");
   return DTWG_OK;
@@ -1082,6 +1089,13 @@ void dtwg_destroy(dtwg_ctx* ctx) {
   ctx->d_chosen.release();
   ctx->d_members.release();
   ctx->d_sil_cls.release();
+  ctx->d_strip_base.release();
+  ctx->d_prog.release();
+  ctx->d_work.release();
+  ctx->d_cols.release();
+  for (double*& h : ctx->h_stage)
+    if (h) cudaFreeHost(h);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   for (int a = 0; a < dtwg_ctx::kAux; ++a) {
     if (ctx->aux[a]) cudaStreamDestroy(ctx->aux[a]);
     if (ctx->aux_done[a]) cudaEventDestroy(ctx->aux_done[a]);
@@ -1319,6 +1333,107 @@ uint64_t dtwg_launch_count(const dtwg_ctx* ctx) { return ctx ? ctx->launches : 0
 
 const char* dtwg_last_plan(const dtwg_ctx* ctx) { return ctx ? ctx->last_plan.c_str() : ""; }
 
+// Large outputs (c3: 2.3 GB): the fill runs in slot chunks on the compute stream while
+// finished chunks go D2H on a copy stream into two pinned staging buffers, and host
+// threads copy each staged chunk into the caller's (pageable) buffer -- so the transfer,
+// and the page faults of a fresh output array, hide behind the remaining fill.
+namespace {
+constexpr int64_t kStreamMinBytes = 256ll << 20;
+constexpr int64_t kStreamChunk = 4ll << 20;  // slots per chunk (32 MB)
+// Tests shrink both through the environment to exercise many chunks on small inputs.
+int64_t env_or(const char* name, int64_t dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::strtoll(v, nullptr, 10) : dflt;
+}
+
+void parallel_copy(double* dst, const double* src, int64_t n) {
+  const int nt = (int)std::min<int64_t>(8, std::max<int64_t>(1, n >> 18));
+  if (nt == 1) {
+    std::memcpy(dst, src, n * sizeof(double));
+    return;
+  }
+  std::vector<std::thread> th;
+  const int64_t per = (n + nt - 1) / nt;
+  for (int t = 0; t < nt; ++t) {
+    const int64_t b = t * per, e = std::min(n, b + per);
+    if (b < e) th.emplace_back([=] { std::memcpy(dst + b, src + b, (e - b) * sizeof(double)); });
+  }
+  for (auto& x : th) x.join();
+}
+}  // namespace
+
+static int build_streamed(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, double* out) {
+  const int64_t total = ctx->p * (ctx->p - 1) / 2;
+  const int64_t chunk = std::max<int64_t>(1, env_or("DTWGPU_STREAM_CHUNK", kStreamChunk));
+  int rc = check_band(ctx, hw, auto_widen);
+  if (rc) return rc;
+  rc = ensure_resident(ctx, ctx->p);
+  if (rc) return rc;
+  ctx->cond_valid = false;
+  if (!ctx->copy_stream)
+    CU(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream");
+  if (ctx->stage_elems < (size_t)chunk) {
+    for (double*& h : ctx->h_stage) {
+      if (h) cudaFreeHost(h);
+      h = nullptr;
+      CU(cudaMallocHost(&h, chunk * sizeof(double)), "pinned staging");
+    }
+    ctx->stage_elems = chunk;
+  }
+  const int64_t nchunk = (total + chunk - 1) / chunk;
+  std::vector<cudaEvent_t> filled(nchunk, nullptr), copied(nchunk, nullptr);
+  auto cleanup = [&] {
+    for (auto& e : filled) if (e) cudaEventDestroy(e);
+    for (auto& e : copied) if (e) cudaEventDestroy(e);
+  };
+  auto fail = [&](int code) { cleanup(); return code; };
+  for (int64_t c = 0; c < nchunk; ++c) {
+    if (cudaEventCreateWithFlags(&filled[c], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&copied[c], cudaEventDisableTiming) != cudaSuccess)
+      return fail(ctx->fail(DTWG_CUDA_ERROR, "event create"));
+  }
+  float fill_ms = 0;
+  cudaEvent_t t0 = nullptr;
+  cudaEventCreate(&t0);
+  cudaEventRecord(t0, ctx->stream);
+  for (int64_t c = 0; c < nchunk; ++c) {
+    const int64_t b = c * chunk, e = std::min(total, b + chunk);
+    rc = run_fill(ctx, hw, auto_widen, precision, b, e, ctx->d_cond.ptr, 0, false);
+    if (rc) return fail(rc);
+    if (cudaEventRecord(filled[c], ctx->stream) != cudaSuccess)
+      return fail(ctx->fail(DTWG_CUDA_ERROR, "event record"));
+  }
+  cudaEventRecord(ctx->ev1, ctx->stream);
+  auto enqueue_copy = [&](int64_t c) -> int {
+    const int64_t b = c * chunk, e = std::min(total, b + chunk);
+    if (cudaStreamWaitEvent(ctx->copy_stream, filled[c], 0) != cudaSuccess ||
+        cudaMemcpyAsync(ctx->h_stage[c & 1], ctx->d_cond.ptr + b, (e - b) * sizeof(double),
+                        cudaMemcpyDeviceToHost, ctx->copy_stream) != cudaSuccess ||
+        cudaEventRecord(copied[c], ctx->copy_stream) != cudaSuccess)
+      return ctx->fail(DTWG_CUDA_ERROR, "D2H chunk");
+    return DTWG_OK;
+  };
+  for (int64_t c = 0; c < std::min<int64_t>(2, nchunk); ++c) {
+    rc = enqueue_copy(c);
+    if (rc) return fail(rc);
+  }
+  for (int64_t c = 0; c < nchunk; ++c) {
+    const cudaError_t err = cudaEventSynchronize(copied[c]);
+    if (err != cudaSuccess) return fail(ctx->cuda_fail(err, "D2H chunk sync"));
+    const int64_t b = c * chunk, e = std::min(total, b + chunk);
+    parallel_copy(out + b, ctx->h_stage[c & 1], e - b);
+    if (c + 2 < nchunk) {
+      rc = enqueue_copy(c + 2);
+      if (rc) return fail(rc);
+    }
+  }
+  if (cudaEventElapsedTime(&fill_ms, t0, ctx->ev1) == cudaSuccess) ctx->last_fill_ms = fill_ms;
+  cudaEventDestroy(t0);
+  cleanup();
+  ctx->cond_valid = true;
+  return validate_resident(ctx);  // distance_matrix.hpp:34-38
+}
+
 int dtwg_build_matrix(dtwg_ctx* ctx, const double* samples, const int64_t* offsets, int64_t p,
                       int64_t half_width, int auto_widen, unsigned workers, int precision,
                       double* out_condensed, uint64_t* evaluations) {
@@ -1331,6 +1446,13 @@ int dtwg_build_matrix(dtwg_ctx* ctx, const double* samples, const int64_t* offse
   int rc = dtwg_upload_series(ctx, samples, offsets, p);
   if (rc) return rc;
   const int64_t total = p * (p - 1) / 2;
+  if (out_condensed && ctx->uniform && total > 0 &&
+      total * (int64_t)sizeof(double) >= env_or("DTWGPU_STREAM_MIN_BYTES", kStreamMinBytes)) {
+    rc = build_streamed(ctx, half_width, auto_widen, precision, out_condensed);
+    if (rc) return rc;
+    if (evaluations) *evaluations = (uint64_t)total;
+    return DTWG_OK;
+  }
   rc = dtwg_fill_slots(ctx, half_width, auto_widen, precision, 0, total, nullptr);
   if (rc) return rc;
   if (total == 0) {

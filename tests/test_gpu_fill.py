@@ -324,3 +324,28 @@ def test_config4_fp32_full_matrix_error_histogram(eng):
     hist = np.histogram(np.log10(np.maximum(rel, 1e-16)), bins=[-16, -9, -8, -7, -6, -5.5, -5, 0])
     print("fp32 rel-error histogram (log10 bins):", hist[0].tolist(), "max", rel.max())
     assert rel.max() <= 1e-5, rel.max()
+
+
+def test_streamed_build_matches_oracle():
+    """Large outputs are filled in slot chunks and copied out through pinned staging while
+    the fill continues; shrink the thresholds so a small input takes many chunks."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, oracle\n"
+        "from paper_2307_04904_b200 import api, generators as gen\n"
+        "from tests.helpers import assert_bitwise\n"
+        "ds = gen.config3().subset(1500)\n"
+        "m = api.build_matrix_packed(ds.samples, ds.offsets, api.WarpWindow(None), False)\n"
+        "want = oracle.build_condensed(ds.samples, ds.offsets, -1, False)\n"
+        "assert_bitwise(m.condensed(), want, 'streamed')\n"
+        "ds = gen.config2().subset(300)\n"
+        "m = api.build_matrix_packed(ds.samples, ds.offsets, api.WarpWindow(100), False)\n"
+        "assert_bitwise(m.condensed(), oracle.build_condensed(ds.samples, ds.offsets, 100, False))\n"
+        "print('ok')\n")
+    env = dict(os.environ, DTWGPU_STREAM_MIN_BYTES="0", DTWGPU_STREAM_CHUNK="77777")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
