@@ -152,6 +152,44 @@ int dtwg_km_assign(dtwg_ctx* ctx, const int64_t* medoids, int64_t k, int64_t* as
 int dtwg_km_update(dtwg_ctx* ctx, const int64_t* medoids, int64_t k, const int64_t* assignment,
                    int64_t* updated_out);
 
+/* ---- host-side data path either side of the fill ------------
+ * No device or context needed. Errors: the dtwclust::ErrorCode values (3 IoFailure,
+ * 4 ParseFailure, 5 InvalidSeries, 6 EmptySeries, 7 EmptyDataset, 9 FormatViolation,
+ * 11 DistanceMatrixInvalid); message, line and column of the last error on this thread
+ * from dtwg_io_last_error (line/column -1 when not applicable), the file (ParseFailure,
+ * EmptySeries) or series id (InvalidSeries) from dtwg_io_last_file. `threads` <= 0 uses
+ * every core. Buffers returned through double** are released with dtwg_free.
+ */
+const char* dtwg_io_last_error(int64_t* line, int64_t* column);
+const char* dtwg_io_last_file(void);
+void dtwg_free(void* ptr);
+
+/* Replaces dtwclust::save_matrix (distance_matrix.hpp:104-122): the same text format,
+ * byte for byte, with rows formatted by several threads. */
+int dtwg_save_matrix_text(const double* condensed, int64_t p, const char* path, int threads);
+/* Replaces dtwclust::load_matrix (distance_matrix.hpp:127-192): same checks, same first
+ * error (FormatViolation with its line); rows parsed by several threads. */
+int dtwg_load_matrix_text(const char* path, int threads, int64_t* p_out, double** condensed_out);
+/* Binary sidecar: "DTWGMAT1", uint64 p, the p(p-1)/2 condensed doubles (little-endian);
+ * loading validates like DistanceMatrix::from_condensed (distance_matrix.hpp:27-41). */
+int dtwg_save_matrix_binary(const double* condensed, int64_t p, const char* path);
+int dtwg_load_matrix_binary(const char* path, int64_t* p_out, double** condensed_out);
+
+/* Replaces dtwclust::ingest (csv.hpp:55-106): one series per row of each file, in file
+ * order; label_column drops each row's first cell; delimiter 0 = ',' (tab for .tsv).
+ * The packed result (samples + offsets[p+1] + ids "<file name>:<row>") is what
+ * dtwg_build_matrix / dtwg_upload_series take. */
+typedef struct dtwg_dataset dtwg_dataset;
+int dtwg_ingest_csv(const char* const* paths, int64_t npaths, int label_column, int delimiter,
+                    int threads, dtwg_dataset** out);
+int64_t dtwg_dataset_size(const dtwg_dataset* ds);
+double* dtwg_dataset_samples(dtwg_dataset* ds);
+const int64_t* dtwg_dataset_offsets(const dtwg_dataset* ds);
+const char* dtwg_dataset_id(const dtwg_dataset* ds, int64_t i);
+void dtwg_dataset_free(dtwg_dataset* ds);
+/* runner.hpp:82-95 in place, per series in parallel (bit-identical: sequential sums). */
+int dtwg_z_normalize(double* samples, const int64_t* offsets, int64_t p, int threads);
+
 #ifdef __cplusplus
 }
 #endif

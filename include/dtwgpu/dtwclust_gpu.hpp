@@ -4,6 +4,10 @@
 // replace
 //     dtwclust::build_matrix(dataset, window, workers, &stats, auto_widen)   // pairwise.hpp:62
 //     dtwclust::kmedoids(matrix, config, observer)                           // kmedoids.hpp:148
+//     dtwclust::silhouette_scores(matrix, result)                            // validation.hpp:30
+//     dtwclust::LazyDistanceSource(dataset, window, auto_widen)              // pairwise.hpp:133
+//     dtwclust::save_matrix / load_matrix                                    // distance_matrix.hpp:104
+//     dtwclust::ingest(paths, format), detail::z_normalize(dataset)          // csv.hpp:55, runner.hpp:82
 // by the same calls in namespace dtwgpu. Signatures, results (bit-identical matrices,
 // identical ClusterResult) and thrown exception types follow the reference; the work runs
 // on the B200 through the C-ABI. Host-side types, data loading, the exact (MIP) solver
@@ -13,12 +17,14 @@
 #pragma once
 
 #include <cstdint>
+#include <filesystem>
 #include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include <dtwclust/cluster_result.hpp>
+#include <dtwclust/csv.hpp>
 #include <dtwclust/distance_matrix.hpp>
 #include <dtwclust/errors.hpp>
 #include <dtwclust/kmedoids.hpp>
@@ -232,5 +238,125 @@ class GpuDistanceSource {
   std::unique_ptr<dtwclust::DistanceMatrix> matrix_;
   std::uint64_t computed_ = 0;
 };
+
+namespace detail {
+
+/// Rethrows a host-I/O error code (include/dtwgpu.h, host-side data path) as the
+/// reference's exception class.
+[[noreturn]] inline void rethrow_io(int rc) {
+  std::int64_t line = -1, column = -1;
+  const std::string msg = dtwg_io_last_error(&line, &column);
+  const std::string where = dtwg_io_last_file();
+  switch (rc) {
+    case 3:
+      throw dtwclust::IoFailureError(msg);
+    case 4: {
+      // the message is "<file>:<line>:<column>: <text>"; the exception rebuilds it
+      const std::string prefix =
+          where + ":" + std::to_string(line) + ":" + std::to_string(column) + ": ";
+      throw dtwclust::ParseFailureError(where, static_cast<std::size_t>(line),
+                                        static_cast<std::size_t>(column),
+                                        msg.rfind(prefix, 0) == 0 ? msg.substr(prefix.size()) : msg);
+    }
+    case 5: {
+      const std::string prefix = "series '" + where + "': ";
+      throw dtwclust::InvalidSeriesError(where, msg.rfind(prefix, 0) == 0 ? msg.substr(prefix.size())
+                                                                         : msg);
+    }
+    case 6:
+      throw dtwclust::EmptySeriesError(where, static_cast<std::size_t>(line));
+    case 7:
+      throw dtwclust::EmptyDatasetError();
+    case 9:
+      throw dtwclust::FormatViolationError(static_cast<std::size_t>(line), msg);
+    case 11:
+      throw dtwclust::DistanceMatrixInvalidError(msg);
+    default:
+      throw dtwclust::InvalidArgumentsError(msg);
+  }
+}
+
+}  // namespace detail
+
+/// distance_matrix.hpp:104-122: byte-identical file, rows formatted by `threads` host
+/// threads (0 = all cores).
+inline void save_matrix(const dtwclust::DistanceMatrix& m, const std::filesystem::path& path,
+                        int threads = 0) {
+  const auto& c = m.condensed();
+  const int rc = dtwg_save_matrix_text(c.empty() ? nullptr : c.data(),
+                                       static_cast<std::int64_t>(m.size()), path.c_str(), threads);
+  if (rc != DTWG_OK) detail::rethrow_io(rc);
+}
+
+/// distance_matrix.hpp:127-192: same checks and first error, rows parsed in parallel.
+inline dtwclust::DistanceMatrix load_matrix(const std::filesystem::path& path, int threads = 0) {
+  std::int64_t p = 0;
+  double* buf = nullptr;
+  const int rc = dtwg_load_matrix_text(path.c_str(), threads, &p, &buf);
+  if (rc != DTWG_OK) detail::rethrow_io(rc);
+  const std::size_t total = dtwclust::DistanceMatrix::condensed_size(static_cast<std::size_t>(p));
+  std::vector<double> values(buf, buf + total);
+  dtwg_free(buf);
+  return dtwclust::DistanceMatrix::from_condensed(static_cast<std::size_t>(p), std::move(values));
+}
+
+/// Binary sidecar of the condensed matrix (loads at disk speed).
+inline void save_matrix_binary(const dtwclust::DistanceMatrix& m, const std::filesystem::path& path) {
+  const auto& c = m.condensed();
+  const int rc = dtwg_save_matrix_binary(c.empty() ? nullptr : c.data(),
+                                         static_cast<std::int64_t>(m.size()), path.c_str());
+  if (rc != DTWG_OK) detail::rethrow_io(rc);
+}
+
+inline dtwclust::DistanceMatrix load_matrix_binary(const std::filesystem::path& path) {
+  std::int64_t p = 0;
+  double* buf = nullptr;
+  const int rc = dtwg_load_matrix_binary(path.c_str(), &p, &buf);
+  if (rc != DTWG_OK) detail::rethrow_io(rc);
+  const std::size_t total = dtwclust::DistanceMatrix::condensed_size(static_cast<std::size_t>(p));
+  std::vector<double> values(buf, buf + total);
+  dtwg_free(buf);
+  return dtwclust::DistanceMatrix::from_condensed(static_cast<std::size_t>(p), std::move(values));
+}
+
+/// csv.hpp:55-106: same series, ids and first error; each file parsed by several threads.
+inline std::vector<dtwclust::TimeSeries> ingest(const std::vector<std::filesystem::path>& paths,
+                                                const dtwclust::CsvFormat& format = {},
+                                                int threads = 0) {
+  std::vector<std::string> names;
+  for (const auto& p : paths) names.push_back(p.string());
+  std::vector<const char*> cps;
+  for (const auto& n : names) cps.push_back(n.c_str());
+  dtwg_dataset* ds = nullptr;
+  const int rc = dtwg_ingest_csv(cps.data(), static_cast<std::int64_t>(cps.size()),
+                                 format.label_column ? 1 : 0,
+                                 format.delimiter ? static_cast<unsigned char>(*format.delimiter) : 0,
+                                 threads, &ds);
+  if (rc != DTWG_OK) detail::rethrow_io(rc);
+  std::vector<dtwclust::TimeSeries> out;
+  const std::int64_t p = dtwg_dataset_size(ds);
+  const double* smp = dtwg_dataset_samples(ds);
+  const std::int64_t* off = dtwg_dataset_offsets(ds);
+  out.reserve(static_cast<std::size_t>(p));
+  for (std::int64_t i = 0; i < p; ++i)
+    out.push_back({dtwg_dataset_id(ds, i), std::vector<double>(smp + off[i], smp + off[i + 1])});
+  dtwg_dataset_free(ds);
+  return out;
+}
+
+/// runner.hpp:82-95 (bit-identical), series normalised in parallel.
+inline void z_normalize(std::vector<dtwclust::TimeSeries>& dataset, int threads = 0) {
+  std::vector<std::int64_t> off(dataset.size() + 1, 0);
+  for (std::size_t i = 0; i < dataset.size(); ++i)
+    off[i + 1] = off[i] + static_cast<std::int64_t>(dataset[i].samples.size());
+  std::vector<double> smp(static_cast<std::size_t>(off.back()));
+  for (std::size_t i = 0; i < dataset.size(); ++i)
+    std::copy(dataset[i].samples.begin(), dataset[i].samples.end(), smp.begin() + off[i]);
+  const int rc = dtwg_z_normalize(smp.data(), off.data(), static_cast<std::int64_t>(dataset.size()),
+                                  threads);
+  if (rc != DTWG_OK) detail::rethrow_io(rc);
+  for (std::size_t i = 0; i < dataset.size(); ++i)
+    std::copy(smp.begin() + off[i], smp.begin() + off[i + 1], dataset[i].samples.begin());
+}
 
 }  // namespace dtwgpu

@@ -94,6 +94,17 @@ def ref():
     L.ref_sweep.restype = C.c_int
     L.ref_silhouette.argtypes = [_dp, _i64, _ip, _i64, _ip, _i64, _dp, C.POINTER(C.c_double)]
     L.ref_silhouette.restype = C.c_int
+    L.ref_free.argtypes = [C.c_void_p]
+    L.ref_free.restype = None
+    L.ref_save_matrix.argtypes = [_dp, _i64, C.c_char_p]
+    L.ref_save_matrix.restype = C.c_int
+    L.ref_load_matrix.argtypes = [C.c_char_p, C.POINTER(_i64), C.POINTER(C.c_void_p)]
+    L.ref_load_matrix.restype = C.c_int
+    L.ref_ingest.argtypes = [C.POINTER(C.c_char_p), _i64, C.c_int, C.c_int, C.POINTER(_i64),
+                             C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
+    L.ref_ingest.restype = C.c_int
+    L.ref_z_normalize.argtypes = [_dp, _ip, _i64]
+    L.ref_z_normalize.restype = C.c_int
     return L
 
 
@@ -269,3 +280,52 @@ def ref_silhouette(D, p, medoids, assignment):
     _ref_check(ref().ref_silhouette(_f64(D), p, _i64a(medoids), len(medoids), asg, len(asg), out,
                                     C.byref(mean)))
     return out[:p], mean.value
+
+
+# ---------------------------------------------------------------- host I/O (reference)
+def _ref_take(ptr, n, dtype):
+    try:
+        if n == 0:
+            return np.zeros(0, dtype=dtype)
+        ct = C.c_double if dtype == np.float64 else C.c_int64
+        return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ct)), shape=(n,)).copy()
+    finally:
+        ref().ref_free(ptr)
+
+
+def ref_save_matrix(D, p, path):
+    """dtwclust::save_matrix (distance_matrix.hpp:104-122)."""
+    _ref_check(ref().ref_save_matrix(_f64(D), p, os.fsencode(path)))
+
+
+def ref_load_matrix(path):
+    """dtwclust::load_matrix (distance_matrix.hpp:127-192) -> (p, condensed)."""
+    p, buf = _i64(), C.c_void_p()
+    _ref_check(ref().ref_load_matrix(os.fsencode(path), C.byref(p), C.byref(buf)))
+    n = int(p.value) * (int(p.value) - 1) // 2
+    return int(p.value), _ref_take(buf, n, np.float64)
+
+
+def ref_ingest(paths, label_column=False, delimiter=None):
+    """dtwclust::ingest (csv.hpp:55-106) -> (samples, offsets, ids)."""
+    enc = [os.fsencode(x) for x in paths]
+    arr = (C.c_char_p * max(len(enc), 1))(*enc)
+    p, smp, off, ids = _i64(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+    _ref_check(ref().ref_ingest(arr, len(enc), int(label_column),
+                                0 if delimiter is None else ord(delimiter), C.byref(p),
+                                C.byref(smp), C.byref(off), C.byref(ids)))
+    n = int(p.value)
+    offsets = _ref_take(off, n + 1, np.int64)
+    samples = _ref_take(smp, int(offsets[-1]), np.float64)
+    try:
+        text = C.cast(ids, C.c_char_p).value.decode()
+    finally:
+        ref().ref_free(ids)
+    return samples, offsets, text.split("\n")[:n]
+
+
+def ref_z_normalize(samples, offsets):
+    """dtwclust::detail::z_normalize (runner.hpp:82-95), returns a normalised copy."""
+    out = _f64(samples).copy()
+    _ref_check(ref().ref_z_normalize(out, _i64a(offsets), len(offsets) - 1))
+    return out

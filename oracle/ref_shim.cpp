@@ -9,9 +9,14 @@
 //   dtwclust::kmedoids       kmedoids.hpp:148-189
 //   dtwclust::assign_to_medoids / assignment_cost  cluster_result.hpp:40-72
 //   dtwclust::testing::dtw_brute_force_oracle      tests/support/oracles.hpp:44-59
+//   dtwclust::silhouette_scores                    validation.hpp:30-79
+//   dtwclust::save_matrix / load_matrix            distance_matrix.hpp:104-192
+//   dtwclust::ingest                               csv.hpp:55-106
+//   dtwclust::detail::z_normalize                  runner.hpp:82-95
 // It is used (a) to pin oracle/dtw_oracle.c and the golden fixtures, and (b) as the
 // "reference" arm of bench.py (the reference's own multithreaded CPU fill).
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -21,7 +26,9 @@
 #include <dtwclust/dtw.hpp>
 #include <dtwclust/errors.hpp>
 #include <dtwclust/kmedoids.hpp>
+#include <dtwclust/csv.hpp>
 #include <dtwclust/pairwise.hpp>
+#include <dtwclust/runner.hpp>
 #include <dtwclust/validation.hpp>
 
 #include "support/oracles.hpp"
@@ -191,6 +198,75 @@ int ref_silhouette(const double* condensed, std::int64_t p, const std::int64_t* 
     const dtwclust::ScoreReport rep = dtwclust::silhouette_scores(m, r);
     for (std::size_t t = 0; t < rep.silhouette.size(); ++t) sil_out[t] = rep.silhouette[t];
     *mean_out = rep.mean_silhouette;
+  });
+}
+
+void ref_free(void* ptr) { std::free(ptr); }
+
+// dtwclust::save_matrix (distance_matrix.hpp:104-122).
+int ref_save_matrix(const double* condensed, std::int64_t p, const char* path) {
+  return guarded([&] {
+    const std::size_t total = dtwclust::DistanceMatrix::condensed_size(static_cast<std::size_t>(p));
+    auto m = dtwclust::DistanceMatrix::from_condensed(
+        static_cast<std::size_t>(p), std::vector<double>(condensed, condensed + total));
+    dtwclust::save_matrix(m, path);
+  });
+}
+
+// dtwclust::load_matrix (distance_matrix.hpp:127-192); *cond_out is malloc'ed.
+int ref_load_matrix(const char* path, std::int64_t* p_out, double** cond_out) {
+  return guarded([&] {
+    const dtwclust::DistanceMatrix m = dtwclust::load_matrix(path);
+    const auto& c = m.condensed();
+    double* buf = static_cast<double*>(std::malloc(std::max<std::size_t>(c.size(), 1) * 8));
+    std::memcpy(buf, c.data(), c.size() * 8);
+    *p_out = static_cast<std::int64_t>(m.size());
+    *cond_out = buf;
+  });
+}
+
+// dtwclust::ingest (csv.hpp:55-106) -> packed buffers (malloc'ed) and '\n'-joined ids.
+int ref_ingest(const char* const* paths, std::int64_t n, int label_column, int delimiter,
+               std::int64_t* p_out, double** samples_out, std::int64_t** offsets_out,
+               char** ids_out) {
+  return guarded([&] {
+    std::vector<std::filesystem::path> ps(paths, paths + n);
+    dtwclust::CsvFormat fmt;
+    fmt.label_column = label_column != 0;
+    if (delimiter > 0) fmt.delimiter = static_cast<char>(delimiter);
+    const auto ds = dtwclust::ingest(ps, fmt);
+    std::size_t total = 0;
+    std::string ids;
+    for (const auto& s : ds) {
+      total += s.samples.size();
+      ids += s.id;
+      ids += '\n';
+    }
+    double* smp = static_cast<double*>(std::malloc(std::max<std::size_t>(total, 1) * 8));
+    auto* off = static_cast<std::int64_t*>(std::malloc((ds.size() + 1) * 8));
+    char* idb = static_cast<char*>(std::malloc(ids.size() + 1));
+    std::size_t pos = 0;
+    off[0] = 0;
+    for (std::size_t i = 0; i < ds.size(); ++i) {
+      std::memcpy(smp + pos, ds[i].samples.data(), ds[i].samples.size() * 8);
+      pos += ds[i].samples.size();
+      off[i + 1] = static_cast<std::int64_t>(pos);
+    }
+    std::memcpy(idb, ids.c_str(), ids.size() + 1);
+    *p_out = static_cast<std::int64_t>(ds.size());
+    *samples_out = smp;
+    *offsets_out = off;
+    *ids_out = idb;
+  });
+}
+
+// dtwclust::z_normalize (runner.hpp:82-95), in place on packed series.
+int ref_z_normalize(double* samples, const std::int64_t* offsets, std::int64_t p) {
+  return guarded([&] {
+    std::vector<dtwclust::TimeSeries> ds = dataset_of(samples, offsets, p);
+    dtwclust::detail::z_normalize(ds);
+    for (std::int64_t i = 0; i < p; ++i)
+      std::memcpy(samples + offsets[i], ds[i].samples.data(), ds[i].samples.size() * 8);
   });
 }
 

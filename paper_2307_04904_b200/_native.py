@@ -29,7 +29,14 @@ EXPORTS = [
     "dtwg_count_cells", "dtwg_last_fill_ms", "dtwg_launch_count", "dtwg_last_plan",
     "dtwg_adopt_condensed", "dtwg_download_condensed", "dtwg_kmedoids", "dtwg_km_nearest_update",
     "dtwg_km_assign", "dtwg_km_update", "dtwg_force_kernel", "dtwg_measure_cell_peak", "dtwg_km_stats", "dtwg_silhouette",
+    # host-side data path (csrc/host_io.cpp)
+    "dtwg_io_last_error", "dtwg_io_last_file", "dtwg_free", "dtwg_save_matrix_text",
+    "dtwg_load_matrix_text", "dtwg_save_matrix_binary", "dtwg_load_matrix_binary",
+    "dtwg_ingest_csv", "dtwg_dataset_size", "dtwg_dataset_samples", "dtwg_dataset_offsets",
+    "dtwg_dataset_id", "dtwg_dataset_free", "dtwg_z_normalize",
 ]
+_HOST_INT = ("dtwg_save_matrix_text", "dtwg_load_matrix_text", "dtwg_save_matrix_binary",
+             "dtwg_load_matrix_binary", "dtwg_ingest_csv", "dtwg_z_normalize")
 
 
 class NativeMissingError(RuntimeError):
@@ -80,6 +87,30 @@ def lib() -> C.CDLL:
     L.dtwg_measure_cell_peak.argtypes = [_vp, C.c_int, P(C.c_double)]
     L.dtwg_km_stats.argtypes = [_vp, _dp, C.c_int]
     L.dtwg_silhouette.argtypes = [_vp, _ip, _i64, _ip, _i64, _dp, P(C.c_double)]
+    L.dtwg_io_last_error.argtypes = [P(_i64), P(_i64)]
+    L.dtwg_io_last_error.restype = C.c_char_p
+    L.dtwg_io_last_file.argtypes = []
+    L.dtwg_io_last_file.restype = C.c_char_p
+    L.dtwg_free.argtypes = [_vp]
+    L.dtwg_free.restype = None
+    L.dtwg_save_matrix_text.argtypes = [_vp, _i64, C.c_char_p, C.c_int]
+    L.dtwg_load_matrix_text.argtypes = [C.c_char_p, C.c_int, P(_i64), P(_vp)]
+    L.dtwg_save_matrix_binary.argtypes = [_vp, _i64, C.c_char_p]
+    L.dtwg_load_matrix_binary.argtypes = [C.c_char_p, P(_i64), P(_vp)]
+    L.dtwg_ingest_csv.argtypes = [P(C.c_char_p), _i64, C.c_int, C.c_int, C.c_int, P(_vp)]
+    L.dtwg_dataset_size.argtypes = [_vp]
+    L.dtwg_dataset_size.restype = _i64
+    L.dtwg_dataset_samples.argtypes = [_vp]
+    L.dtwg_dataset_samples.restype = P(C.c_double)
+    L.dtwg_dataset_offsets.argtypes = [_vp]
+    L.dtwg_dataset_offsets.restype = P(_i64)
+    L.dtwg_dataset_id.argtypes = [_vp, _i64]
+    L.dtwg_dataset_id.restype = C.c_char_p
+    L.dtwg_dataset_free.argtypes = [_vp]
+    L.dtwg_dataset_free.restype = None
+    L.dtwg_z_normalize.argtypes = [_vp, _vp, _i64, C.c_int]
+    for name in _HOST_INT:
+        getattr(L, name).restype = C.c_int
     for name in EXPORTS:
         fn = getattr(L, name)
         if fn.restype is C.c_int or name in ("dtwg_set_stream", "dtwg_synchronize",

@@ -5,6 +5,8 @@
 // on the GPU box by tests/test_gpu_dropin.py.
 #include <cmath>
 #include <cstdio>
+#include <fstream>
+#include <sstream>
 #include <functional>
 #include <string>
 #include <vector>
@@ -12,6 +14,7 @@
 #include <dtwclust/dtw.hpp>
 #include <dtwclust/kmedoids.hpp>
 #include <dtwclust/pairwise.hpp>
+#include <dtwclust/runner.hpp>
 
 #include "support/synthetic.hpp"
 
@@ -146,6 +149,60 @@ int main() {
          require(dtwclust::kmedoids(lazy, cfg) == dtwclust::kmedoids(gpu, cfg), "results differ");
          require(gpu.computed_pairs() == 60 * 59 / 2, "computed_pairs");
          return "kmedoids(lazy) == kmedoids(GpuDistanceSource); computed_pairs = p(p-1)/2";
+       }},
+      {"matrix files: byte-identical text, round trips, same first error",
+       [] {
+         const auto ds = walks(8, 40, 30, 60);
+         const DistanceMatrix m = dtwclust::build_matrix(ds, WarpWindow::unlimited(), 2);
+         const std::filesystem::path dir = std::filesystem::temp_directory_path() / "dtwgpu_io";
+         std::filesystem::create_directories(dir);
+         dtwclust::save_matrix(m, dir / "ref.txt");
+         dtwgpu::save_matrix(m, dir / "gpu.txt", 4);
+         auto slurp = [](const std::filesystem::path& p) {
+           std::ifstream f(p, std::ios::binary);
+           std::stringstream ss;
+           ss << f.rdbuf();
+           return ss.str();
+         };
+         require(slurp(dir / "ref.txt") == slurp(dir / "gpu.txt"), "files differ");
+         require(dtwgpu::load_matrix(dir / "ref.txt", 3) == m, "load differs");
+         dtwgpu::save_matrix_binary(m, dir / "m.bin");
+         require(dtwgpu::load_matrix_binary(dir / "m.bin") == m, "binary round trip");
+         {
+           std::ofstream f(dir / "bad.txt", std::ios::binary);
+           f << "p=3\n0,1,2\n1,0,3\n2,4,0\n";
+         }
+         std::string a, b;
+         try { dtwclust::load_matrix(dir / "bad.txt"); } catch (const FormatViolationError& e) { a = e.what(); }
+         try { dtwgpu::load_matrix(dir / "bad.txt"); } catch (const FormatViolationError& e) { b = e.what(); }
+         require(!a.empty() && a == b, "errors differ: '" + a + "' vs '" + b + "'");
+         return "40x40 text identical; text/binary round trips; '" + b + "'";
+       }},
+      {"ingest + z-normalise: same series, ids, errors",
+       [] {
+         const std::filesystem::path dir = std::filesystem::temp_directory_path() / "dtwgpu_io";
+         std::filesystem::create_directories(dir);
+         {
+           std::ofstream f(dir / "u.csv", std::ios::binary);
+           f << "1,0.5,2.25,\n2,3e-2,-4,5\r\n3, +6 ,7\n";
+         }
+         CsvFormat fmt;
+         fmt.label_column = true;
+         auto a = dtwclust::ingest({dir / "u.csv"}, fmt);
+         auto b = dtwgpu::ingest({dir / "u.csv"}, fmt, 2);
+         require(a == b, "ingested series differ");
+         dtwclust::detail::z_normalize(a);
+         dtwgpu::z_normalize(b, 2);
+         require(a == b, "z-normalised series differ");
+         {
+           std::ofstream f(dir / "v.csv", std::ios::binary);
+           f << "1,2\n3,,4\n";
+         }
+         std::string e1, e2;
+         try { dtwclust::ingest({dir / "v.csv"}); } catch (const ParseFailureError& e) { e1 = e.what(); }
+         try { dtwgpu::ingest({dir / "v.csv"}); } catch (const ParseFailureError& e) { e2 = e.what(); }
+         require(!e1.empty() && e1 == e2, "errors differ: '" + e1 + "' vs '" + e2 + "'");
+         return "3 rows equal (label column, CRLF, '+'); ParseFailure '" + e2 + "'";
        }},
   };
   int failed = 0;
