@@ -96,6 +96,7 @@ struct PlanClass {
   std::vector<int64_t> slots;  // empty + range mode when uniform
   double cost = 0;
   int64_t max_n = 0;
+  double cells = 0;  // in-band cells of the class (diagnostics: dtwg_last_plan)
   // Strip family: strips per pair (uniform) or prefix sums over `slots` (ragged)
   int strips_per_pair = 0;
   std::vector<int64_t> strip_base;
@@ -534,6 +535,7 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
       counts[cls][bk]++;
       plan[cls].max_n = std::max(plan[cls].max_n, s.n);
       plan[cls].cost += double(s.n) * double(s.m);
+      plan[cls].cells += double(pair_cells(s.n, s.m, s.hw));
       if (++j == p) {
         ++i;
         j = i + 1;
@@ -552,16 +554,46 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
     }
     plan[c].slots.resize(acc);
   }
-  // pass 2: place slots
+  // pass 2: place slots (and remember each one's shorter length)
+  std::vector<std::vector<int32_t>> mkey(plan.size());
+  for (size_t c = 0; c < plan.size(); ++c) mkey[c].resize(plan[c].slots.size());
   {
     int64_t i = i0, j = j0;
     Shape s;
     for (int64_t slot = sb; slot < se; ++slot) {
       const int cls = class_of(i, j, s);
-      plan[cls].slots[start[cls][bucket_of(cls, s)]++] = slot;
+      const int64_t at = start[cls][bucket_of(cls, s)]++;
+      plan[cls].slots[at] = slot;
+      mkey[cls][at] = (int32_t)s.m;
       if (++j == p) {
         ++i;
         j = i + 1;
+      }
+    }
+  }
+  // pass 3: inside each (passes, rows) bucket, order by the shorter length too, so the
+  // lane groups of a warp mostly share one (n, m) -- same band geometry, same masked
+  // steps, same trip counts. Counting sort per bucket (start[c][b] now marks its end).
+  {
+    std::vector<int64_t> cnt(L1 + 1);
+    std::vector<int64_t> tmp;
+    for (size_t c = 0; c < plan.size(); ++c) {
+      auto& cn = counts[c];
+      auto& sl = plan[c].slots;
+      auto& mk = mkey[c];
+      for (int64_t b = 0; b < (int64_t)cn.size(); ++b) {
+        const int64_t e = start[c][b], a = e - cn[b];
+        if (e - a < 2) continue;
+        std::fill(cnt.begin(), cnt.end(), 0);
+        for (int64_t t = a; t < e; ++t) cnt[mk[t]]++;
+        int64_t acc = a;
+        for (int64_t v = L1; v >= 0; --v) {  // descending m
+          const int64_t k = cnt[v];
+          cnt[v] = acc;
+          acc += k;
+        }
+        tmp.assign(sl.begin() + a, sl.begin() + e);
+        for (int64_t t = a; t < e; ++t) sl[cnt[mk[t]]++] = tmp[t - a];
       }
     }
   }
@@ -766,7 +798,7 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
     cudaStream_t st = concurrent ? ctx->aux[next_aux++ % dtwg_ctx::kAux] : ctx->stream;
     CU(dtwgpu::launch_fill(pc.cfg, a, (int)blocks, st), "fill launch");
     ctx->launches++;
-    char buf[160];
+    char buf[200];
     char krs[32] = "";
     if (pc.cfg.family == Family::Band)
       snprintf(krs, sizeof(krs), "%s,P=%d%s%s",
@@ -774,9 +806,11 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
                pc.cfg.ring ? ",ring" : "",
                pc.cfg.U > 1 ? (",U=" + std::to_string(pc.cfg.U)).c_str() : "");
     if (pc.cfg.family != Family::Band) snprintf(krs, sizeof(krs), ",T=%d", pc.cfg.TR);
-    snprintf(buf, sizeof(buf), "%s%s[G=%d,R=%d%s%s%s] pairs=%lld blocks=%lld(%d/SM)",
+    char cellsb[32] = "";
+    if (pc.cells > 0) snprintf(cellsb, sizeof(cellsb), " cells=%.4g", pc.cells);
+    snprintf(buf, sizeof(buf), "%s%s[G=%d,R=%d%s%s%s] pairs=%lld%s blocks=%lld(%d/SM)",
              ctx->last_plan.empty() ? "" : "; ", family_name(pc.cfg.family), pc.cfg.G, pc.cfg.R,
-             pc.cfg.mask ? ",mask" : "", fp32 ? ",fp32" : "", krs, (long long)count,
+             pc.cfg.mask ? ",mask" : "", fp32 ? ",fp32" : "", krs, (long long)count, cellsb,
              (long long)blocks, bps);
     ctx->last_plan += buf;
     pos += pc.slots.size();

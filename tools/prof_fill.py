@@ -31,8 +31,8 @@ def main():
     for _ in range(a.reps):
         eng.fill_slots(ds.half_width, ds.auto_widen, a.prec, 0, total, out.data_ptr())
     cells = eng.count_cells(ds.half_width, ds.auto_widen, 0, total)
-    print(f"config={a.config} p={ds.p} plan={eng.last_plan()} ms={eng.last_fill_ms():.3f} "
-          f"gcups={cells / eng.last_fill_ms() / 1e6:.1f}")
+    print(f"config={a.config} p={ds.p} ms={eng.last_fill_ms():.3f} "
+          f"gcups={cells / eng.last_fill_ms() / 1e6:.1f} plan={eng.last_plan()}")
 
 
 if __name__ == "__main__":
