@@ -1176,9 +1176,10 @@ int dtwg_upload_series(dtwg_ctx* ctx, const double* samples, const int64_t* offs
   if (p <= 0) return ctx->fail(DTWG_EMPTY_DATASET, "dataset contains no series");
   if (!offsets || (offsets[p] > 0 && !samples))
     return ctx->fail(DTWG_INVALID_ARGUMENTS, "null series buffers");
-  int rc = validate_series(ctx, samples, offsets, p);
-  if (rc) return rc;
-  ctx->p = p;
+  for (int64_t i = 0; i < p; ++i)
+    if (offsets[i + 1] < offsets[i])
+      return ctx->fail(DTWG_INVALID_ARGUMENTS, "offsets must be non-decreasing");
+  ctx->p = 0;  // nothing uploaded is usable until the series validate
   ctx->h_offsets.assign(offsets, offsets + p + 1);
   const int64_t base = offsets[0];
   for (auto& o : ctx->h_offsets) o -= base;
@@ -1206,7 +1207,11 @@ int dtwg_upload_series(dtwg_ctx* ctx, const double* samples, const int64_t* offs
   CU(cudaMemcpyAsync(ctx->d_offsets.ptr, ctx->h_offsets.data(), (p + 1) * sizeof(int64_t),
                      cudaMemcpyHostToDevice, ctx->stream),
      "H2D offsets");
+  // time_series.hpp:24-33 on the host while the (pinned) copy runs
+  const int rc = validate_series(ctx, samples, offsets, p);
   CU(cudaStreamSynchronize(ctx->stream), "sync");
+  if (rc) return rc;
+  ctx->p = p;
   return DTWG_OK;
 }
 
@@ -1372,7 +1377,8 @@ const char* dtwg_last_plan(const dtwg_ctx* ctx) { return ctx ? ctx->last_plan.c_
 // threads copy each staged chunk into the caller's (pageable) buffer -- so the transfer,
 // and the page faults of a fresh output array, hide behind the remaining fill.
 namespace {
-constexpr int64_t kStreamMinBytes = 256ll << 20;
+constexpr int64_t kStreamMinBytes = 1ll << 20;       // staged D2H from 1 MB of output
+constexpr int64_t kChunkFillMinBytes = 256ll << 20;  // chunked fill from 256 MB
 constexpr int64_t kStreamChunk = 4ll << 20;  // slots per chunk (32 MB)
 // Tests shrink both through the environment to exercise many chunks on small inputs.
 int64_t env_or(const char* name, int64_t dflt) {
@@ -1396,7 +1402,8 @@ void parallel_copy(double* dst, const double* src, int64_t n) {
 }
 }  // namespace
 
-static int build_streamed(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, double* out) {
+static int build_streamed(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, double* out,
+                          bool chunk_fill) {
   const int64_t total = ctx->p * (ctx->p - 1) / 2;
   const int64_t chunk = std::max<int64_t>(1, env_or("DTWGPU_STREAM_CHUNK", kStreamChunk));
   int rc = check_band(ctx, hw, auto_widen);
@@ -1430,10 +1437,16 @@ static int build_streamed(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precisi
   cudaEvent_t t0 = nullptr;
   cudaEventCreate(&t0);
   cudaEventRecord(t0, ctx->stream);
-  for (int64_t c = 0; c < nchunk; ++c) {
-    const int64_t b = c * chunk, e = std::min(total, b + chunk);
-    rc = run_fill(ctx, hw, auto_widen, precision, b, e, ctx->d_cond.ptr, 0, false);
+  if (!chunk_fill) {  // one fill (its plan stays cached); the D2H is still staged
+    rc = run_fill(ctx, hw, auto_widen, precision, 0, total, ctx->d_cond.ptr, 0, false);
     if (rc) return fail(rc);
+  }
+  for (int64_t c = 0; c < nchunk; ++c) {
+    if (chunk_fill) {
+      const int64_t b = c * chunk, e = std::min(total, b + chunk);
+      rc = run_fill(ctx, hw, auto_widen, precision, b, e, ctx->d_cond.ptr, 0, false);
+      if (rc) return fail(rc);
+    }
     if (cudaEventRecord(filled[c], ctx->stream) != cudaSuccess)
       return fail(ctx->fail(DTWG_CUDA_ERROR, "event record"));
   }
@@ -1480,9 +1493,12 @@ int dtwg_build_matrix(dtwg_ctx* ctx, const double* samples, const int64_t* offse
   int rc = dtwg_upload_series(ctx, samples, offsets, p);
   if (rc) return rc;
   const int64_t total = p * (p - 1) / 2;
-  if (out_condensed && ctx->uniform && total > 0 &&
-      total * (int64_t)sizeof(double) >= env_or("DTWGPU_STREAM_MIN_BYTES", kStreamMinBytes)) {
-    rc = build_streamed(ctx, half_width, auto_widen, precision, out_condensed);
+  const int64_t out_bytes = total * (int64_t)sizeof(double);
+  if (out_condensed && total > 0 &&
+      out_bytes >= env_or("DTWGPU_STREAM_MIN_BYTES", kStreamMinBytes)) {
+    const bool chunk_fill =
+        ctx->uniform && out_bytes >= env_or("DTWGPU_CHUNK_FILL_MIN_BYTES", kChunkFillMinBytes);
+    rc = build_streamed(ctx, half_width, auto_widen, precision, out_condensed, chunk_fill);
     if (rc) return rc;
     if (evaluations) *evaluations = (uint64_t)total;
     return DTWG_OK;

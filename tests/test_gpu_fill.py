@@ -344,7 +344,8 @@ def test_streamed_build_matches_oracle():
         "m = api.build_matrix_packed(ds.samples, ds.offsets, api.WarpWindow(100), False)\n"
         "assert_bitwise(m.condensed(), oracle.build_condensed(ds.samples, ds.offsets, 100, False))\n"
         "print('ok')\n")
-    env = dict(os.environ, DTWGPU_STREAM_MIN_BYTES="0", DTWGPU_STREAM_CHUNK="77777")
+    env = dict(os.environ, DTWGPU_STREAM_MIN_BYTES="0", DTWGPU_CHUNK_FILL_MIN_BYTES="0",
+               DTWGPU_STREAM_CHUNK="77777")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                        text=True, timeout=600)
