@@ -36,7 +36,7 @@ struct FillArgs {
   int64_t col_stride;
 };
 
-constexpr int kBandPad = 640;  // >= hw + G + G*R (+3 ring chunks) for every band instantiation
+constexpr int kBandPad = 1024;  // >= hw + G + G*R (+3 ring chunks) for every band instantiation
 
 enum class Family : int { Full = 0, Band = 1, Strip = 2 };
 

@@ -987,7 +987,7 @@ struct Units {
   static constexpr int maxw() { return R / U + (R % U ? 1 : 0); }
 };
 
-template <int G, int R, int U, int KR, class Ar, bool CHECK>
+template <int G, int R, int U, int KR, class Ar, bool CHECK, int RING>
 __device__ __forceinline__ void unit_steps(int nst, int& i1, const typename Ar::T*& xp,
                                            typename Ar::T& xq, typename Ar::T (&xs)[U], int& b,
                                            const typename Ar::T* ring, typename Ar::T (&pv)[R],
@@ -1074,7 +1074,7 @@ __device__ __forceinline__ void unit_steps(int nst, int& i1, const typename Ar::
       send_off = off;
     }
     send = pv[R - 1];
-    b = (b + 1) & (kRing - 1);
+    b = (b + 1) & (RING - 1);
     ++i1;
   }
 }
@@ -1087,7 +1087,9 @@ __device__ __forceinline__ void unit_steps(int nst, int& i1, const typename Ar::
 template <int G, int R, int U, int KR, class Ar>
 __global__ void __launch_bounds__(kThreads, DTWG_UNIT_MINB(R)) dtw_bandunit_kernel(const FillArgs A) {
   static_assert(U >= 1 && R / U >= 2, "units need >= 2 columns");
-  static_assert(G * (R - U) <= kRing - 33, "ring too small for this band width");
+  // ring slots: a power of two holding the group's window (G*(R-U)+1) plus one chunk ahead
+  constexpr int RING = G * (R - U) <= 256 - 33 ? 256 : (G * (R - U) <= 512 - 33 ? 512 : 1024);
+  static_assert(G * (R - U) <= RING - 33, "ring too small for this band width");
   static_assert((R - U) % 2 == 1, "unit variant needs odd R-U (bank-conflict-free reads)");
   using T = typename Ar::T;
   constexpr int GPW = 32 / G;
@@ -1100,10 +1102,10 @@ __global__ void __launch_bounds__(kThreads, DTWG_UNIT_MINB(R)) dtw_bandunit_kern
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const T INF = Ar::inf();
   const T* S = Ar::bbase(A);
-  constexpr int kStride = ((kRing + R + 7) / 16) * 16 + 8;
+  constexpr int kStride = ((RING + R + 7) / 16) * 16 + 8;
   __shared__ T rings[kThreads / G][kStride];
   T* ring = rings[threadIdx.x / G];
-  constexpr int JOFF = 4 * kRing;
+  constexpr int JOFF = 4 * RING;
 
   for (int64_t base = warp * GPW; base < A.count; base += nwarps * GPW) {
     const int64_t item = base + gw;
@@ -1126,9 +1128,9 @@ __global__ void __launch_bounds__(kThreads, DTWG_UNIT_MINB(R)) dtw_bandunit_kern
     const int D = G * (R - U) + 2 - hw;  // first sample index of the chunk written at step 0
 
     auto put = [&](int j, T v) {
-      const int slot = (j + JOFF) & (kRing - 1);
+      const int slot = (j + JOFF) & (RING - 1);
       ring[slot] = v;
-      if (slot < R) ring[slot + kRing] = v;
+      if (slot < R) ring[slot + RING] = v;
     };
     for (int j = 1 - hw + gl; j < D; j += G) put(j, __ldg(Y + (j - 1)));
     T chunk[PER];
@@ -1147,7 +1149,7 @@ __global__ void __launch_bounds__(kThreads, DTWG_UNIT_MINB(R)) dtw_bandunit_kern
 #pragma unroll
     for (int h = 0; h < U - 1; ++h) xs[h] = __ldg(xp - 1 - h);  // shifted in at step 0
     xs[U - 1] = INF;
-    int b = (i1 + kbase - hw + JOFF) & (kRing - 1);
+    int b = (i1 + kbase - hw + JOFF) & (RING - 1);
     const int nsteps = __reduce_max_sync(kFull, n + G * U - 1);
     const int fill_end = ((G * U - 1 + C - 1) / C) * C;
     const int drain_start = (__reduce_min_sync(kFull, n) / C) * C;
@@ -1158,11 +1160,11 @@ __global__ void __launch_bounds__(kThreads, DTWG_UNIT_MINB(R)) dtw_bandunit_kern
       for (int u = 0; u < PER; ++u) chunk[u] = __ldg(Y + (s0 + C + D + gl + u * G - 1));
       __syncwarp();
       if (s0 < fill_end || s0 >= drain_start)
-        unit_steps<G, R, U, KR, Ar, true>(C, i1, xp, xq, xs, b, ring, pv, send, send_off, off, n,
-                                          lK, rK, gl);
+        unit_steps<G, R, U, KR, Ar, true, RING>(C, i1, xp, xq, xs, b, ring, pv, send, send_off,
+                                                off, n, lK, rK, gl);
       else
-        unit_steps<G, R, U, KR, Ar, false>(C, i1, xp, xq, xs, b, ring, pv, send, send_off, off,
-                                           n, lK, rK, gl);
+        unit_steps<G, R, U, KR, Ar, false, RING>(C, i1, xp, xq, xs, b, ring, pv, send, send_off,
+                                                 off, n, lK, rK, gl);
       __syncwarp();
     }
     if (hold) {

@@ -142,11 +142,19 @@ const Cand kBand[] = {{16, 7, 1500},    {16, 9, 1600},    {16, 11, 1700},  {16, 
                       {32, 6, 1300, 1, 2, true},
                       // ring with U units per lane (c2 sweep, round 1)
                       {8, 26, 2286, 1, 2, true, 3}, {8, 26, 2198, 1, 2, true, 5},
-                      {16, 14, 2166, 1, 2, true, 3}, {16, 13, 2128, 1, 2, true, 2}};
+                      {16, 14, 2166, 1, 2, true, 3}, {16, 13, 2128, 1, 2, true, 2},
+                      // wide bands (512-slot ring)
+                      {16, 20, 2186, 1, 2, true, 3}, {16, 26, 2220, 1, 2, true, 3},
+                      {32, 20, 2150, 1, 2, true, 3}, {32, 26, 2170, 1, 2, true, 3}};
 
 // fp32 mode: the cell is FADD FMUL FMNMX3 FADD, so the Full family runs ~2.15x the fp64
 // rate while the Band family (shuffle-heavy per step) gains only ~1.33x (measured, c2-c4).
 constexpr double kFp32Full = 2.15, kFp32Band = 1.33;
+
+// Masked Full fills: rows where the strip lies entirely inside the band run the plain
+// cell; rows crossing a band edge run the masked cell at 1.79x the cost (least-squares fit
+// over hw = 101..400 at n = m = 1000, tools: exp/band_rates.py, profiles/round1_sweep.md).
+constexpr double kMaskedRowCost = 1.79;
 
 double full_cost(const Shape& s, const Cand& c, bool mask, bool fp32) {
   const int64_t W = (int64_t)c.G * c.R;
@@ -160,13 +168,23 @@ double full_cost(const Shape& s, const Cand& c, bool mask, bool fp32) {
       re = std::min<int64_t>(s.n, c0 + W + s.hw);
     }
     // TR rows per step, G-1 steps of wavefront fill/drain
-    cells += double(((re - rs + c.TR) / c.TR) * c.TR + c.TR * (c.G - 1)) * double(W);
+    const int64_t rows = ((re - rs + c.TR) / c.TR) * c.TR;
+    double eff_rows = double(rows);
+    if (mask) {
+      const int64_t fast = std::max<int64_t>(
+          0, std::min<int64_t>(re, c0 + 1 + s.hw) - std::max<int64_t>(rs, c0 + W - s.hw) + 1);
+      const int64_t masked = std::max<int64_t>(0, rows - fast);
+      eff_rows = double(rows - masked) + kMaskedRowCost * double(masked);
+    }
+    cells += (eff_rows + c.TR * (c.G - 1)) * double(W);
   }
   double rate = c.rate * (fp32 ? kFp32Full : 1.0);
-  if (mask) rate *= 0.75;  // masked steps (measured on c2 / c5)
-  if (npass > 1) {         // boundary-column round trips per pass (measured on c4)
+  if (npass > 1) {  // boundary-column round trips per pass (measured on c4)
+    // The per-group boundary columns stay in L2 up to ~n = 1500 (c5, L = 1000 sweeps);
+    // the c4-measured penalties apply beyond.
+    const bool l2_resident = s.n <= 1500;
     if (c.G == 2) rate *= c.TR == 4 ? 0.68 : 0.59;
-    else if (c.G == 4) rate *= c.TR == 4 ? 0.92 : 0.78;
+    else if (c.G == 4) rate *= (c.TR == 4 && l2_resident) ? 1.05 : (c.TR == 4 ? 0.92 : 0.78);
     else if (c.G == 8) rate *= c.TR == 4 ? 1.0 : 0.95;
   }
   return cells / rate;

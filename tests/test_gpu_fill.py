@@ -152,7 +152,8 @@ def test_full_family_every_instantiation(eng, G, R, fam, fp32):
 
 
 RING = [(8, 16), (8, 26), (16, 8), (16, 14), (32, 6)]
-UNIT = [(8, 26, 3), (8, 26, 5), (16, 14, 3), (16, 13, 2)]  # ring with U units per lane
+UNIT = [(8, 26, 3), (8, 26, 5), (16, 14, 3), (16, 13, 2), (16, 20, 3), (16, 26, 3), (32, 20, 3),
+        (32, 26, 3)]  # ring with U units per lane
 
 
 @pytest.mark.parametrize("G,R,family", [(g, r, f) for g, r in BAND for f in (1, 2)] +
@@ -165,7 +166,7 @@ def test_band_family_every_instantiation(eng, G, R, fp32, family):
     for hw in sorted({0, 1, (kmax - 1) // 2, max((kmax - 1) // 2 - 3, 0), 7}):
         if 2 * hw + 1 > kmax:
             continue
-        base = int(rng.integers(hw + 2, 400))
+        base = int(rng.integers(hw + 2, max(400, hw + 3)))
         lengths = [base + int(d) for d in rng.integers(-hw, hw + 1, size=10)]
         lengths = [max(L, 1) for L in lengths]
         samples, offsets = _walks(11 + hw, lengths)
