@@ -205,7 +205,19 @@ def run_gpu_arm(a, ds):
     mine = full[rank * width:(rank + 1) * width]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
+    # Exchange: fused P2P stores (each fill kernel writes every distance into all ranks'
+    # resident matrices over NVLink; include/dtwgpu.h dtwg_exchange_*) or the NCCL
+    # all-gather of padded slices. P2P falls back to NCCL if any rank cannot open a peer.
+    exchange = "none"
+    if world > 1:
+        exchange = a.exchange
+        if exchange == "p2p" and not dd.open_p2p_exchange(eng, p, rank, world):
+            exchange = "nccl (p2p unavailable)"
+
     def step():
+        if exchange == "p2p":
+            eng.exchange_fill(ds.half_width, ds.auto_widen, prec, b, e)
+            return
         if e > b:
             eng.fill_slots(ds.half_width, ds.auto_widen, prec, b, e, mine.data_ptr())
         if world > 1:
@@ -220,6 +232,9 @@ def run_gpu_arm(a, ds):
         """The gathered slices in condensed order (ragged shards are padded to `width`)."""
         if world == 1:
             return mine[:total]
+        if exchange == "p2p":  # every rank's resident matrix is complete after the barrier
+            eng.exchange_complete()
+            return torch.from_numpy(eng.download(p)).to(dev)
         return torch.cat([full[r * width:r * width + (ee - bb)] for r, (bb, ee) in enumerate(bounds)])
 
     for _ in range(max(a.warmup, 0)):
@@ -329,8 +344,11 @@ def run_gpu_arm(a, ds):
     # sharded over ranks and reduced in restart order.
     kmed = None
     if a.kmedoids and ds.k:
-        cond = assembled().contiguous()
-        eng.adopt(None, p, on_device_ptr=cond.data_ptr())
+        if exchange == "p2p":
+            eng.exchange_complete()  # resident already, written by all ranks' fills
+        else:
+            cond = assembled().contiguous()
+            eng.adopt(None, p, on_device_ptr=cond.data_ptr())
         eng._p_resident = p
         eng.km_stats(reset=True)
         torch.cuda.synchronize()
@@ -353,7 +371,7 @@ def run_gpu_arm(a, ds):
                                   "achieved_gbs": st["assign_bytes"] / max(st["assign_ms"], 1e-9) / 1e6}}
         if rank == 0 and a.check and p <= 5000:
             import oracle
-            D = cond.cpu().numpy()
+            D = eng.download(p) if exchange == "p2p" else cond.cpu().numpy()
             med, asg, cost = oracle.kmedoids(D, p, ds.k, ds.restarts, 100, 0)
             kmed["parity"] = bool(list(med) == list(best[2]) and list(asg) == list(best[3])
                                   and cost == best[0])
@@ -373,7 +391,12 @@ def run_gpu_arm(a, ds):
             "vs_baseline": None, "dtype": "f64" if prec == 0 else "f32", "data": "synthetic",
             "config": {"workload": CONFIG_NAMES[a.config], "pairs": total, "cells": all_cells,
                        "series": p, "precision": a.precision,
-                       "parallelism": f"condensed-slot shards x{world} + NCCL all-gather",
+                       "parallelism": (f"condensed-slot shards x{world} + fused P2P stores "
+                                       "into every rank's matrix (NVLink)"
+                                       if exchange == "p2p" else
+                                       f"condensed-slot shards x{world} + NCCL all-gather"
+                                       if world > 1 else "condensed-slot shards x1"),
+                       "exchange": exchange,
                        "l2": "flushed (256 MB write) between timed steps",
                        "plan": eng.last_plan()},
             "pairs_per_s": total * a.steps / (max_ms * 1e-3),
@@ -435,6 +458,9 @@ def main():
     ap.add_argument("--no-check", dest="check", action="store_false")
     ap.add_argument("--subset", type=int, default=0,
                     help="diagnostics: only the first N series of the config")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1: fused P2P stores from the fill kernels (default) or NCCL "
+                         "all-gather of the slices")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: diagnostic multi-rank run (ranks may share a GPU)")
     ap.add_argument("--kmedoids", action="store_true",

@@ -152,6 +152,22 @@ int dtwg_km_assign(dtwg_ctx* ctx, const int64_t* medoids, int64_t k, int64_t* as
 int dtwg_km_update(dtwg_ctx* ctx, const int64_t* medoids, int64_t k, const int64_t* assignment,
                    int64_t* updated_out);
 
+/* ---- fused fill + all-gather over peer memory (one process per GPU, NVLink/NVSwitch) ----
+ * Replaces the fill-then-NCCL-all-gather of a sharded build: every rank exports its
+ * resident matrix buffer (sized for p series), opens every other rank's through CUDA IPC,
+ * and fills its own slot range; the fill kernels store each distance into ALL ranks'
+ * buffers (st.global to peer-mapped addresses), so the exchange overlaps the fill tile by
+ * tile and no collective follows. After every rank's dtwg_exchange_fill has returned
+ * (host barrier), dtwg_exchange_complete validates the matrix and makes it resident for
+ * k-medoids. Handles are 64 bytes per rank (cudaIpcMemHandle_t), handles[r] for rank r.
+ */
+int dtwg_exchange_export(dtwg_ctx* ctx, int64_t p, unsigned char* handle_out);
+int dtwg_exchange_open(dtwg_ctx* ctx, const unsigned char* handles, int n_ranks, int my_rank);
+int dtwg_exchange_fill(dtwg_ctx* ctx, int64_t half_width, int auto_widen, int precision,
+                       int64_t slot_begin, int64_t slot_end);
+int dtwg_exchange_complete(dtwg_ctx* ctx);
+int dtwg_exchange_close(dtwg_ctx* ctx);
+
 /* ---- host-side data path either side of the fill ------------
  * No device or context needed. Errors: the dtwclust::ErrorCode values (3 IoFailure,
  * 4 ParseFailure, 5 InvalidSeries, 6 EmptySeries, 7 EmptyDataset, 9 FormatViolation,

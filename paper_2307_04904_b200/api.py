@@ -213,6 +213,26 @@ class Engine:
         self._last_evaluations = int(ev.value)
         return out[:total]
 
+    # -- fused fill + all-gather over peer memory (include/dtwgpu.h, dtwg_exchange_*) --
+    def exchange_export(self, p: int) -> bytes:
+        buf = C.create_string_buffer(64)
+        self.check(self.L.dtwg_exchange_export(self.h, p, buf))
+        return buf.raw
+
+    def exchange_open(self, handles, rank: int) -> None:
+        blob = b"".join(handles)
+        self.check(self.L.dtwg_exchange_open(self.h, blob, len(handles), rank))
+
+    def exchange_fill(self, half_width: int, auto_widen: bool, precision: int, b: int,
+                      e: int) -> None:
+        self.check(self.L.dtwg_exchange_fill(self.h, half_width, int(auto_widen), precision, b, e))
+
+    def exchange_complete(self) -> None:
+        self.check(self.L.dtwg_exchange_complete(self.h))
+
+    def exchange_close(self) -> None:
+        self.check(self.L.dtwg_exchange_close(self.h))
+
     def adopt(self, condensed, p: int, on_device_ptr: int = 0) -> None:
         if on_device_ptr:
             self.check(self.L.dtwg_adopt_condensed(self.h, C.c_void_p(on_device_ptr), p, 1))

@@ -34,6 +34,11 @@ struct FillArgs {
   int* prog;                     // per strip item: last row published (zeroed before the launch)
   double* cols;                  // two boundary columns per pair, col_stride doubles each
   int64_t col_stride;
+  // Fused exchange: every result is also stored to peer_out[r][slot - peer_base]
+  static constexpr int kMaxPeers = 7;
+  double* peer_out[kMaxPeers];
+  int n_peer;
+  int64_t peer_base;
 };
 
 constexpr int kBandPad = 1024;  // >= hw + G + G*R (+3 ring chunks) for every band instantiation

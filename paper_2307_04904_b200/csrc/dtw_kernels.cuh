@@ -92,6 +92,14 @@ struct F32 {
   static __device__ __forceinline__ const T* bbase(const FillArgs& A) { return A.bsamples32; }
 };
 
+// One pair's distance: into this launch's output and, for the fused fill + all-gather
+// over peer memory (dtwg_exchange_*), into every other rank's copy of the matrix -- plain
+// st.global to NVLink-mapped peer addresses, so the exchange overlaps the fill.
+__device__ __forceinline__ void store_result(const FillArgs& A, int64_t slot, double v) {
+  A.out[slot - A.out_base] = v;
+  for (int r = 0; r < A.n_peer; ++r) A.peer_out[r][slot - A.peer_base] = v;
+}
+
 struct Pair {
   int64_t slot;
   int64_t xoff, yoff;  // rows series (longer), columns series (shorter)
@@ -333,7 +341,7 @@ __global__ void __launch_bounds__(kThreads) dtw_full_kernel(const FillArgs A) {
       __syncwarp();
     }
     const int last_c0 = (npass_g - 1) * W;
-    if (valid && ((m - 1 - last_c0) / R) == gl) A.out[P.slot - A.out_base] = result;
+    if (valid && ((m - 1 - last_c0) / R) == gl) store_result(A, P.slot, result);
   }
 }
 
@@ -551,7 +559,7 @@ __global__ void __launch_bounds__(kThreads) dtw_strip_kernel(const FillArgs A) {
       if (wb && (st % kPublish) == kPublish - 1 && last_written > 0) st_release_gpu(pout, last_written);
     }
     if (wb) st_release_gpu(pout, 1 << 30);  // strip done
-    if (hold) A.out[P.slot - A.out_base] = result;
+    if (hold) store_result(A, P.slot, result);
     __syncwarp();
   }
 }
@@ -780,7 +788,7 @@ __global__ void __launch_bounds__(kThreads, P == 1 ? 5 : 3) dtw_band_kernel(cons
         for (int r = 1; r < R; ++r) rv = (r == r_res[p]) ? pv[p][r] : rv;
         double result = (double)rv;
         if constexpr (kF32) result += off[p];
-        A.out[slot[p] - A.out_base] = result;
+        store_result(A, slot[p], result);
       }
     }
   }
@@ -959,7 +967,7 @@ __global__ void __launch_bounds__(kThreads, DTWG_RING_MINB) dtw_bandring_kernel(
       for (int r = 1; r < R; ++r) rv = (r == r_res) ? pv[r] : rv;
       double result = (double)rv;
       if constexpr (sizeof(T) == 4) result += off;
-      A.out[Pp.slot - A.out_base] = result;
+      store_result(A, Pp.slot, result);
     }
     __syncwarp();
   }
@@ -1173,7 +1181,7 @@ __global__ void __launch_bounds__(kThreads, DTWG_UNIT_MINB(R)) dtw_bandunit_kern
       for (int r = 1; r < R; ++r) rv = (r == r_res) ? pv[r] : rv;
       double result = (double)rv;
       if constexpr (sizeof(T) == 4) result += off;
-      A.out[Pp.slot - A.out_base] = result;
+      store_result(A, Pp.slot, result);
     }
     __syncwarp();
   }

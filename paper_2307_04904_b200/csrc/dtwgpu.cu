@@ -289,6 +289,10 @@ struct dtwg_ctx {
   DevBuf<int> d_prog;
   DevBuf<unsigned long long> d_work;
   DevBuf<double> d_cols;
+  // fused fill + all-gather over peer memory (dtwg_exchange_*): other ranks' resident
+  // matrices opened through CUDA IPC
+  std::vector<double*> peers;
+  bool exchange_open = false;
   // streamed build (large outputs): copy stream, two pinned staging buffers
   cudaStream_t copy_stream = nullptr;
   double* h_stage[2] = {nullptr, nullptr};
@@ -805,6 +809,11 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
       a.scratch = ctx->d_scratch.ptr + scratch_off[c];
       a.scratch_stride = pc.max_n + 2;
     }
+    if (ctx->exchange_open && d_out - out_base == ctx->d_cond.ptr) {  // resident, global slots
+      a.n_peer = (int)ctx->peers.size();
+      for (int r = 0; r < a.n_peer; ++r) a.peer_out[r] = ctx->peers[r];
+      a.peer_base = 0;
+    }
     if (pc.cfg.family == Family::Strip) {
       a.strip_base = sb_off[c] >= 0 ? ctx->d_strip_base.ptr + sb_off[c] : nullptr;
       a.strips_per_pair = pc.strips_per_pair;
@@ -1145,6 +1154,7 @@ void dtwg_destroy(dtwg_ctx* ctx) {
   ctx->d_prog.release();
   ctx->d_work.release();
   ctx->d_cols.release();
+  dtwg_exchange_close(ctx);
   for (double*& h : ctx->h_stage)
     if (h) cudaFreeHost(h);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
@@ -1537,6 +1547,76 @@ int dtwg_build_matrix(dtwg_ctx* ctx, const double* samples, const int64_t* offse
   }
   if (evaluations) *evaluations = (uint64_t)total;
   return DTWG_OK;
+}
+
+// ---- fused fill + all-gather over peer memory ----------------------------------------
+int dtwg_exchange_export(dtwg_ctx* ctx, int64_t p, unsigned char* handle_out) {
+  if (!ctx || !handle_out || p < 2) return DTWG_INVALID_ARGUMENTS;
+  cudaSetDevice(ctx->device);
+  int rc = ensure_resident(ctx, p);
+  if (rc) return rc;
+  ctx->cond_valid = false;
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, ctx->d_cond.ptr), "ipc export");
+  std::memcpy(handle_out, &h, sizeof(h));
+  return DTWG_OK;
+}
+
+int dtwg_exchange_open(dtwg_ctx* ctx, const unsigned char* handles, int n_ranks, int my_rank) {
+  if (!ctx || !handles || n_ranks < 1 || my_rank < 0 || my_rank >= n_ranks ||
+      n_ranks - 1 > dtwgpu::FillArgs::kMaxPeers)
+    return ctx ? ctx->fail(DTWG_INVALID_ARGUMENTS, "bad exchange geometry (at most %d peers)",
+                           dtwgpu::FillArgs::kMaxPeers)
+               : DTWG_INVALID_ARGUMENTS;
+  cudaSetDevice(ctx->device);
+  dtwg_exchange_close(ctx);
+  for (int r = 0; r < n_ranks; ++r) {
+    if (r == my_rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles + (size_t)r * sizeof(h), sizeof(h));
+    void* ptr = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      dtwg_exchange_close(ctx);
+      return ctx->cuda_fail(e, "ipc open of a peer's matrix");
+    }
+    ctx->peers.push_back(static_cast<double*>(ptr));
+  }
+  ctx->exchange_open = true;
+  return DTWG_OK;
+}
+
+int dtwg_exchange_close(dtwg_ctx* ctx) {
+  if (!ctx) return DTWG_INVALID_ARGUMENTS;
+  for (double* ptr : ctx->peers) cudaIpcCloseMemHandle(ptr);
+  ctx->peers.clear();
+  ctx->exchange_open = false;
+  return DTWG_OK;
+}
+
+int dtwg_exchange_fill(dtwg_ctx* ctx, int64_t half_width, int auto_widen, int precision,
+                       int64_t slot_begin, int64_t slot_end) {
+  if (!ctx) return DTWG_INVALID_ARGUMENTS;
+  if (!ctx->exchange_open) return ctx->fail(DTWG_INVALID_ARGUMENTS, "exchange not open");
+  if (ctx->mat_p != ctx->p)
+    return ctx->fail(DTWG_INVALID_ARGUMENTS, "exchange buffer is for %lld series, dataset has %lld",
+                     (long long)ctx->mat_p, (long long)ctx->p);
+  cudaSetDevice(ctx->device);
+  ctx->cond_valid = false;
+  if (slot_end <= slot_begin) return DTWG_OK;
+  // slots [b, e) into this rank's resident matrix at their global index, and (inside the
+  // same kernels) into every peer's
+  return dtwg_fill_slots(ctx, half_width, auto_widen, precision, slot_begin, slot_end,
+                         ctx->d_cond.ptr + slot_begin);
+}
+
+int dtwg_exchange_complete(dtwg_ctx* ctx) {
+  if (!ctx) return DTWG_INVALID_ARGUMENTS;
+  cudaSetDevice(ctx->device);
+  ctx->cond_valid = true;
+  ctx->square_valid = false;
+  return validate_resident(ctx);  // distance_matrix.hpp:34-38
 }
 
 int dtwg_adopt_condensed(dtwg_ctx* ctx, const double* condensed, int64_t p, int on_device) {

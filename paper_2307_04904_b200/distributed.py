@@ -137,12 +137,59 @@ def build_matrix_distributed(engine, ds: gen.Dataset, precision: int = 0,
     return fill_all_gather(fill, total, bounds, rank, device, group)
 
 
+def open_p2p_exchange(engine, p: int, rank: int, world: int, group=None) -> bool:
+    """Fused fill + all-gather over peer memory: export this rank's resident matrix buffer,
+    open every other rank's (CUDA IPC over NVLink), and agree on success. Returns False on
+    every rank (all exchanges closed) if any rank could not open a peer -- the caller then
+    uses the NCCL all-gather path."""
+    handle = engine.exchange_export(p)
+    handles = [None] * world
+    dist.all_gather_object(handles, handle, group=group)
+    ok = True
+    try:
+        engine.exchange_open(handles, rank)
+    except Exception:  # noqa: BLE001 -- reported collectively below
+        ok = False
+    oks = [None] * world
+    dist.all_gather_object(oks, ok, group=group)
+    if not all(oks):
+        engine.exchange_close()
+        return False
+    return True
+
+
+def fill_p2p(engine, ds: gen.Dataset, precision: int, bounds: Sequence[Tuple[int, int]],
+             rank: int, group=None) -> None:
+    """This rank's slots into every rank's matrix (one fused launch per class); after the
+    barrier each rank's resident matrix is complete -- no collective on the data path."""
+    b, e = bounds[rank]
+    engine.exchange_fill(ds.half_width, ds.auto_widen, precision, b, e)
+    engine.synchronize()
+    dist.barrier(group=group)
+    engine.exchange_complete()
+
+
+def build_matrix_p2p(engine, ds: gen.Dataset, precision: int = 0, group=None) -> bool:
+    """Sharded fill whose kernels write every distance into all ranks' resident matrices
+    (dtwg_exchange_*). Returns False (nothing filled) when peer memory is unavailable."""
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    engine.upload(ds.samples, ds.offsets)
+    if not open_p2p_exchange(engine, ds.p, rank, world, group):
+        return False
+    bounds = cell_bounds(ds.lengths, ds.half_width, ds.auto_widen, world)
+    fill_p2p(engine, ds, precision, bounds, rank, group)
+    engine._p_resident = ds.p
+    return True
+
+
 def kmedoids_distributed(engine, condensed: torch.Tensor, p: int, k: int, restarts: int,
                          max_iterations: int = 100, seed: int = 0, group=None) -> tuple:
     """Restart-sharded k-medoids over a replicated device-resident matrix."""
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    engine.adopt(None, p, on_device_ptr=condensed.data_ptr())
+    if condensed is not None:  # None: already resident (build_matrix_p2p)
+        engine.adopt(None, p, on_device_ptr=condensed.data_ptr())
     engine._p_resident = p
 
     def run(rb, re):

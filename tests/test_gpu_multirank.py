@@ -13,16 +13,22 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+@pytest.mark.parametrize("exchange", ["p2p", "nccl"])
 @pytest.mark.parametrize("config,subset", [(2, 160), (5, 120)])
-def test_two_rank_bench_assembles_the_matrix(config, subset):
+def test_two_rank_bench_assembles_the_matrix(config, subset, exchange):
+    """p2p: the fill kernels store every distance into both ranks' resident matrices
+    through CUDA IPC (same device here, NVLink peers on a multi-GPU node) -- no waiting
+    between the ranks' kernels; "nccl": slices all-gathered (over gloo here)."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", "--master-port=29531", os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "2", "--warmup", "1", "--config", str(config),
-           "--subset", str(subset), "--dist-backend", "gloo", "--no-cpu-baseline", "--kmedoids"]
+           "--subset", str(subset), "--dist-backend", "gloo", "--no-cpu-baseline", "--kmedoids",
+           "--exchange", exchange]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
     line = [l for l in out.stdout.splitlines() if l.startswith("{")][-1]
     d = json.loads(line)
     assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["config"]["exchange"] == exchange, d["config"]
     assert d["parity"].startswith("8/8"), d["parity"]
     assert d["kmedoids"]["parity"] is True
