@@ -351,3 +351,24 @@ def test_streamed_build_matches_oracle():
     r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+# ---------------------------------------------------------------- full-size parity
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg,q", [(1, 0), (2, 0), (3, 6000), (5, 1200)])
+def test_full_size_matrix_bitwise_vs_reference(eng, cfg, q):
+    """Whole matrices (c1, the headline c2; c3 and c5 at 6000 / 1200 series) against the
+    UNMODIFIED reference's own multithreaded build_matrix (oracle/_ref) -- every pair,
+    bit for bit, through the same kernels and plan the bench times."""
+    if not oracle.have_ref():
+        pytest.skip("oracle/_ref not built")
+    import os
+    ds = gen.make_config(cfg)
+    if q:
+        ds = ds.subset(q)
+    got = eng.build_condensed(ds.samples, ds.offsets, ds.half_width, ds.auto_widen)
+    plan = eng.last_plan()
+    want, ev = oracle.ref_build_condensed(ds.samples, ds.offsets, ds.half_width, ds.auto_widen,
+                                          workers=os.cpu_count() or 1)
+    assert ev == ds.p * (ds.p - 1) // 2
+    assert_bitwise(got, want, f"c{cfg} (p={ds.p}) plan={plan[:200]}")
