@@ -198,17 +198,28 @@ double band_cost(const Shape& s, const Cand& c, bool fp32) {
   return double(s.n + c.G * c.U - 1) * double(c.G * c.R) / (c.rate * (fp32 ? f32 : 1.0));
 }
 
-KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out);
+KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out, int64_t count, int sms);
 
 // Planner entry: a forced (family, G, R) wins when it can legally run the shape.
-KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cost_out);
+KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cost_out,
+                     int64_t count = 0);
 
-KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out) {
+// Fraction of the GPU a class of `count` pairs can keep busy with G lanes per pair: about
+// 8 warps per SM are needed to cover the cell chain (c1: 4950 pairs fill it with G = 32,
+// not with G = 4 -- 1765 against 946 GCUPS). count = 0: unknown (ragged classes).
+double fill_factor(int64_t count, int G, int sms) {
+  if (count <= 0) return 1.0;
+  const double warps = double(count) * G / 32.0;
+  return std::min(1.0, warps / (8.0 * sms));
+}
+
+KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out, int64_t count = 0,
+                           int sms = 148) {
   KernelCfg best{Family::Full, 32, 16, true, fp32};
   double bc = 1e300;
   const bool mask = s.hw < s.n - 1;  // a band that excludes some cell
   for (const Cand& c : kFull) {
-    const double cst = full_cost(s, c, mask, fp32);
+    const double cst = full_cost(s, c, mask, fp32) / fill_factor(count, c.G, sms);
     if (cst < bc) {
       bc = cst;
       best = KernelCfg{Family::Full, c.G, c.R, mask, fp32, -1, 1, c.TR};
@@ -218,7 +229,7 @@ KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out) {
     const int64_t K = 2 * s.hw + 1;
     for (const Cand& c : kBand) {
       if ((int64_t)c.G * c.R < K) continue;
-      const double cst = band_cost(s, c, fp32);
+      const double cst = band_cost(s, c, fp32) / fill_factor(count, c.G, sms);
       if (cst < bc) {
         bc = cst;
         best = KernelCfg{Family::Band, c.G, c.R, false, fp32, fp32 ? -1 : (int)(K % c.R), c.P,
@@ -346,7 +357,8 @@ struct dtwg_ctx {
 
 namespace {
 
-KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cost_out) {
+KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cost_out,
+                     int64_t count) {
   const bool mask = s.hw < s.n - 1;
   if (ctx->force_family >= 0) {
     // 0: full (2 rows/step), 1: band P=1, 2: band P=2, 3: full (4 rows/step), 4: band ring,
@@ -372,7 +384,7 @@ KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cos
       return f;
     }
   }
-  return choose_cfg_model(s, fp32, cost_out);
+  return choose_cfg_model(s, fp32, cost_out, count, ctx->num_sms);
 }
 
 // time_series.hpp:24-33 per-series checks (ids are the caller's; see dtwgpu.hpp).
@@ -433,8 +445,9 @@ Shape shape_of(const dtwg_ctx* ctx, int64_t a, int64_t b, int64_t hw, int auto_w
 // A Full-family class of few, long pairs leaves most of the GPU idle (one lane group per
 // pair, passes in sequence). Such classes become Strip classes: every column strip of
 // every pair is a work item for a full warp, pipelined along the pair (dtw_strip_kernel).
-// Rule: fewer pairs than half the warps the Full configuration keeps resident, and on
-// average at least two strips per pair. m_uniform < 0: ragged class (lengths per slot).
+// Rule: at most 4 pairs per SM with >= 2 strips per pair, or at most 16 pairs per SM with
+// >= 8 strips per pair (c1's 4950 pairs of 2 strips stay Full: 1763 against 776 GCUPS).
+// m_uniform < 0: ragged class (lengths per slot).
 constexpr int kStripR = 15;
 void maybe_strip(dtwg_ctx* ctx, PlanClass& pc, int64_t count, int64_t m_uniform) {
   if (count <= 0) return;
@@ -442,16 +455,15 @@ void maybe_strip(dtwg_ctx* ctx, PlanClass& pc, int64_t count, int64_t m_uniform)
   KernelCfg sc = pc.cfg;
   if (!forced) {
     if (pc.cfg.family != Family::Full || ctx->force_family >= 0) return;
-    const int64_t resident_groups = (int64_t)ctx->num_sms * dtwgpu::fill_blocks_per_sm(pc.cfg) *
-                                    (dtwgpu::kThreads / pc.cfg.G);
-    if (count * 2 > resident_groups) return;  // enough pairs to fill the GPU already
+    if (count > 16 * (int64_t)ctx->num_sms) return;  // enough pairs to fill the GPU already
     sc = KernelCfg{Family::Strip, 32, kStripR, pc.cfg.mask, pc.cfg.fp32, -1, 1, 4};
     if (!dtwgpu::fill_cfg_supported(sc)) return;
   }
   const int64_t W = 32 * (int64_t)sc.R;
+  const int64_t min_strips = count <= 4 * (int64_t)ctx->num_sms ? 2 : 8;  // strips per pair
   if (m_uniform >= 0) {
     const int64_t S = (m_uniform + W - 1) / W;
-    if (S < 2 && !forced) return;
+    if (S < min_strips && !forced) return;
     pc.strips_per_pair = (int)S;
   } else {
     std::vector<int64_t> base(count + 1, 0);
@@ -468,7 +480,7 @@ void maybe_strip(dtwg_ctx* ctx, PlanClass& pc, int64_t count, int64_t m_uniform)
       const int64_t m = std::min(ctx->h_len[i], ctx->h_len[j]);
       base[q + 1] = base[q] + (m + W - 1) / W;
     }
-    if (base[count] < 2 * count && !forced) return;
+    if (base[count] < min_strips * count && !forced) return;
     pc.strip_base = std::move(base);
   }
   pc.cfg = sc;
@@ -482,7 +494,7 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
   if (ctx->uniform) {
     PlanClass pc;
     const Shape s = shape_of(ctx, 0, 1, hw, auto_widen);
-    pc.cfg = choose_cfg(ctx, s, fp32, &pc.cost);
+    pc.cfg = choose_cfg(ctx, s, fp32, &pc.cost, se - sb);
     pc.max_n = s.n;
     plan.push_back(pc);
     maybe_strip(ctx, plan[0], se - sb, s.m);

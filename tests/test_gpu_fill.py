@@ -372,3 +372,17 @@ def test_full_size_matrix_bitwise_vs_reference(eng, cfg, q):
                                           workers=os.cpu_count() or 1)
     assert ev == ds.p * (ds.p - 1) // 2
     assert_bitwise(got, want, f"c{cfg} (p={ds.p}) plan={plan[:200]}")
+
+
+@pytest.mark.parametrize("cfg,expect", [(1, "full[G=32,R=16"), (2, "band[G=8,R=26,kr=19,P=1,ring,U=3]"),
+                                        (4, "full[G=32,R=15,T=4]")])
+def test_planner_picks_the_measured_best(eng, cfg, expect):
+    """The cost model's choices on the benchmark configs (profiles/round1_*: the sweeps
+    that calibrated it); guards against a model change silently regressing a config."""
+    ds = gen.make_config(cfg)
+    eng.upload(ds.samples, ds.offsets)
+    p = ds.p
+    import torch
+    out = torch.empty(p * (p - 1) // 2, dtype=torch.float64, device="cuda")
+    eng.fill_slots(ds.half_width, ds.auto_widen, 0, 0, 1000, out.data_ptr())  # plan only matters
+    assert expect in eng.last_plan(), eng.last_plan()
