@@ -384,5 +384,5 @@ def test_planner_picks_the_measured_best(eng, cfg, expect):
     p = ds.p
     import torch
     out = torch.empty(p * (p - 1) // 2, dtype=torch.float64, device="cuda")
-    eng.fill_slots(ds.half_width, ds.auto_widen, 0, 0, 1000, out.data_ptr())  # plan only matters
+    eng.fill_slots(ds.half_width, ds.auto_widen, 0, 0, p * (p - 1) // 2, out.data_ptr())
     assert expect in eng.last_plan(), eng.last_plan()
