@@ -74,9 +74,10 @@ constexpr int kThreads = 128;
 cudaError_t measure_cell_peak(cudaStream_t st, int sms, bool fp32, double* cells_per_s);
 
 // ---- k-medoids sweep kernels (kmedoids.cu) -------------------------------------
-cudaError_t launch_silhouette(const double* square, int64_t p, const int32_t* members,
-                              const int64_t* cluster_begin, const int32_t* cls, int64_t k,
-                              double* sil, cudaStream_t s);
+// The sweep kernels read the dense square (condensed = false) or the condensed matrix.
+cudaError_t launch_silhouette(const double* matrix, bool condensed, int64_t p,
+                              const int32_t* members, const int64_t* cluster_begin,
+                              const int32_t* cls, int64_t k, double* sil, cudaStream_t s);
 cudaError_t launch_to_f32(const double* in, int64_t n, float* out, cudaStream_t s);
 cudaError_t launch_band_pad(const double* samples, const int64_t* off, const int64_t* boff,
                             int64_t p, int64_t pad, void* out, bool fp32, cudaStream_t s);
@@ -84,12 +85,14 @@ cudaError_t launch_expand_square(const double* condensed, int64_t p, double* squ
                                  cudaStream_t s);
 cudaError_t launch_validate_condensed(const double* condensed, int64_t total, int* bad,
                                       cudaStream_t s);
-cudaError_t launch_nearest_update(const double* square, int64_t p, int64_t current,
-                                  const uint8_t* chosen, double* nearest, cudaStream_t s);
-cudaError_t launch_assign(const double* square, int64_t p, const int64_t* medoids, int64_t k,
-                          int64_t* assignment, double* dist, cudaStream_t s);
-cudaError_t launch_update(const double* square, int64_t p, const int32_t* members,
-                          const int64_t* cluster_begin, int64_t k, int64_t* best_member,
-                          double* best_sum, cudaStream_t s);
+cudaError_t launch_nearest_update(const double* matrix, bool condensed, int64_t p,
+                                  int64_t current, const uint8_t* chosen, double* nearest,
+                                  cudaStream_t s);
+cudaError_t launch_assign(const double* matrix, bool condensed, int64_t p,
+                          const int64_t* medoids, int64_t k, int64_t* assignment, double* dist,
+                          cudaStream_t s);
+cudaError_t launch_update(const double* matrix, bool condensed, int64_t p,
+                          const int32_t* members, const int64_t* cluster_begin, int64_t k,
+                          int64_t* best_member, double* best_sum, cudaStream_t s);
 
 }  // namespace dtwgpu

@@ -1090,7 +1090,7 @@ __device__ __forceinline__ void unit_steps(int nst, int& i1, const typename Ar::
 // Resident CTAs the register allocation is capped for (ILP U needs fewer warps; wide R
 // keeps 4 CTAs without spills, narrower ones fit 5).
 #ifndef DTWG_UNIT_MINB
-#define DTWG_UNIT_MINB(R) ((R) >= 20 ? 4 : 5)
+#define DTWG_UNIT_MINB(R) ((R) >= 40 ? 3 : ((R) >= 20 ? 4 : 5))
 #endif
 template <int G, int R, int U, int KR, class Ar>
 __global__ void __launch_bounds__(kThreads, DTWG_UNIT_MINB(R)) dtw_bandunit_kernel(const FillArgs A) {

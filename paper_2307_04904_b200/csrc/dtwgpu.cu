@@ -319,7 +319,8 @@ struct dtwg_ctx {
   DevBuf<double> d_cond;
   bool cond_valid = false;
   DevBuf<double> d_square;
-  bool square_valid = false;
+  bool square_valid = false;  // the sweep view is ready (square expanded, or condensed mode)
+  bool km_condensed = false;  // sweeps read the condensed matrix (square does not fit)
   DevBuf<int> d_flag;
 
   // k-medoids sweep statistics (dtwg_km_stats): device time and algorithmic bytes of the
@@ -895,10 +896,27 @@ int validate_resident(dtwg_ctx* ctx) {
   return DTWG_OK;
 }
 
+// The sweeps read a dense p x p square (contiguous rows) when it fits in HBM next to the
+// condensed matrix -- p up to ~140 000 on a 180 GB B200 -- and the condensed matrix
+// itself beyond that (or with DTWGPU_KM_CONDENSED=1); both give identical results.
+const double* km_matrix(const dtwg_ctx* ctx) {
+  return ctx->km_condensed ? ctx->d_cond.ptr : ctx->d_square.ptr;
+}
+
 int ensure_square(dtwg_ctx* ctx) {
   if (ctx->square_valid) return DTWG_OK;
   if (!ctx->cond_valid) return ctx->fail(DTWG_INVALID_ARGUMENTS, "no resident distance matrix");
   const int64_t p = ctx->mat_p;
+  const char* force = std::getenv("DTWGPU_KM_CONDENSED");
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const double need = double(p) * double(p) * 8.0 - double(ctx->d_square.cap) * 8.0;
+  ctx->km_condensed = (force && force[0] == '1') || need > 0.85 * double(free_b);
+  if (ctx->km_condensed) {
+    ctx->d_square.release();
+    ctx->square_valid = true;
+    return DTWG_OK;
+  }
   CU(ctx->d_square.reserve((size_t)(p * p)), "cudaMalloc square");
   if (p >= 2) {
     CU(dtwgpu::launch_expand_square(ctx->d_cond.ptr, p, ctx->d_square.ptr, ctx->stream),
@@ -925,7 +943,8 @@ int km_assign(KmState& S, const std::vector<int64_t>& medoids) {
                      cudaMemcpyHostToDevice, ctx->stream),
      "H2D medoids");
   CU(cudaEventRecord(ctx->km0, ctx->stream), "event");
-  CU(dtwgpu::launch_assign(ctx->d_square.ptr, S.p, ctx->d_medoids.ptr, (int64_t)medoids.size(),
+  CU(dtwgpu::launch_assign(km_matrix(ctx), ctx->km_condensed, S.p, ctx->d_medoids.ptr,
+                           (int64_t)medoids.size(),
                            ctx->d_assign.ptr, ctx->d_dist.ptr, ctx->stream),
      "assign");
   CU(cudaEventRecord(ctx->km1, ctx->stream), "event");
@@ -978,7 +997,7 @@ int km_update(KmState& S, const std::vector<int64_t>& medoids, std::vector<int64
   CU(cudaMemcpyAsync(ctx->d_cb.ptr, cb.data(), (k + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
      "H2D cb");
   CU(cudaEventRecord(ctx->km0, ctx->stream), "event");
-  CU(dtwgpu::launch_update(ctx->d_square.ptr, p, ctx->d_members.ptr, ctx->d_cb.ptr, k,
+  CU(dtwgpu::launch_update(km_matrix(ctx), ctx->km_condensed, p, ctx->d_members.ptr, ctx->d_cb.ptr, k,
                            ctx->d_best_member.ptr, ctx->d_best_sum.ptr, ctx->stream),
      "update");
   CU(cudaEventRecord(ctx->km1, ctx->stream), "event");
@@ -1051,7 +1070,7 @@ int km_seeds(KmState& S, int64_t k, SplitMix64& rng, std::vector<int64_t>& medoi
     CU(cudaMemcpyAsync(ctx->d_chosen.ptr + current, &chosen[current], 1, cudaMemcpyHostToDevice,
                        ctx->stream),
        "H2D chosen");
-    CU(dtwgpu::launch_nearest_update(ctx->d_square.ptr, p, current, ctx->d_chosen.ptr,
+    CU(dtwgpu::launch_nearest_update(km_matrix(ctx), ctx->km_condensed, p, current, ctx->d_chosen.ptr,
                                      ctx->d_nearest.ptr, ctx->stream),
        "nearest");
     ctx->launches++;
@@ -1366,7 +1385,7 @@ int dtwg_silhouette(dtwg_ctx* ctx, const int64_t* medoids, int64_t k, const int6
      "H2D cb");
   CU(cudaMemcpyAsync(ctx->d_sil_cls.ptr, cls.data(), p * 4, cudaMemcpyHostToDevice, ctx->stream),
      "H2D cls");
-  CU(dtwgpu::launch_silhouette(ctx->d_square.ptr, p, ctx->d_members.ptr, ctx->d_cb.ptr,
+  CU(dtwgpu::launch_silhouette(km_matrix(ctx), ctx->km_condensed, p, ctx->d_members.ptr, ctx->d_cb.ptr,
                                ctx->d_sil_cls.ptr, k, ctx->d_dist.ptr, ctx->stream),
      "silhouette");
   ctx->launches++;
@@ -1735,7 +1754,7 @@ int dtwg_km_nearest_update(dtwg_ctx* ctx, int64_t current, const uint8_t* chosen
   CU(cudaMemcpyAsync(ctx->d_nearest.ptr, nearest_inout, p * 8, cudaMemcpyHostToDevice,
                      ctx->stream),
      "H2D");
-  CU(dtwgpu::launch_nearest_update(ctx->d_square.ptr, p, current, ctx->d_chosen.ptr,
+  CU(dtwgpu::launch_nearest_update(km_matrix(ctx), ctx->km_condensed, p, current, ctx->d_chosen.ptr,
                                    ctx->d_nearest.ptr, ctx->stream),
      "nearest");
   ctx->launches++;

@@ -28,6 +28,25 @@ namespace {
 
 __device__ __forceinline__ int64_t coff(int64_t i, int64_t p) { return i * p - i * (i + 1) / 2; }
 
+// The sweeps read D(r, c) through a view: the dense square (contiguous rows, the fast
+// path) or, when p x p doubles do not fit next to everything else in HBM, the condensed
+// matrix itself (D(r, r) = 0; other entries at the upper-triangle slot). Both return the
+// same stored double for (r, c) and (c, r), so results are identical either way.
+struct SquareView {
+  const double* m;
+  int64_t p;
+  __device__ __forceinline__ double operator()(int64_t r, int64_t c) const { return m[r * p + c]; }
+};
+struct CondView {
+  const double* m;
+  int64_t p;
+  __device__ __forceinline__ double operator()(int64_t r, int64_t c) const {
+    if (r == c) return 0.0;
+    const int64_t i = r < c ? r : c, j = r < c ? c : r;
+    return m[coff(i, p) + (j - i - 1)];
+  }
+};
+
 // Dense square from condensed: 32x32 tiles; lower tiles read their transposed upper
 // tile coalesced through shared memory.
 __global__ void expand_square_kernel(const double* __restrict__ cond, int64_t p,
@@ -72,14 +91,14 @@ __global__ void validate_kernel(const double* __restrict__ cond, int64_t total, 
 }
 
 // kmedoids.hpp:48-52: nearest[j] = std::min(nearest[j], D(j, current)) for unchosen j.
-__global__ void nearest_update_kernel(const double* __restrict__ sq, int64_t p, int64_t current,
+template <class V>
+__global__ void nearest_update_kernel(const V D, int64_t p, int64_t current,
                                       const uint8_t* __restrict__ chosen,
                                       double* __restrict__ nearest) {
-  const double* row = sq + current * p;  // D(current, j) == D(j, current)
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p;
        j += (int64_t)gridDim.x * blockDim.x) {
     if (chosen[j]) continue;
-    const double a = nearest[j], b = row[j];
+    const double a = nearest[j], b = D(current, j);  // D(current, j) == D(j, current)
     nearest[j] = b < a ? b : a;
   }
 }
@@ -87,8 +106,8 @@ __global__ void nearest_update_kernel(const double* __restrict__ sq, int64_t p, 
 // cluster_result.hpp:40-61. Medoids ascending; a medoid owns itself; otherwise the
 // strictly smaller distance wins, so ties keep the lowest medoid index. Row reads
 // D(medoid_t, j) are coalesced across j.
-__global__ void assign_kernel(const double* __restrict__ sq, int64_t p,
-                              const int64_t* __restrict__ medoids, int64_t k,
+template <class V>
+__global__ void assign_kernel(const V D, int64_t p, const int64_t* __restrict__ medoids, int64_t k,
                               int64_t* __restrict__ assignment, double* __restrict__ dist) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p;
        j += (int64_t)gridDim.x * blockDim.x) {
@@ -100,10 +119,10 @@ __global__ void assign_kernel(const double* __restrict__ sq, int64_t p,
       continue;
     }
     int64_t best = __ldg(medoids);
-    double bd = sq[best * p + j];
+    double bd = D(best, j);
     for (int64_t t = 1; t < k; ++t) {
       const int64_t mt = __ldg(medoids + t);
-      const double d = sq[mt * p + j];
+      const double d = D(mt, j);
       if (d < bd) {
         bd = d;
         best = mt;
@@ -129,8 +148,8 @@ __global__ void assign_kernel(const double* __restrict__ sq, int64_t p,
 //     have the smallest sequential sum; the remaining "contenders" (normally just one)
 //     get the reference's exact sequential sum, and the (sum, position) minimum over
 //     them is the reference's choice, bit for bit.
-__global__ void tree_sum_kernel(const double* __restrict__ sq, int64_t p,
-                                const int32_t* __restrict__ members,
+template <class V>
+__global__ void tree_sum_kernel(const V D, int64_t p, const int32_t* __restrict__ members,
                                 const int64_t* __restrict__ cb, int64_t k,
                                 double* __restrict__ tsum) {
   const int lane = threadIdx.x & 31;
@@ -143,23 +162,23 @@ __global__ void tree_sum_kernel(const double* __restrict__ sq, int64_t p,
       else hi = mid - 1;
     }
     const int64_t b = __ldg(cb + lo), e = __ldg(cb + lo + 1);
-    const double* row = sq + (int64_t)__ldg(members + q) * p;  // D[a][.] == D[.][a]
+    const int64_t a = __ldg(members + q);  // D[a][.] == D[.][a]
     double acc = 0.0;
     int64_t t = b + lane;
     for (; t + 96 < e; t += 128) {  // 4 loads in flight per lane
-      const double v0 = row[__ldg(members + t)], v1 = row[__ldg(members + t + 32)];
-      const double v2 = row[__ldg(members + t + 64)], v3 = row[__ldg(members + t + 96)];
+      const double v0 = D(a, __ldg(members + t)), v1 = D(a, __ldg(members + t + 32));
+      const double v2 = D(a, __ldg(members + t + 64)), v3 = D(a, __ldg(members + t + 96));
       acc = __dadd_rn(__dadd_rn(acc, v0), __dadd_rn(__dadd_rn(v1, v2), v3));
     }
-    for (; t < e; t += 32) acc = __dadd_rn(acc, row[__ldg(members + t)]);
+    for (; t < e; t += 32) acc = __dadd_rn(acc, D(a, __ldg(members + t)));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
     if (lane == 0) tsum[q] = acc;
   }
 }
 
-__global__ void cluster_select_kernel(const double* __restrict__ sq, int64_t p,
-                                      const int32_t* __restrict__ members,
+template <class V>
+__global__ void cluster_select_kernel(const V D, int64_t p, const int32_t* __restrict__ members,
                                       const int64_t* __restrict__ cb,
                                       const double* __restrict__ tsum, int64_t* best_member,
                                       double* best_sum) {
@@ -187,17 +206,17 @@ __global__ void cluster_select_kernel(const double* __restrict__ sq, int64_t p,
   int64_t bq = -1;
   for (int64_t q = b + threadIdx.x; q < e; q += blockDim.x) {
     if (!(tsum[q] <= thr)) continue;
-    const double* row = sq + (int64_t)members[q] * p;
+    const int64_t a = members[q];
     double sum = 0.0;
     int64_t t = b;
     for (; t + 8 <= e; t += 8) {  // loads batched, additions kept in order
       double v[8];
 #pragma unroll
-      for (int uu = 0; uu < 8; ++uu) v[uu] = row[__ldg(members + t + uu)];
+      for (int uu = 0; uu < 8; ++uu) v[uu] = D(a, __ldg(members + t + uu));
 #pragma unroll
       for (int uu = 0; uu < 8; ++uu) sum = __dadd_rn(sum, v[uu]);
     }
-    for (; t < e; ++t) sum = __dadd_rn(sum, row[__ldg(members + t)]);
+    for (; t < e; ++t) sum = __dadd_rn(sum, D(a, __ldg(members + t)));
     if (bq < 0 || sum < bv) {  // q ascending per thread: strict < keeps the first minimum
       bv = sum;
       bq = q;
@@ -251,7 +270,8 @@ __global__ void to_f32_kernel(const double* __restrict__ in, int64_t n, float* _
 // (b - a) / max(a, b) (0 when that is 0; singletons score 0). Every sum runs over the
 // members in ascending order, as the reference does, reading D(m, t) = D(t, m) so a warp
 // of consecutive t reads one coalesced row segment per member m.
-__global__ void silhouette_kernel(const double* __restrict__ sq, int64_t p,
+template <class V>
+__global__ void silhouette_kernel(const V D, int64_t p,
                                   const int32_t* __restrict__ members,
                                   const int64_t* __restrict__ cb, const int32_t* __restrict__ cls,
                                   int64_t k, double* __restrict__ sil) {
@@ -266,7 +286,7 @@ __global__ void silhouette_kernel(const double* __restrict__ sq, int64_t p,
     double own = 0.0;
     for (int64_t q = cb[c]; q < cb[c + 1]; ++q) {
       const int64_t m = members[q];
-      if (m != t) own = __dadd_rn(own, sq[m * p + t]);
+      if (m != t) own = __dadd_rn(own, D(m, t));
     }
     const double a = __ddiv_rn(own, (double)(own_n - 1));
     double b = CUDART_INF;
@@ -274,7 +294,7 @@ __global__ void silhouette_kernel(const double* __restrict__ sq, int64_t p,
       const int64_t n_o = cb[o + 1] - cb[o];
       if (o == c || n_o == 0) continue;
       double across = 0.0;
-      for (int64_t q = cb[o]; q < cb[o + 1]; ++q) across = __dadd_rn(across, sq[(int64_t)members[q] * p + t]);
+      for (int64_t q = cb[o]; q < cb[o + 1]; ++q) across = __dadd_rn(across, D((int64_t)members[q], t));
       const double mean = __ddiv_rn(across, (double)n_o);
       b = mean < b ? mean : b;  // std::min(b, mean)
     }
@@ -306,11 +326,15 @@ cudaError_t launch_to_f32(const double* in, int64_t n, float* out, cudaStream_t 
   return cudaGetLastError();
 }
 
-cudaError_t launch_silhouette(const double* square, int64_t p, const int32_t* members,
-                              const int64_t* cluster_begin, const int32_t* cls, int64_t k,
-                              double* sil, cudaStream_t s) {
-  silhouette_kernel<<<grid_for(p, 128), 128, 0, s>>>(square, p, members, cluster_begin, cls, k,
-                                                      sil);
+cudaError_t launch_silhouette(const double* matrix, bool condensed, int64_t p,
+                              const int32_t* members, const int64_t* cluster_begin,
+                              const int32_t* cls, int64_t k, double* sil, cudaStream_t s) {
+  if (condensed)
+    silhouette_kernel<<<grid_for(p, 128), 128, 0, s>>>(CondView{matrix, p}, p, members,
+                                                        cluster_begin, cls, k, sil);
+  else
+    silhouette_kernel<<<grid_for(p, 128), 128, 0, s>>>(SquareView{matrix, p}, p, members,
+                                                        cluster_begin, cls, k, sil);
   return cudaGetLastError();
 }
 
@@ -327,30 +351,49 @@ cudaError_t launch_validate_condensed(const double* condensed, int64_t total, in
   return cudaGetLastError();
 }
 
-cudaError_t launch_nearest_update(const double* square, int64_t p, int64_t current,
-                                  const uint8_t* chosen, double* nearest, cudaStream_t s) {
-  nearest_update_kernel<<<grid_for(p, 256), 256, 0, s>>>(square, p, current, chosen, nearest);
+cudaError_t launch_nearest_update(const double* matrix, bool condensed, int64_t p,
+                                  int64_t current, const uint8_t* chosen, double* nearest,
+                                  cudaStream_t s) {
+  if (condensed)
+    nearest_update_kernel<<<grid_for(p, 256), 256, 0, s>>>(CondView{matrix, p}, p, current,
+                                                           chosen, nearest);
+  else
+    nearest_update_kernel<<<grid_for(p, 256), 256, 0, s>>>(SquareView{matrix, p}, p, current,
+                                                           chosen, nearest);
   return cudaGetLastError();
 }
 
-cudaError_t launch_assign(const double* square, int64_t p, const int64_t* medoids, int64_t k,
-                          int64_t* assignment, double* dist, cudaStream_t s) {
-  assign_kernel<<<grid_for(p, 256), 256, 0, s>>>(square, p, medoids, k, assignment, dist);
+cudaError_t launch_assign(const double* matrix, bool condensed, int64_t p,
+                          const int64_t* medoids, int64_t k, int64_t* assignment, double* dist,
+                          cudaStream_t s) {
+  if (condensed)
+    assign_kernel<<<grid_for(p, 256), 256, 0, s>>>(CondView{matrix, p}, p, medoids, k,
+                                                   assignment, dist);
+  else
+    assign_kernel<<<grid_for(p, 256), 256, 0, s>>>(SquareView{matrix, p}, p, medoids, k,
+                                                   assignment, dist);
   return cudaGetLastError();
 }
 
-cudaError_t launch_update(const double* square, int64_t p, const int32_t* members,
-                          const int64_t* cluster_begin, int64_t k, int64_t* best_member,
-                          double* best_sum, cudaStream_t s) {
+cudaError_t launch_update(const double* matrix, bool condensed, int64_t p,
+                          const int32_t* members, const int64_t* cluster_begin, int64_t k,
+                          int64_t* best_member, double* best_sum, cudaStream_t s) {
   // sums scratch lives right after best_sum (k doubles) -- caller allocates p more.
   double* sums = best_sum + k;
   const int64_t warps = std::min<int64_t>(p, 148 * 64);
-  tree_sum_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(square, p, members, cluster_begin,
-                                                               k, sums);
+  const unsigned tb = (unsigned)((warps + 7) / 8);
+  if (condensed)
+    tree_sum_kernel<<<tb, 256, 0, s>>>(CondView{matrix, p}, p, members, cluster_begin, k, sums);
+  else
+    tree_sum_kernel<<<tb, 256, 0, s>>>(SquareView{matrix, p}, p, members, cluster_begin, k, sums);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  cluster_select_kernel<<<(unsigned)k, 256, 0, s>>>(square, p, members, cluster_begin, sums,
-                                                    best_member, best_sum);
+  if (condensed)
+    cluster_select_kernel<<<(unsigned)k, 256, 0, s>>>(CondView{matrix, p}, p, members,
+                                                      cluster_begin, sums, best_member, best_sum);
+  else
+    cluster_select_kernel<<<(unsigned)k, 256, 0, s>>>(SquareView{matrix, p}, p, members,
+                                                      cluster_begin, sums, best_member, best_sum);
   return cudaGetLastError();
 }
 

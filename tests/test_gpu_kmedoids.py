@@ -180,3 +180,25 @@ def test_update_near_ties_match_reference(spread):
             assert got == list(upd_ref), (spread, medoids)
         cfg = KMedoidsConfig(k=len(medoids), restarts=2, seed=7)
         check_same(D, p, cfg)
+
+
+@pytest.mark.parametrize("cfgno,q", [(3, 900), (5, 300)])
+def test_condensed_view_matches_square(monkeypatch, cfgno, q):
+    """Matrices whose p x p square does not fit in HBM are swept straight from the
+    condensed storage; forced here, every result must equal the square path's and the
+    reference's."""
+    ds = gen.make_config(cfgno).subset(q)
+    m = api.build_matrix_packed(ds.samples, ds.offsets,
+                                WarpWindow(None if ds.half_width < 0 else ds.half_width),
+                                ds.auto_widen)
+    cfg = KMedoidsConfig(k=ds.k, restarts=3, seed=1)
+    a = kmedoids(m, cfg)
+    sa = api.silhouette_scores(m, a)
+    monkeypatch.setenv("DTWGPU_KM_CONDENSED", "1")
+    m2 = DistanceMatrix.from_condensed(ds.p, m.condensed())
+    b = kmedoids(m2, cfg)
+    sb = api.silhouette_scores(m2, b)
+    assert (a.medoids, a.assignment, a.total_cost) == (b.medoids, b.assignment, b.total_cost)
+    assert sa.silhouette == sb.silhouette and sa.mean_silhouette == sb.mean_silhouette
+    med, asg, cost = kref(m.condensed(), ds.p, cfg)
+    assert b.medoids == list(med) and b.assignment == list(asg) and b.total_cost == cost
