@@ -386,3 +386,45 @@ def test_planner_picks_the_measured_best(eng, cfg, expect):
     out = torch.empty(p * (p - 1) // 2, dtype=torch.float64, device="cuda")
     eng.fill_slots(ds.half_width, ds.auto_widen, 0, 0, p * (p - 1) // 2, out.data_ptr())
     assert expect in eng.last_plan(), eng.last_plan()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_full_size_properties(eng, cfg):
+    """Full-size c4 / c5 (4e12 cells: beyond a CPU oracle in test time) through
+    size-independent properties: the matrix of the REVERSED dataset is the same matrix
+    with rows/columns permuted, bit for bit (DTW is symmetric bitwise: (a-b)^2 == (b-a)^2
+    and min is commutative), and 64 random pairs equal the oracle."""
+    import torch
+    ds = gen.make_config(cfg)
+    p = ds.p
+    total = p * (p - 1) // 2
+    a = torch.empty(total, dtype=torch.float64, device="cuda")
+    eng.upload(ds.samples, ds.offsets)
+    eng.fill_slots(ds.half_width, ds.auto_widen, 0, 0, total, a.data_ptr())
+    A = a.cpu().numpy()
+    lens = np.diff(ds.offsets)
+    rows = [ds.samples[ds.offsets[i]:ds.offsets[i + 1]] for i in range(p)][::-1]
+    rs, ro = pack(rows)
+    b = torch.empty(total, dtype=torch.float64, device="cuda")
+    eng.upload(rs, ro)
+    eng.fill_slots(ds.half_width, ds.auto_widen, 0, 0, total, b.data_ptr())
+    B = b.cpu().numpy()
+    # slot of (i, j), i < j, in a p-series condensed matrix
+    rng = np.random.default_rng(cfg)
+    i = rng.integers(0, p, size=200000)
+    j = rng.integers(0, p, size=200000)
+    keep = i != j
+    i, j = np.minimum(i[keep], j[keep]), np.maximum(i[keep], j[keep])
+    off = lambda r: r * p - r * (r + 1) // 2
+    sa = off(i) + (j - i - 1)
+    ri, rj = p - 1 - j, p - 1 - i  # reversed indices, ri < rj
+    sb = off(ri) + (rj - ri - 1)
+    assert_bitwise(A[sa], B[sb], f"c{cfg} reversed-order symmetry")
+    # and the whole matrices hold the same multiset of values
+    assert np.array_equal(np.sort(A), np.sort(B))
+    for t in range(64):
+        x = ds.series(int(i[t]))
+        y = ds.series(int(j[t]))
+        hw = int(gen.effective_half_width(lens[i[t]], lens[j[t]], ds.half_width, ds.auto_widen))
+        assert A[sa[t]] == oracle.dtw(x, y, hw), (cfg, int(i[t]), int(j[t]))
