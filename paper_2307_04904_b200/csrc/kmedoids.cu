@@ -202,24 +202,60 @@ __global__ void cluster_select_kernel(const V D, int64_t p, const int32_t* __res
   const double u = 1.1102230246251565e-16;  // 2^-53
   const double g = n * u / (1.0 - n * u);
   const double thr = mn * (1.0 + 8.0 * g) * (1.0 + 4.0 * u);
-  double bv = CUDART_INF;
-  int64_t bq = -1;
+  // Collect the contenders; the block then computes each one's sequential sum: all
+  // threads gather the candidate's member distances into shared memory (parallel loads),
+  // thread 0 adds them in ascending member order (the reference's order).
+  constexpr int kMaxCand = 64, kChunk = 2048;
+  __shared__ int ncand;
+  __shared__ int64_t cand[kMaxCand];
+  __shared__ double vals[kChunk];
+  if (threadIdx.x == 0) ncand = 0;
+  __syncthreads();
   for (int64_t q = b + threadIdx.x; q < e; q += blockDim.x) {
     if (!(tsum[q] <= thr)) continue;
-    const int64_t a = members[q];
-    double sum = 0.0;
-    int64_t t = b;
-    for (; t + 8 <= e; t += 8) {  // loads batched, additions kept in order
-      double v[8];
-#pragma unroll
-      for (int uu = 0; uu < 8; ++uu) v[uu] = D(a, __ldg(members + t + uu));
-#pragma unroll
-      for (int uu = 0; uu < 8; ++uu) sum = __dadd_rn(sum, v[uu]);
+    const int slot = atomicAdd(&ncand, 1);
+    if (slot < kMaxCand) cand[slot] = q;
+  }
+  __syncthreads();
+  double bv = CUDART_INF;
+  int64_t bq = -1;
+  if (ncand <= kMaxCand) {
+    for (int ci = 0; ci < ncand; ++ci) {
+      const int64_t q = cand[ci];
+      const int64_t a = members[q];
+      double sum = 0.0;
+      for (int64_t t0 = b; t0 < e; t0 += kChunk) {
+        const int64_t len = e - t0 < kChunk ? e - t0 : kChunk;
+        for (int64_t t = threadIdx.x; t < len; t += blockDim.x) vals[t] = D(a, __ldg(members + t0 + t));
+        __syncthreads();
+        if (threadIdx.x == 0)
+          for (int64_t t = 0; t < len; ++t) sum = __dadd_rn(sum, vals[t]);
+        __syncthreads();
+      }
+      // contenders arrive in any order: lexicographic (sum, position) keeps the first minimum
+      if (threadIdx.x == 0 && (bq < 0 || sum < bv || (sum == bv && q < bq))) {
+        bv = sum;
+        bq = q;
+      }
     }
-    for (; t < e; ++t) sum = __dadd_rn(sum, D(a, __ldg(members + t)));
-    if (bq < 0 || sum < bv) {  // q ascending per thread: strict < keeps the first minimum
-      bv = sum;
-      bq = q;
+  } else {  // many near-equal sums (e.g. duplicated series): one thread per contender
+    for (int64_t q = b + threadIdx.x; q < e; q += blockDim.x) {
+      if (!(tsum[q] <= thr)) continue;
+      const int64_t a = members[q];
+      double sum = 0.0;
+      int64_t t = b;
+      for (; t + 8 <= e; t += 8) {  // loads batched, additions kept in order
+        double v[8];
+#pragma unroll
+        for (int uu = 0; uu < 8; ++uu) v[uu] = D(a, __ldg(members + t + uu));
+#pragma unroll
+        for (int uu = 0; uu < 8; ++uu) sum = __dadd_rn(sum, v[uu]);
+      }
+      for (; t < e; ++t) sum = __dadd_rn(sum, D(a, __ldg(members + t)));
+      if (bq < 0 || sum < bv) {  // q ascending per thread: strict < keeps the first minimum
+        bv = sum;
+        bq = q;
+      }
     }
   }
   sv[threadIdx.x] = bv;
