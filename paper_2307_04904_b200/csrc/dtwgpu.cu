@@ -232,8 +232,10 @@ KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out, int64_t 
       const double cst = band_cost(s, c, fp32) / fill_factor(count, c.G, sms);
       if (cst < bc) {
         bc = cst;
-        best = KernelCfg{Family::Band, c.G, c.R, false, fp32, fp32 ? -1 : (int)(K % c.R), c.P,
-                         2, c.ring, c.U};
+        // static kill position: fp64 everywhere, fp32 for the unit-ring variant
+        const bool static_kr = !fp32 || (c.ring && c.U > 1);
+        best = KernelCfg{Family::Band, c.G, c.R, false, fp32, static_kr ? (int)(K % c.R) : -1,
+                         c.P, 2, c.ring, c.U};
       }
     }
   }
@@ -375,7 +377,8 @@ KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cos
     const bool band = ff == 1 || ff == 2 || ff == 4 || ff > 10;
     KernelCfg f{band ? Family::Band : Family::Full, ctx->force_G, ctx->force_R,
                 band ? false : mask, fp32,
-                (band && !fp32 && ctx->force_R > 0) ? (int)((2 * s.hw + 1) % ctx->force_R) : -1,
+                (band && (!fp32 || ff > 10) && ctx->force_R > 0) ? (int)((2 * s.hw + 1) % ctx->force_R)
+                                                                  : -1,
                 ff == 2 ? 2 : 1, ff == 3 ? 4 : 2, ff == 4 || ff > 10, ff > 10 ? ff - 10 : 1};
     const bool ok = dtwgpu::fill_cfg_supported(f) &&
                     (f.family == Family::Full ||

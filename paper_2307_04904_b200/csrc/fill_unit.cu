@@ -1,5 +1,6 @@
-// fill_unit.cu -- instantiations of the units-per-lane ring Band variant (dtw_kernels.cuh).
-// fp64 kernels for every static kill position KR = (2hw+1) % R; fp32 with a runtime KR.
+// fill_unit.cu -- fp64 instantiations of the units-per-lane ring Band variant
+// (dtw_kernels.cuh) for every static kill position KR = (2hw+1) % R, plus the runtime-KR
+// fallback; fp32 lives in fill_unit32.cu (compiled in parallel).
 #include "dtw_kernels.cuh"
 #include "fill_table.h"
 
@@ -16,10 +17,12 @@ struct UnitTable {
 };
 }  // namespace
 
+const void* unit32_kernel_ptr(int G, int R, int U, int kr);
+
 const void* unit_kernel_ptr(int G, int R, int U, int kr, bool fp32) {
+  if (fp32) return unit32_kernel_ptr(G, R, U, kr);
 #define DTWG_UN(g, r, u)                                                          \
   if (G == g && R == r && U == u) {                                               \
-    if (fp32) return (const void*)dtw_bandunit_kernel<g, r, u, -1, F32>;         \
     if (kr < 0) return (const void*)dtw_bandunit_kernel<g, r, u, -1, F64>;       \
     return UnitTable<g, r, u, r - 1>::get(kr);                                    \
   }
