@@ -49,7 +49,11 @@ namespace dtwgpu {
 namespace kern {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kRenormSteps = 8;  // fp32 mode: steps between per-lane offset renormalisations
+// fp32 mode: steps between per-lane offset renormalisations. The Band kernels key them on
+// the warp-uniform step index (not the lane's skewed row), so a whole warp renormalises
+// together on 1 step in 8 instead of some lane on every step (which made the predicated
+// renormalisation run every step: ~1.5 extra instructions per cell).
+constexpr int kRenormSteps = 8;
 
 __device__ __forceinline__ int64_t row_off(int64_t i, int64_t p) { return i * p - i * (i + 1) / 2; }
 
@@ -678,7 +682,7 @@ __device__ __forceinline__ void band_steps(
           if (lK[p] == gl && rK[p] != 0) kill_cell<R>(pv[p], rK[p], INF);
         }
         if constexpr (kF32) {
-          if (((i1 - 1) & (kRenormSteps - 1)) == kRenormSteps - 1) {
+          if (((i1 - 1 + gl) & (kRenormSteps - 1)) == kRenormSteps - 1) {
             T mnv = pv[p][0];
 #pragma unroll
             for (int r = 1; r < R; ++r) mnv = Ar::mn(mnv, pv[p][r]);
@@ -854,7 +858,7 @@ __device__ __forceinline__ void ring_steps(int nst, int& i1, const typename Ar::
         if (lK == gl && rK != 0) kill_cell<R>(pv, rK, INF);
       }
       if constexpr (kF32) {
-        if (((i1 - 1) & (kRenormSteps - 1)) == kRenormSteps - 1) {
+        if (((i1 - 1 + gl) & (kRenormSteps - 1)) == kRenormSteps - 1) {
           T mnv = pv[0];
 #pragma unroll
           for (int r = 1; r < R; ++r) mnv = Ar::mn(mnv, pv[r]);
@@ -1069,7 +1073,7 @@ __device__ __forceinline__ void unit_steps(int nst, int& i1, const typename Ar::
       if (lK == gl && rK != 0) kill_cell<R>(pv, rK, INF);
     }
     if constexpr (kF32) {
-      if (((i1 - 1) & (kRenormSteps - 1)) == kRenormSteps - 1) {
+      if (((i1 - 1 + gl * U) & (kRenormSteps - 1)) == kRenormSteps - 1) {
         T mnv = pv[0];
 #pragma unroll
         for (int r = 1; r < R; ++r) mnv = Ar::mn(mnv, pv[r]);
