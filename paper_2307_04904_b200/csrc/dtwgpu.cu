@@ -149,7 +149,7 @@ const Cand kBand[] = {{16, 7, 1500},    {16, 9, 1600},    {16, 11, 1700},  {16, 
 
 // fp32 mode: the cell is FADD FMUL FMNMX3 FADD, so the Full family runs ~2.15x the fp64
 // rate while the Band family (shuffle-heavy per step) gains only ~1.33x (measured, c2-c4).
-constexpr double kFp32Full = 2.15, kFp32Band = 1.33;
+constexpr double kFp32Full = 2.15, kFp32Band = 1.45;
 
 // Masked Full fills: rows where the strip lies entirely inside the band run the plain
 // cell; rows crossing a band edge run the masked cell at 1.79x the cost (least-squares fit
@@ -191,9 +191,9 @@ double full_cost(const Shape& s, const Cand& c, bool mask, bool fp32) {
 }
 
 double band_cost(const Shape& s, const Cand& c, bool fp32) {
-  // the smem-ring variants keep more of the fp32 gain (fewer registers; 1.39x / 1.46x
-  // measured on c2 for U = 1 / U = 3)
-  const double f32 = c.ring ? (c.U > 1 ? 1.46 : 1.39) : kFp32Band;
+  // fp32 / fp64 throughput ratios measured on c2 (G=8 R=26: 1.69 ring, 2.06 units;
+  // G=16 R=14: 1.52 ring, 1.72 units; register-rotation band 1.45)
+  const double f32 = c.ring ? (c.U > 1 ? 1.9 : 1.6) : kFp32Band;
   // wavefront fill/drain: one step per unit of the group
   return double(s.n + c.G * c.U - 1) * double(c.G * c.R) / (c.rate * (fp32 ? f32 : 1.0));
 }
