@@ -52,6 +52,17 @@ typedef struct dtwg_ctx dtwg_ctx;
 /* Context: owns device buffers, a stream, the resident series and matrix. */
 int dtwg_create(int device, dtwg_ctx** out);
 void dtwg_destroy(dtwg_ctx* ctx);
+/* One context driving several GPUs from one host thread (the C++ drop-in's default on a
+ * multi-GPU node; devices may repeat, e.g. {0, 0} in tests): dtwg_build_matrix gives each
+ * device a contiguous, cell-balanced slot range, fills the ranges concurrently and copies
+ * each straight into the caller's buffer; dtwg_adopt_condensed places the matrix on every
+ * device; dtwg_kmedoids runs contiguous blocks of restarts on the devices concurrently,
+ * replays observer calls in restart order and reduces the best restart in restart order
+ * with strict < (kmedoids.hpp:182). The other entry points act on the first device. */
+int dtwg_create_multi(const int* devices, int n_devices, dtwg_ctx** out);
+int dtwg_device_count(const dtwg_ctx* ctx);
+/* CUDA devices visible to this process (0 when none). */
+int dtwg_visible_devices(void);
 const char* dtwg_last_error(const dtwg_ctx* ctx);
 /* Pair reported by the last BandInfeasible error (pairwise.hpp:70-79), else -1,-1. */
 void dtwg_last_error_pair(const dtwg_ctx* ctx, int64_t* i, int64_t* j);

@@ -13,10 +13,13 @@
 // on the B200 through the C-ABI. Host-side types, data loading, the exact (MIP) solver
 // and the scores keep consuming the returned dtwclust::DistanceMatrix unchanged.
 //
-// Threading: one device context per host thread (thread_local), as the C-ABI requires.
+// Threading: one device context per host thread (thread_local), as the C-ABI requires;
+// it drives every visible GPU (or DTWGPU_DEVICES) -- see default_devices().
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <filesystem>
 #include <memory>
 #include <stdexcept>
@@ -47,11 +50,17 @@ class DeviceError : public std::runtime_error {
   int code_;
 };
 
-/// RAII owner of one dtwg_ctx on `device`.
+/// RAII owner of one dtwg_ctx on `device`, or on several devices (dtwg_create_multi).
 class Context {
  public:
   explicit Context(int device = 0) {
     const int rc = dtwg_create(device, &ctx_);
+    if (rc != DTWG_OK) throw DeviceError(rc, "no CUDA device available (there is no CPU fallback)");
+  }
+  explicit Context(const std::vector<int>& devices) {
+    const int rc = devices.empty()
+                       ? DTWG_NO_DEVICE
+                       : dtwg_create_multi(devices.data(), static_cast<int>(devices.size()), &ctx_);
     if (rc != DTWG_OK) throw DeviceError(rc, "no CUDA device available (there is no CPU fallback)");
   }
   ~Context() { dtwg_destroy(ctx_); }
@@ -63,9 +72,30 @@ class Context {
   dtwg_ctx* ctx_ = nullptr;
 };
 
+/// Devices the drop-in uses: DTWGPU_DEVICES ("0,1,2,3"; repeats allowed) or every
+/// visible GPU -- build_matrix splits the slots over them, kmedoids the restarts.
+inline std::vector<int> default_devices() {
+  std::vector<int> devs;
+  if (const char* env = std::getenv("DTWGPU_DEVICES")) {
+    std::string cur;
+    for (const char* c = env;; ++c) {
+      if (*c == ',' || *c == 0) {
+        if (!cur.empty()) devs.push_back(std::stoi(cur));
+        cur.clear();
+        if (*c == 0) break;
+      } else {
+        cur += *c;
+      }
+    }
+  }
+  if (devs.empty())
+    for (int d = 0; d < std::max(1, dtwg_visible_devices()); ++d) devs.push_back(d);
+  return devs;
+}
+
 inline Context& thread_context() {
   thread_local std::unique_ptr<Context> ctx;
-  if (!ctx) ctx = std::make_unique<Context>(0);
+  if (!ctx) ctx = std::make_unique<Context>(default_devices());
   return *ctx;
 }
 

@@ -29,6 +29,7 @@ EXPORTS = [
     "dtwg_count_cells", "dtwg_last_fill_ms", "dtwg_launch_count", "dtwg_last_plan",
     "dtwg_adopt_condensed", "dtwg_download_condensed", "dtwg_kmedoids", "dtwg_km_nearest_update",
     "dtwg_km_assign", "dtwg_km_update", "dtwg_force_kernel", "dtwg_measure_cell_peak", "dtwg_km_stats", "dtwg_silhouette",
+    "dtwg_create_multi", "dtwg_device_count", "dtwg_visible_devices",
     "dtwg_exchange_export", "dtwg_exchange_open", "dtwg_exchange_fill", "dtwg_exchange_complete",
     "dtwg_exchange_close",
     # host-side data path (csrc/host_io.cpp)
@@ -37,7 +38,8 @@ EXPORTS = [
     "dtwg_ingest_csv", "dtwg_dataset_size", "dtwg_dataset_samples", "dtwg_dataset_offsets",
     "dtwg_dataset_id", "dtwg_dataset_free", "dtwg_z_normalize",
 ]
-_HOST_INT = ("dtwg_exchange_export", "dtwg_exchange_open", "dtwg_exchange_fill",
+_HOST_INT = ("dtwg_create_multi", "dtwg_device_count", "dtwg_visible_devices",
+             "dtwg_exchange_export", "dtwg_exchange_open", "dtwg_exchange_fill",
              "dtwg_exchange_complete", "dtwg_exchange_close", "dtwg_save_matrix_text", "dtwg_load_matrix_text", "dtwg_save_matrix_binary",
              "dtwg_load_matrix_binary", "dtwg_ingest_csv", "dtwg_z_normalize")
 
@@ -90,6 +92,9 @@ def lib() -> C.CDLL:
     L.dtwg_measure_cell_peak.argtypes = [_vp, C.c_int, P(C.c_double)]
     L.dtwg_km_stats.argtypes = [_vp, _dp, C.c_int]
     L.dtwg_silhouette.argtypes = [_vp, _ip, _i64, _ip, _i64, _dp, P(C.c_double)]
+    L.dtwg_create_multi.argtypes = [P(C.c_int), C.c_int, P(_vp)]
+    L.dtwg_device_count.argtypes = [_vp]
+    L.dtwg_visible_devices.argtypes = []
     L.dtwg_exchange_export.argtypes = [_vp, _i64, C.c_char_p]
     L.dtwg_exchange_open.argtypes = [_vp, C.c_char_p, C.c_int, C.c_int]
     L.dtwg_exchange_fill.argtypes = [_vp, _i64, C.c_int, C.c_int, _i64, _i64]

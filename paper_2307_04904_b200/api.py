@@ -104,10 +104,17 @@ _BY_CODE = {2: InvalidArgumentsError, 7: EmptyDatasetError, 10: KOutOfRangeError
 class Engine:
     """One dtwg_ctx (device buffers, stream, resident series and matrix) on one GPU."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, devices: Optional[Sequence[int]] = None):
+        """devices: drive several GPUs from this one context (dtwg_create_multi): builds
+        split the slots over them, k-medoids splits the restarts; results are identical."""
         self.L = _native.lib()
         h = C.c_void_p()
-        rc = self.L.dtwg_create(device, C.byref(h))
+        if devices:
+            arr = (C.c_int * len(devices))(*devices)
+            rc = self.L.dtwg_create_multi(arr, len(devices), C.byref(h))
+            device = int(devices[0])
+        else:
+            rc = self.L.dtwg_create(device, C.byref(h))
         if rc != 0:
             raise DeviceError(f"dtwg_create(device={device}) failed with code {rc}: no CUDA "
                               "device visible (there is no CPU fallback)")

@@ -302,6 +302,9 @@ struct dtwg_ctx {
   DevBuf<int> d_prog;
   DevBuf<unsigned long long> d_work;
   DevBuf<double> d_cols;
+  // multi-device context (dtwg_create_multi): one child context per further device;
+  // this context drives the first
+  std::vector<dtwg_ctx*> devs;
   // fused fill + all-gather over peer memory (dtwg_exchange_*): other ranks' resident
   // matrices opened through CUDA IPC
   std::vector<double*> peers;
@@ -879,12 +882,15 @@ int ensure_resident(dtwg_ctx* ctx, int64_t p) {
   return DTWG_OK;
 }
 
-int validate_resident(dtwg_ctx* ctx) {
+// distance_matrix.hpp:34-38 over slots [sb, se) of the resident matrix (se < 0: all).
+int validate_resident(dtwg_ctx* ctx, int64_t sb = 0, int64_t se = -1) {
   const int64_t total = ctx->mat_p * (ctx->mat_p - 1) / 2;
-  if (total == 0) return DTWG_OK;
+  if (se < 0) se = total;
+  if (se <= sb) return DTWG_OK;
   CU(ctx->d_flag.reserve(1), "cudaMalloc flag");
   CU(cudaMemsetAsync(ctx->d_flag.ptr, 0, sizeof(int), ctx->stream), "memset");
-  CU(dtwgpu::launch_validate_condensed(ctx->d_cond.ptr, total, ctx->d_flag.ptr, ctx->stream),
+  CU(dtwgpu::launch_validate_condensed(ctx->d_cond.ptr + sb, se - sb, ctx->d_flag.ptr,
+                                       ctx->stream),
      "validate");
   ctx->launches++;
   int bad = 0;
@@ -895,7 +901,7 @@ int validate_resident(dtwg_ctx* ctx) {
     ctx->cond_valid = false;
     return ctx->fail(DTWG_DISTANCE_MATRIX_INVALID, "entries must be finite and non-negative");
   }
-  ctx->cond_valid = true;
+  ctx->cond_valid = sb == 0 && se == total;
   return DTWG_OK;
 }
 
@@ -1159,8 +1165,40 @@ int dtwg_create(int device, dtwg_ctx** out) {
   return DTWG_OK;
 }
 
+int dtwg_create_multi(const int* devices, int n_devices, dtwg_ctx** out) {
+  if (!out || !devices || n_devices < 1) return DTWG_INVALID_ARGUMENTS;
+  *out = nullptr;
+  dtwg_ctx* ctx = nullptr;
+  int rc = dtwg_create(devices[0], &ctx);
+  if (rc) return rc;
+  for (int d = 1; d < n_devices; ++d) {
+    dtwg_ctx* c = nullptr;
+    rc = dtwg_create(devices[d], &c);
+    if (rc) {
+      dtwg_destroy(ctx);
+      return rc;
+    }
+    ctx->devs.push_back(c);
+  }
+  *out = ctx;
+  return DTWG_OK;
+}
+
+int dtwg_device_count(const dtwg_ctx* ctx) { return ctx ? 1 + (int)ctx->devs.size() : 0; }
+
+int dtwg_visible_devices(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 void dtwg_destroy(dtwg_ctx* ctx) {
   if (!ctx) return;
+  for (dtwg_ctx* c : ctx->devs) dtwg_destroy(c);
+  ctx->devs.clear();
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   ctx->d_samples.release();
@@ -1464,9 +1502,12 @@ void parallel_copy(double* dst, const double* src, int64_t n) {
 }
 }  // namespace
 
+// Slots [sb, se) of the matrix (all when se < 0) into out[sb, se).
 static int build_streamed(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, double* out,
-                          bool chunk_fill) {
-  const int64_t total = ctx->p * (ctx->p - 1) / 2;
+                          bool chunk_fill, int64_t sb = 0, int64_t se = -1) {
+  const int64_t all = ctx->p * (ctx->p - 1) / 2;
+  if (se < 0) se = all;
+  const int64_t total = se - sb;  // slots of this range
   const int64_t chunk = std::max<int64_t>(1, env_or("DTWGPU_STREAM_CHUNK", kStreamChunk));
   int rc = check_band(ctx, hw, auto_widen);
   if (rc) return rc;
@@ -1484,6 +1525,7 @@ static int build_streamed(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precisi
     ctx->stage_elems = chunk;
   }
   const int64_t nchunk = (total + chunk - 1) / chunk;
+  if (nchunk == 0) return DTWG_OK;
   std::vector<cudaEvent_t> filled(nchunk, nullptr), copied(nchunk, nullptr);
   auto cleanup = [&] {
     for (auto& e : filled) if (e) cudaEventDestroy(e);
@@ -1500,12 +1542,12 @@ static int build_streamed(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precisi
   cudaEventCreate(&t0);
   cudaEventRecord(t0, ctx->stream);
   if (!chunk_fill) {  // one fill (its plan stays cached); the D2H is still staged
-    rc = run_fill(ctx, hw, auto_widen, precision, 0, total, ctx->d_cond.ptr, 0, false);
+    rc = run_fill(ctx, hw, auto_widen, precision, sb, se, ctx->d_cond.ptr, 0, false);
     if (rc) return fail(rc);
   }
   for (int64_t c = 0; c < nchunk; ++c) {
     if (chunk_fill) {
-      const int64_t b = c * chunk, e = std::min(total, b + chunk);
+      const int64_t b = sb + c * chunk, e = std::min(se, b + chunk);
       rc = run_fill(ctx, hw, auto_widen, precision, b, e, ctx->d_cond.ptr, 0, false);
       if (rc) return fail(rc);
     }
@@ -1514,7 +1556,7 @@ static int build_streamed(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precisi
   }
   cudaEventRecord(ctx->ev1, ctx->stream);
   auto enqueue_copy = [&](int64_t c) -> int {
-    const int64_t b = c * chunk, e = std::min(total, b + chunk);
+    const int64_t b = sb + c * chunk, e = std::min(se, b + chunk);
     if (cudaStreamWaitEvent(ctx->copy_stream, filled[c], 0) != cudaSuccess ||
         cudaMemcpyAsync(ctx->h_stage[c & 1], ctx->d_cond.ptr + b, (e - b) * sizeof(double),
                         cudaMemcpyDeviceToHost, ctx->copy_stream) != cudaSuccess ||
@@ -1529,7 +1571,7 @@ static int build_streamed(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precisi
   for (int64_t c = 0; c < nchunk; ++c) {
     const cudaError_t err = cudaEventSynchronize(copied[c]);
     if (err != cudaSuccess) return fail(ctx->cuda_fail(err, "D2H chunk sync"));
-    const int64_t b = c * chunk, e = std::min(total, b + chunk);
+    const int64_t b = sb + c * chunk, e = std::min(se, b + chunk);
     parallel_copy(out + b, ctx->h_stage[c & 1], e - b);
     if (c + 2 < nchunk) {
       rc = enqueue_copy(c + 2);
@@ -1539,9 +1581,69 @@ static int build_streamed(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precisi
   if (cudaEventElapsedTime(&fill_ms, t0, ctx->ev1) == cudaSuccess) ctx->last_fill_ms = fill_ms;
   cudaEventDestroy(t0);
   cleanup();
-  ctx->cond_valid = true;
-  return validate_resident(ctx);  // distance_matrix.hpp:34-38
+  return validate_resident(ctx, sb, se);  // distance_matrix.hpp:34-38
 }
+
+// ---- one context, several devices ---------------------------------------------------
+extern "C++" {
+// Cell-balanced contiguous slot ranges, one per device (equal pairs for same-length
+// series), like the per-rank shards of the multi-process path.
+std::vector<int64_t> device_bounds(dtwg_ctx* ctx, int64_t hw, int auto_widen, int nd) {
+  const int64_t p = ctx->p, total = p * (p - 1) / 2;
+  std::vector<int64_t> bnd(nd + 1, total);
+  bnd[0] = 0;
+  if (ctx->uniform) {
+    for (int d = 1; d < nd; ++d) bnd[d] = total * d / nd;
+    return bnd;
+  }
+  double all = 0;
+  for (int64_t i = 0; i + 1 < p; ++i)
+    for (int64_t j = i + 1; j < p; ++j) {
+      const Shape sh = shape_of(ctx, i, j, hw, auto_widen);
+      all += (double)pair_cells(sh.n, sh.m, sh.hw);
+    }
+  double acc = 0;
+  int d = 1;
+  int64_t slot = 0;
+  for (int64_t i = 0; i + 1 < p && d < nd; ++i)
+    for (int64_t j = i + 1; j < p && d < nd; ++j, ++slot) {
+      const Shape sh = shape_of(ctx, i, j, hw, auto_widen);
+      acc += (double)pair_cells(sh.n, sh.m, sh.hw);
+      while (d < nd && acc >= all * d / nd) bnd[d++] = slot + 1;
+    }
+  for (int k = 1; k <= nd; ++k) bnd[k] = std::max(bnd[k], bnd[k - 1]);
+  return bnd;
+}
+
+// Runs f(ctx_d, d) for every device of the context on its own host thread; returns the
+// first error in device order (its message copied to the parent).
+template <class F>
+int for_each_device(dtwg_ctx* ctx, F&& f) {
+  const int nd = 1 + (int)ctx->devs.size();
+  std::vector<int> rcs(nd, DTWG_OK);
+  std::vector<std::thread> th;
+  for (int d = 0; d < nd; ++d) {
+    dtwg_ctx* c = d == 0 ? ctx : ctx->devs[d - 1];
+    th.emplace_back([&, c, d] {
+      cudaSetDevice(c->device);
+      rcs[d] = f(c, d);
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int d = 0; d < nd; ++d) {
+    if (rcs[d] != DTWG_OK) {
+      dtwg_ctx* c = d == 0 ? ctx : ctx->devs[d - 1];
+      if (c != ctx) {
+        ctx->last_error = c->last_error;
+        ctx->err_i = c->err_i;
+        ctx->err_j = c->err_j;
+      }
+      return rcs[d];
+    }
+  }
+  return DTWG_OK;
+}
+}  // extern "C++"
 
 int dtwg_build_matrix(dtwg_ctx* ctx, const double* samples, const int64_t* offsets, int64_t p,
                       int64_t half_width, int auto_widen, unsigned workers, int precision,
@@ -1556,6 +1658,25 @@ int dtwg_build_matrix(dtwg_ctx* ctx, const double* samples, const int64_t* offse
   if (rc) return rc;
   const int64_t total = p * (p - 1) / 2;
   const int64_t out_bytes = total * (int64_t)sizeof(double);
+  if (!ctx->devs.empty() && out_condensed && total > 0) {
+    // every device fills its slot range and copies it straight into the caller's buffer
+    rc = check_band(ctx, half_width, auto_widen);  // first infeasible pair, row-major
+    if (rc) return rc;
+    const std::vector<int64_t> bnd =
+        device_bounds(ctx, half_width, auto_widen, 1 + (int)ctx->devs.size());
+    rc = for_each_device(ctx, [&](dtwg_ctx* c, int d) -> int {
+      if (c != ctx) {
+        const int r = dtwg_upload_series(c, samples, offsets, p);
+        if (r) return r;
+      }
+      return build_streamed(c, half_width, auto_widen, precision, out_condensed,
+                            c->uniform && (bnd[d + 1] - bnd[d]) * 8 >= kChunkFillMinBytes,
+                            bnd[d], bnd[d + 1]);
+    });
+    if (rc) return rc;
+    if (evaluations) *evaluations = (uint64_t)total;
+    return DTWG_OK;
+  }
   if (out_condensed && total > 0 &&
       out_bytes >= env_or("DTWGPU_STREAM_MIN_BYTES", kStreamMinBytes)) {
     const bool chunk_fill =
@@ -1653,8 +1774,7 @@ int dtwg_exchange_complete(dtwg_ctx* ctx) {
   return validate_resident(ctx);  // distance_matrix.hpp:34-38
 }
 
-int dtwg_adopt_condensed(dtwg_ctx* ctx, const double* condensed, int64_t p, int on_device) {
-  if (!ctx) return DTWG_INVALID_ARGUMENTS;
+static int adopt_one(dtwg_ctx* ctx, const double* condensed, int64_t p, int on_device) {
   cudaSetDevice(ctx->device);
   if (p <= 0) return ctx->fail(DTWG_DISTANCE_MATRIX_INVALID, "matrix needs at least one series");
   int rc = ensure_resident(ctx, p);
@@ -1670,6 +1790,13 @@ int dtwg_adopt_condensed(dtwg_ctx* ctx, const double* condensed, int64_t p, int 
   return validate_resident(ctx);
 }
 
+int dtwg_adopt_condensed(dtwg_ctx* ctx, const double* condensed, int64_t p, int on_device) {
+  if (!ctx) return DTWG_INVALID_ARGUMENTS;
+  if (ctx->devs.empty()) return adopt_one(ctx, condensed, p, on_device);
+  // every device of the context gets the matrix (device pointers may live on any device)
+  return for_each_device(ctx, [&](dtwg_ctx* c, int) { return adopt_one(c, condensed, p, on_device); });
+}
+
 int dtwg_download_condensed(dtwg_ctx* ctx, double* out) {
   if (!ctx || !out) return DTWG_INVALID_ARGUMENTS;
   if (!ctx->cond_valid) return ctx->fail(DTWG_INVALID_ARGUMENTS, "no resident distance matrix");
@@ -1682,11 +1809,81 @@ int dtwg_download_condensed(dtwg_ctx* ctx, double* out) {
   return DTWG_OK;
 }
 
+static int km_run(dtwg_ctx* ctx, int64_t k, int64_t restarts, int64_t max_iterations,
+                  uint64_t seed, int64_t restart_begin, int64_t restart_end,
+                  dtwg_observer_fn observer, void* user, int64_t* medoids_out,
+                  int64_t* assignment_out, double* cost_out, int64_t* best_restart_out);
+
+namespace {
+struct KmRecord {
+  int64_t r, it;
+  double cost;
+};
+void km_record(void* user, int64_t r, int64_t it, double cost) {
+  static_cast<std::vector<KmRecord>*>(user)->push_back({r, it, cost});
+}
+}  // namespace
+
 int dtwg_kmedoids(dtwg_ctx* ctx, int64_t k, int64_t restarts, int64_t max_iterations,
                   uint64_t seed, int64_t restart_begin, int64_t restart_end,
                   dtwg_observer_fn observer, void* user, int64_t* medoids_out,
                   int64_t* assignment_out, double* cost_out, int64_t* best_restart_out) {
   if (!ctx) return DTWG_INVALID_ARGUMENTS;
+  if (ctx->devs.empty() || !ctx->cond_valid)
+    return km_run(ctx, k, restarts, max_iterations, seed, restart_begin, restart_end, observer,
+                  user, medoids_out, assignment_out, cost_out, best_restart_out);
+  // Several devices: contiguous blocks of restarts per device, run concurrently over a
+  // copy of the matrix on each device; observer calls are replayed in restart order and
+  // the best restart is reduced in restart order with strict < (kmedoids.hpp:182).
+  if (restart_end > restarts) restart_end = restarts;
+  const int nd = 1 + (int)ctx->devs.size();
+  const int64_t p = ctx->mat_p;
+  if (k < 1 || k > p || restart_begin < 0 || restart_begin >= restart_end)
+    return km_run(ctx, k, restarts, max_iterations, seed, restart_begin, restart_end, observer,
+                  user, medoids_out, assignment_out, cost_out, best_restart_out);  // errors
+  struct Part {
+    std::vector<int64_t> med, asg;
+    double cost = 0;
+    int64_t best_r = -1;
+    std::vector<KmRecord> recs;
+  };
+  std::vector<Part> parts(nd);
+  const int64_t nr = restart_end - restart_begin;
+  int rc = for_each_device(ctx, [&](dtwg_ctx* c, int d) -> int {
+    const int64_t rb = restart_begin + nr * d / nd, re = restart_begin + nr * (d + 1) / nd;
+    if (re <= rb) return DTWG_OK;
+    if (c != ctx) {
+      const int r = adopt_one(c, ctx->d_cond.ptr, p, 1);
+      if (r) return r;
+    }
+    Part& P = parts[d];
+    P.med.resize(k);
+    P.asg.resize(p);
+    return km_run(c, k, restarts, max_iterations, seed, rb, re, observer ? km_record : nullptr,
+                  &P.recs, P.med.data(), P.asg.data(), &P.cost, &P.best_r);
+  });
+  if (rc) return rc;
+  bool have = false;
+  double best = 0.0;
+  for (const Part& P : parts) {
+    for (const KmRecord& r : P.recs) observer(user, r.r, r.it, r.cost);
+    if (P.best_r < 0) continue;
+    if (!have || P.cost < best) {
+      have = true;
+      best = P.cost;
+      if (cost_out) *cost_out = P.cost;
+      if (medoids_out) std::copy(P.med.begin(), P.med.end(), medoids_out);
+      if (assignment_out) std::copy(P.asg.begin(), P.asg.end(), assignment_out);
+      if (best_restart_out) *best_restart_out = P.best_r;
+    }
+  }
+  return DTWG_OK;
+}
+
+static int km_run(dtwg_ctx* ctx, int64_t k, int64_t restarts, int64_t max_iterations,
+                  uint64_t seed, int64_t restart_begin, int64_t restart_end,
+                  dtwg_observer_fn observer, void* user, int64_t* medoids_out,
+                  int64_t* assignment_out, double* cost_out, int64_t* best_restart_out) {
   cudaSetDevice(ctx->device);
   if (!ctx->cond_valid) return ctx->fail(DTWG_INVALID_ARGUMENTS, "no resident distance matrix");
   const int64_t p = ctx->mat_p;

@@ -202,3 +202,29 @@ def test_condensed_view_matches_square(monkeypatch, cfgno, q):
     assert sa.silhouette == sb.silhouette and sa.mean_silhouette == sb.mean_silhouette
     med, asg, cost = kref(m.condensed(), ds.p, cfg)
     assert b.medoids == list(med) and b.assignment == list(asg) and b.total_cost == cost
+
+
+@pytest.mark.parametrize("cfgno,q", [(2, 120), (5, 200)])
+def test_multi_device_context_matches_single(cfgno, q):
+    """One context over two device contexts (dtwg_create_multi, both on the one B200 here):
+    the slot ranges and restart blocks are split between them; matrix, clustering,
+    observer trace and silhouettes must equal the single-device results."""
+    ds = gen.make_config(cfgno).subset(q)
+    single = api.Engine(0)
+    multi = api.Engine(devices=[0, 0])
+    a = single.build_condensed(ds.samples, ds.offsets, ds.half_width, ds.auto_widen)
+    b = multi.build_condensed(ds.samples, ds.offsets, ds.half_width, ds.auto_widen)
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    for eng in (single, multi):
+        eng.adopt(a, ds.p)
+    res = []
+    for eng in (single, multi):
+        trace = []
+        med, asg, cost, br = eng.kmedoids(ds.p, ds.k, 6, 100, 3, 0, 6,
+                                          lambda r, it, c: trace.append((r, it, c)))
+        res.append((list(med), list(asg), cost, br, trace))
+    assert res[0] == res[1]
+    med, asg, cost = kref(a, ds.p, KMedoidsConfig(k=ds.k, restarts=6, seed=3))
+    assert res[1][0] == list(med) and res[1][1] == list(asg) and res[1][2] == cost
+    multi.close()
+    single.close()
