@@ -55,6 +55,11 @@ constexpr unsigned kFull = 0xffffffffu;
 // renormalisation run every step: ~1.5 extra instructions per cell).
 constexpr int kRenormSteps = 8;
 
+#ifndef DTWG_UNIT_UNROLL  // steps unrolled per loop iteration in the unit-ring kernel
+#define DTWG_UNIT_UNROLL 2
+#endif
+constexpr int kUnitUnroll = DTWG_UNIT_UNROLL;
+
 __device__ __forceinline__ int64_t row_off(int64_t i, int64_t p) { return i * p - i * (i + 1) / 2; }
 
 // Condensed slot -> (i, j), i < j (pairwise.hpp:41-53), closed form + fix-up.
@@ -1010,7 +1015,7 @@ __device__ __forceinline__ void unit_steps(int nst, int& i1, const typename Ar::
   constexpr bool kF32 = sizeof(T) == 4;
   const T INF = Ar::inf();
   const bool last = gl == G - 1;
-#pragma unroll 2
+#pragma unroll kUnitUnroll
   for (int q = 0; q < nst; ++q) {
     bool act[U];
 #pragma unroll
@@ -1094,7 +1099,10 @@ __device__ __forceinline__ void unit_steps(int nst, int& i1, const typename Ar::
 // Resident CTAs the register allocation is capped for (ILP U needs fewer warps; wide R
 // keeps 4 CTAs without spills, narrower ones fit 5).
 #ifndef DTWG_UNIT_MINB
-#define DTWG_UNIT_MINB(R) ((R) >= 40 ? 3 : ((R) >= 20 ? 4 : 5))
+#define DTWG_UNIT_MINB(R) ((R) >= 40 ? 3 : ((R) >= 20 ? DTWG_UNIT_MINB20 : 5))
+#endif
+#ifndef DTWG_UNIT_MINB20
+#define DTWG_UNIT_MINB20 4
 #endif
 template <int G, int R, int U, int KR, class Ar>
 __global__ void __launch_bounds__(kThreads, DTWG_UNIT_MINB(R)) dtw_bandunit_kernel(const FillArgs A) {
