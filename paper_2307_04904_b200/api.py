@@ -311,12 +311,15 @@ class Engine:
 _ENGINES: dict = {}
 
 
-def engine(device: int = 0) -> Engine:
-    """Process-wide engine per device."""
-    e = _ENGINES.get(device)
+def engine(device: int = 0, devices: Optional[Sequence[int]] = None) -> Engine:
+    """Process-wide engine per device, or per device list (one context over several GPUs:
+    builds split the slots, k-medoids the restarts -- dtwg_create_multi)."""
+    key = tuple(int(d) for d in devices) if devices else device
+    e = _ENGINES.get(key)
     if e is None or e.h is None:
-        e = Engine(device)
-        _ENGINES[device] = e
+        e = Engine(device, devices=list(key) if devices else None)
+        e.multi = bool(devices) and len(key) > 1
+        _ENGINES[key] = e
     return e
 
 
@@ -477,7 +480,8 @@ def _pack(dataset: Sequence[TimeSeries]):
 
 def build_matrix(dataset: Sequence[TimeSeries], w: WarpWindow, workers: int,
                  stats: Optional[BuildStats] = None, auto_widen: bool = False, *,
-                 precision: int = FP64, device: int = 0) -> DistanceMatrix:
+                 precision: int = FP64, device: int = 0,
+                 devices: Optional[Sequence[int]] = None) -> DistanceMatrix:
     """pairwise.hpp:62-127 on the GPU. `workers` is validated (>= 1) as the reference does.
 
     Validation order follows the reference: EmptyDataset, InvalidArguments (workers),
@@ -489,34 +493,35 @@ def build_matrix(dataset: Sequence[TimeSeries], w: WarpWindow, workers: int,
         raise InvalidArgumentsError("workers must be >= 1")
     validate_dataset(dataset)
     samples, offsets = _pack(dataset)
-    eng = engine(device)
+    eng = engine(device, devices)
     cond = eng.build_condensed(samples, offsets, w.native, auto_widen, max(int(workers), 1),
                                precision)
     if stats is not None:
         stats.evaluations = eng._last_evaluations
-    m = DistanceMatrix(len(dataset))
+    return _wrap(cond, len(dataset), eng)
+
+
+def _wrap(cond: np.ndarray, p: int, eng: Engine) -> DistanceMatrix:
+    m = DistanceMatrix(p)
     m._values = cond
     m._engine = eng
-    eng._resident_matrix = m
-    eng._p_resident = len(dataset)
+    if not getattr(eng, "multi", False):  # a multi-device build leaves only slices resident
+        eng._resident_matrix = m
+        eng._p_resident = p
     return m
 
 
 def build_matrix_packed(samples: np.ndarray, offsets: np.ndarray, w: WarpWindow,
                         auto_widen: bool = False, *, precision: int = FP64,
-                        device: int = 0) -> DistanceMatrix:
+                        device: int = 0, devices: Optional[Sequence[int]] = None
+                        ) -> DistanceMatrix:
     """build_matrix over an already-packed CSR dataset (ids implicit and unique)."""
-    eng = engine(device)
+    eng = engine(device, devices)
     p = len(offsets) - 1
     if p <= 0:
         raise EmptyDatasetError()
     cond = eng.build_condensed(samples, offsets, w.native, auto_widen, 1, precision)
-    m = DistanceMatrix(p)
-    m._values = cond
-    m._engine = eng
-    eng._resident_matrix = m
-    eng._p_resident = p
-    return m
+    return _wrap(cond, p, eng)
 
 
 # ----------------------------------------------------------------------------- k-medoids
@@ -546,8 +551,9 @@ class ClusterResult:
 IterationObserver = Callable[[int, int, float], None]
 
 
-def _resident(source: DistanceMatrix, device: int = 0) -> Engine:
-    eng = source._engine or engine(device)
+def _resident(source: DistanceMatrix, device: int = 0,
+              devices: Optional[Sequence[int]] = None) -> Engine:
+    eng = engine(device, devices) if devices else (source._engine or engine(device))
     if getattr(eng, "_resident_matrix", None) is not source:
         eng.adopt(source.condensed(), source.size())
         eng._resident_matrix = source
@@ -558,6 +564,7 @@ def _resident(source: DistanceMatrix, device: int = 0) -> Engine:
 
 def kmedoids(source: DistanceMatrix, config: KMedoidsConfig,
              observer: Optional[IterationObserver] = None, *, device: int = 0,
+             devices: Optional[Sequence[int]] = None,
              restart_range: Optional[tuple] = None) -> ClusterResult:
     """kmedoids.hpp:148-189 with the distance sweeps on the GPU."""
     p = source.size()
@@ -567,7 +574,7 @@ def kmedoids(source: DistanceMatrix, config: KMedoidsConfig,
         raise InvalidArgumentsError("restarts must be >= 1")
     if config.max_iterations < 1:
         raise InvalidArgumentsError("max_iterations must be >= 1")
-    eng = _resident(source, device)
+    eng = _resident(source, device, devices)
     rb, re = restart_range if restart_range else (0, config.restarts)
     med, asg, cost, best_r = eng.kmedoids(p, config.k, config.restarts, config.max_iterations,
                                           config.seed, rb, re, observer)

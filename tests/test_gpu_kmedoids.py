@@ -228,3 +228,18 @@ def test_multi_device_context_matches_single(cfgno, q):
     assert res[1][0] == list(med) and res[1][1] == list(asg) and res[1][2] == cost
     multi.close()
     single.close()
+
+
+def test_python_api_devices_option():
+    """api.build_matrix / kmedoids with devices=[0, 0]: the same matrix and clustering."""
+    ds = gen.make_config(1).subset(60)
+    data = [TimeSeries(f"s{i}", ds.series(i)) for i in range(ds.p)]
+    a = build_matrix(data, WarpWindow.unlimited(), 1)
+    b = build_matrix(data, WarpWindow.unlimited(), 1, devices=[0, 0])
+    assert np.array_equal(a.condensed().view(np.uint64), b.condensed().view(np.uint64))
+    cfg = KMedoidsConfig(k=4, restarts=5, seed=2)
+    ta, tb = [], []
+    ra = kmedoids(a, cfg, lambda r, i, c: ta.append((r, i, c)))
+    rb = kmedoids(b, cfg, lambda r, i, c: tb.append((r, i, c)), devices=[0, 0])
+    assert (ra.medoids, ra.assignment, ra.total_cost) == (rb.medoids, rb.assignment, rb.total_cost)
+    assert ta == tb
