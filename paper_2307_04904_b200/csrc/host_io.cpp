@@ -72,6 +72,17 @@ bool read_file(const char* path, std::string& out) {
   std::FILE* f = std::fopen(path, "rb");
   if (!f) return false;
   out.clear();
+  // one read into a buffer sized from the file (streams fall back to chunked reads)
+  if (std::fseek(f, 0, SEEK_END) == 0) {
+    const long size = std::ftell(f);
+    if (size > 0 && std::fseek(f, 0, SEEK_SET) == 0) {
+      out.resize((size_t)size);
+      const size_t got = std::fread(&out[0], 1, (size_t)size, f);
+      out.resize(got);
+    } else {
+      std::fseek(f, 0, SEEK_SET);
+    }
+  }
   char buf[1 << 16];
   size_t got;
   while ((got = std::fread(buf, 1, sizeof(buf), f)) > 0) out.append(buf, got);
@@ -208,7 +219,10 @@ int dtwg_load_matrix_text(const char* path, int threads, int64_t* p_out, double*
   const int64_t rows_avail = std::min<int64_t>(p, nlines - 1);
   const int64_t total = p * (p - 1) / 2;
   double* cond = (double*)std::malloc((size_t)std::max<int64_t>(total, 1) * sizeof(double));
-  std::vector<double> lower((size_t)std::max<int64_t>(total, 1));  // (i, j<i) as written in row i
+  // (i, j < i) as written in row i, row-major (row i at i(i-1)/2): sequential writes while
+  // parsing, compared against the upper triangle afterwards
+  std::vector<double> lower((size_t)std::max<int64_t>(total, 1));
+  auto loff = [](int64_t i) { return i * (i - 1) / 2; };
   if (!cond) return io_fail(3, "out of host memory");
   auto off = [p](int64_t i) { return i * p - i * (i + 1) / 2; };
   const int nt = thread_count(threads, rows_avail);
@@ -254,7 +268,7 @@ int dtwg_load_matrix_text(const char* path, int threads, int64_t* p_out, double*
             break;
           }
           if (j > i) cond[off(i) + (j - i - 1)] = v;
-          else lower[(size_t)(off(j) + (i - j - 1))] = v;
+          else lower[(size_t)(loff(i) + j)] = v;
         }
       }
       if (!err.empty()) {
@@ -281,7 +295,7 @@ int dtwg_load_matrix_text(const char* path, int threads, int64_t* p_out, double*
     for (int64_t i = b; i < e; ++i) {
       for (int64_t j = 0; j < i; ++j) {
         if (i == bad_row) break;  // handled below (needs the column of the row-local error)
-        if (lower[(size_t)(off(j) + (i - j - 1))] != cond[off(j) + (i - j - 1)]) {
+        if (lower[(size_t)(loff(i) + j)] != cond[off(j) + (i - j - 1)]) {
           serrs[t] = Err{i + 2, 9,
                          "matrix is not symmetric at (" + std::to_string(i) + ", " +
                              std::to_string(j) + ")",

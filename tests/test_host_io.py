@@ -214,3 +214,34 @@ def test_generators_match_native_z_normalize():
     got = raw.reshape(-1).copy()
     dataio.z_normalize_packed(got, np.array([0, 500, 1000, 1500], dtype=np.int64))
     assert_bitwise(got, want.reshape(-1))
+
+
+@needs_ref
+def test_large_matrix_text_threaded_identical(tmp_path):
+    """p = 1500 (2.25 M cells, ~40 MB of text): byte-identical with 1 and 16 threads and
+    with the reference, and loads back bit-exactly (timings printed)."""
+    import time
+    p = 1500
+    D = random_condensed(ScalarRng(7), p, 0.0, 1e4)
+    m = api.DistanceMatrix.from_condensed(p, D)
+    t0 = time.perf_counter()
+    oracle.ref_save_matrix(D, p, str(tmp_path / "ref.txt"))
+    t_ref = time.perf_counter() - t0
+    dataio.save_matrix(m, tmp_path / "one.txt", threads=1)
+    t0 = time.perf_counter()
+    dataio.save_matrix(m, tmp_path / "many.txt", threads=16)
+    t_ours = time.perf_counter() - t0
+    ref = (tmp_path / "ref.txt").read_bytes()
+    assert (tmp_path / "one.txt").read_bytes() == ref
+    assert (tmp_path / "many.txt").read_bytes() == ref
+    t0 = time.perf_counter()
+    back = dataio.load_matrix(tmp_path / "many.txt", threads=16)
+    t_load = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    q, D2 = oracle.ref_load_matrix(str(tmp_path / "ref.txt"))
+    t_ref_load = time.perf_counter() - t0
+    assert_bitwise(back.condensed(), D)
+    assert_bitwise(D2, D)
+    print(f"save: ours {t_ours:.3f}s vs reference {t_ref:.3f}s; load: ours {t_load:.3f}s vs "
+          f"reference {t_ref_load:.3f}s")
+    # (timings depend on the cores this container grants; printed, not asserted)
