@@ -428,3 +428,25 @@ def test_full_size_properties(eng, cfg):
         y = ds.series(int(j[t]))
         hw = int(gen.effective_half_width(lens[i[t]], lens[j[t]], ds.half_width, ds.auto_widen))
         assert A[sa[t]] == oracle.dtw(x, y, hw), (cfg, int(i[t]), int(j[t]))
+
+
+def test_multi_device_context_edge_cases():
+    """One context over three device contexts (all on the one B200 here): tiny matrices
+    (empty device ranges), ragged auto-widened pairs, and the first band-infeasible pair
+    reported exactly as by a single device."""
+    multi = api.Engine(devices=[0, 0, 0])
+    single = api.Engine(0)
+    try:
+        for rows in ([[1.0, 2.0], [2.0, 3.0]], [[1.0], [2.0, 3.0], [4.0, 5.0, 6.0]]):
+            s, o = pack(rows)
+            assert_bitwise(multi.build_condensed(s, o), single.build_condensed(s, o))
+        ds = gen.config5().subset(90)
+        assert_bitwise(multi.build_condensed(ds.samples, ds.offsets, 40, True),
+                       single.build_condensed(ds.samples, ds.offsets, 40, True))
+        s, o = pack([[1, 2], [1, 2, 3], [1, 2, 3, 4, 5, 6]])
+        with pytest.raises(BandInfeasibleError) as ei:
+            multi.build_condensed(s, o, 1, False)
+        assert (ei.value.pair_i, ei.value.pair_j) == (0, 2)
+    finally:
+        multi.close()
+        single.close()
