@@ -326,6 +326,10 @@ struct dtwg_ctx {
   DevBuf<double> d_square;
   bool square_valid = false;  // the sweep view is ready (square expanded, or condensed mode)
   bool km_condensed = false;  // sweeps read the condensed matrix (square does not fit)
+  // k-medoids restart workers: contexts on the same device (own stream and sweep buffers)
+  // that read this context's matrix (km_src), so independent restarts run concurrently
+  std::vector<dtwg_ctx*> kmw;
+  const dtwg_ctx* km_src = nullptr;
   DevBuf<int> d_flag;
 
   // k-medoids sweep statistics (dtwg_km_stats): device time and algorithmic bytes of the
@@ -909,7 +913,11 @@ int validate_resident(dtwg_ctx* ctx, int64_t sb = 0, int64_t se = -1) {
 // condensed matrix -- p up to ~140 000 on a 180 GB B200 -- and the condensed matrix
 // itself beyond that (or with DTWGPU_KM_CONDENSED=1); both give identical results.
 const double* km_matrix(const dtwg_ctx* ctx) {
-  return ctx->km_condensed ? ctx->d_cond.ptr : ctx->d_square.ptr;
+  const dtwg_ctx* m = ctx->km_src ? ctx->km_src : ctx;
+  return m->km_condensed ? m->d_cond.ptr : m->d_square.ptr;
+}
+bool km_is_cond(const dtwg_ctx* ctx) {
+  return (ctx->km_src ? ctx->km_src : ctx)->km_condensed;
 }
 
 int ensure_square(dtwg_ctx* ctx) {
@@ -952,7 +960,7 @@ int km_assign(KmState& S, const std::vector<int64_t>& medoids) {
                      cudaMemcpyHostToDevice, ctx->stream),
      "H2D medoids");
   CU(cudaEventRecord(ctx->km0, ctx->stream), "event");
-  CU(dtwgpu::launch_assign(km_matrix(ctx), ctx->km_condensed, S.p, ctx->d_medoids.ptr,
+  CU(dtwgpu::launch_assign(km_matrix(ctx), km_is_cond(ctx), S.p, ctx->d_medoids.ptr,
                            (int64_t)medoids.size(),
                            ctx->d_assign.ptr, ctx->d_dist.ptr, ctx->stream),
      "assign");
@@ -1006,7 +1014,7 @@ int km_update(KmState& S, const std::vector<int64_t>& medoids, std::vector<int64
   CU(cudaMemcpyAsync(ctx->d_cb.ptr, cb.data(), (k + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
      "H2D cb");
   CU(cudaEventRecord(ctx->km0, ctx->stream), "event");
-  CU(dtwgpu::launch_update(km_matrix(ctx), ctx->km_condensed, p, ctx->d_members.ptr, ctx->d_cb.ptr, k,
+  CU(dtwgpu::launch_update(km_matrix(ctx), km_is_cond(ctx), p, ctx->d_members.ptr, ctx->d_cb.ptr, k,
                            ctx->d_best_member.ptr, ctx->d_best_sum.ptr, ctx->stream),
      "update");
   CU(cudaEventRecord(ctx->km1, ctx->stream), "event");
@@ -1079,7 +1087,7 @@ int km_seeds(KmState& S, int64_t k, SplitMix64& rng, std::vector<int64_t>& medoi
     CU(cudaMemcpyAsync(ctx->d_chosen.ptr + current, &chosen[current], 1, cudaMemcpyHostToDevice,
                        ctx->stream),
        "H2D chosen");
-    CU(dtwgpu::launch_nearest_update(km_matrix(ctx), ctx->km_condensed, p, current, ctx->d_chosen.ptr,
+    CU(dtwgpu::launch_nearest_update(km_matrix(ctx), km_is_cond(ctx), p, current, ctx->d_chosen.ptr,
                                      ctx->d_nearest.ptr, ctx->stream),
        "nearest");
     ctx->launches++;
@@ -1199,6 +1207,8 @@ void dtwg_destroy(dtwg_ctx* ctx) {
   if (!ctx) return;
   for (dtwg_ctx* c : ctx->devs) dtwg_destroy(c);
   ctx->devs.clear();
+  for (dtwg_ctx* c : ctx->kmw) dtwg_destroy(c);
+  ctx->kmw.clear();
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   ctx->d_samples.release();
@@ -1426,7 +1436,7 @@ int dtwg_silhouette(dtwg_ctx* ctx, const int64_t* medoids, int64_t k, const int6
      "H2D cb");
   CU(cudaMemcpyAsync(ctx->d_sil_cls.ptr, cls.data(), p * 4, cudaMemcpyHostToDevice, ctx->stream),
      "H2D cls");
-  CU(dtwgpu::launch_silhouette(km_matrix(ctx), ctx->km_condensed, p, ctx->d_members.ptr, ctx->d_cb.ptr,
+  CU(dtwgpu::launch_silhouette(km_matrix(ctx), km_is_cond(ctx), p, ctx->d_members.ptr, ctx->d_cb.ptr,
                                ctx->d_sil_cls.ptr, k, ctx->d_dist.ptr, ctx->stream),
      "silhouette");
   ctx->launches++;
@@ -1813,6 +1823,10 @@ static int km_run(dtwg_ctx* ctx, int64_t k, int64_t restarts, int64_t max_iterat
                   uint64_t seed, int64_t restart_begin, int64_t restart_end,
                   dtwg_observer_fn observer, void* user, int64_t* medoids_out,
                   int64_t* assignment_out, double* cost_out, int64_t* best_restart_out);
+static int km_loop(dtwg_ctx* ctx, int64_t p, int64_t k, int64_t max_iterations, uint64_t seed,
+                   int64_t restart_begin, int64_t restart_end, dtwg_observer_fn observer,
+                   void* user, int64_t* medoids_out, int64_t* assignment_out, double* cost_out,
+                   int64_t* best_restart_out);
 
 namespace {
 struct KmRecord {
@@ -1898,9 +1912,92 @@ static int km_run(dtwg_ctx* ctx, int64_t k, int64_t restarts, int64_t max_iterat
     return ctx->fail(DTWG_INVALID_ARGUMENTS, "empty restart range");
   int rc = ensure_square(ctx);
   if (rc) return rc;
-  rc = km_reserve(ctx, p, k);
-  if (rc) return rc;
+  // Independent restarts run concurrently: contiguous restart blocks on restart workers
+  // (same device, own streams), observer calls replayed and the best restart reduced in
+  // restart order with strict < -- the sequential loop's result, bit for bit.
+  const int64_t nr = restart_end - restart_begin;
+  // (small matrices: a restart is a few tens of microseconds, less than a thread hand-off)
+  const int64_t cap = p >= 2048 ? 8 : 1;
+  const int nw = (int)std::min<int64_t>(nr, std::max<int64_t>(1, env_or("DTWGPU_KM_WORKERS", cap)));
+  if (nw <= 1)
+    return km_loop(ctx, p, k, max_iterations, seed, restart_begin, restart_end, observer, user,
+                   medoids_out, assignment_out, cost_out, best_restart_out);
+  while ((int)ctx->kmw.size() < nw - 1) {
+    dtwg_ctx* w = nullptr;
+    rc = dtwg_create(ctx->device, &w);
+    if (rc) return ctx->fail(rc, "cannot create a k-medoids worker context");
+    w->km_src = ctx;
+    ctx->kmw.push_back(w);
+  }
+  struct Part {
+    std::vector<int64_t> med, asg;
+    double cost = 0;
+    int64_t best_r = -1;
+    std::vector<KmRecord> recs;
+    int rc = DTWG_OK;
+  };
+  std::vector<Part> parts(nw);
+  std::vector<std::thread> th;
+  for (int w = 0; w < nw; ++w) {
+    dtwg_ctx* c = w == 0 ? ctx : ctx->kmw[w - 1];
+    th.emplace_back([&, c, w] {
+      cudaSetDevice(c->device);
+      Part& P = parts[w];
+      const int64_t rb = restart_begin + nr * w / nw, re = restart_begin + nr * (w + 1) / nw;
+      if (re <= rb) return;
+      P.med.resize(k);
+      P.asg.resize(p);
+      P.rc = km_loop(c, p, k, max_iterations, seed, rb, re, observer ? km_record : nullptr,
+                     &P.recs, P.med.data(), P.asg.data(), &P.cost, &P.best_r);
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int w = 0; w < nw; ++w) {
+    dtwg_ctx* c = w == 0 ? ctx : ctx->kmw[w - 1];
+    if (c != ctx) {  // fold the worker's sweep statistics into this context's
+      ctx->km_assign_ms += c->km_assign_ms;
+      ctx->km_assign_bytes += c->km_assign_bytes;
+      ctx->km_update_ms += c->km_update_ms;
+      ctx->km_update_bytes += c->km_update_bytes;
+      ctx->km_sweeps += c->km_sweeps;
+      ctx->launches += c->launches;
+      c->km_assign_ms = c->km_assign_bytes = c->km_update_ms = c->km_update_bytes = 0;
+      c->km_sweeps = 0;
+      c->launches = 0;
+    }
+  }
+  for (int w = 0; w < nw; ++w) {
+    if (parts[w].rc != DTWG_OK) {
+      dtwg_ctx* c = w == 0 ? ctx : ctx->kmw[w - 1];
+      if (c != ctx) ctx->last_error = c->last_error;
+      return parts[w].rc;
+    }
+  }
+  bool have = false;
+  double best = 0.0;
+  for (const Part& P : parts) {
+    for (const KmRecord& r : P.recs) observer(user, r.r, r.it, r.cost);
+    if (P.best_r < 0) continue;
+    if (!have || P.cost < best) {
+      have = true;
+      best = P.cost;
+      if (cost_out) *cost_out = P.cost;
+      if (medoids_out) std::copy(P.med.begin(), P.med.end(), medoids_out);
+      if (assignment_out) std::copy(P.asg.begin(), P.asg.end(), assignment_out);
+      if (best_restart_out) *best_restart_out = P.best_r;
+    }
+  }
+  return DTWG_OK;
+}
 
+// The reference's restart loop (kmedoids.hpp:158-187) over restarts [restart_begin,
+// restart_end) on one context's stream and sweep buffers.
+static int km_loop(dtwg_ctx* ctx, int64_t p, int64_t k, int64_t max_iterations, uint64_t seed,
+                   int64_t restart_begin, int64_t restart_end, dtwg_observer_fn observer,
+                   void* user, int64_t* medoids_out, int64_t* assignment_out, double* cost_out,
+                   int64_t* best_restart_out) {
+  int rc = km_reserve(ctx, p, k);
+  if (rc) return rc;
   KmState S{ctx, p, k, {}, {}};
   bool have_best = false;
   double best_cost = 0.0;
@@ -1954,7 +2051,7 @@ int dtwg_km_nearest_update(dtwg_ctx* ctx, int64_t current, const uint8_t* chosen
   CU(cudaMemcpyAsync(ctx->d_nearest.ptr, nearest_inout, p * 8, cudaMemcpyHostToDevice,
                      ctx->stream),
      "H2D");
-  CU(dtwgpu::launch_nearest_update(km_matrix(ctx), ctx->km_condensed, p, current, ctx->d_chosen.ptr,
+  CU(dtwgpu::launch_nearest_update(km_matrix(ctx), km_is_cond(ctx), p, current, ctx->d_chosen.ptr,
                                    ctx->d_nearest.ptr, ctx->stream),
      "nearest");
   ctx->launches++;

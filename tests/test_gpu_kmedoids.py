@@ -243,3 +243,19 @@ def test_python_api_devices_option():
     rb = kmedoids(b, cfg, lambda r, i, c: tb.append((r, i, c)), devices=[0, 0])
     assert (ra.medoids, ra.assignment, ra.total_cost) == (rb.medoids, rb.assignment, rb.total_cost)
     assert ta == tb
+
+
+@pytest.mark.parametrize("workers", ["1", "3", "8"])
+def test_restart_workers_identical(monkeypatch, workers):
+    """Restarts run concurrently on restart-worker streams (DTWGPU_KM_WORKERS); the result
+    and the observer trace equal the sequential loop's and the reference's."""
+    monkeypatch.setenv("DTWGPU_KM_WORKERS", workers)
+    D = random_condensed(ScalarRng(31), 400)
+    cfg = KMedoidsConfig(k=7, restarts=9, seed=5)
+    trace = []
+    got = kmedoids(DistanceMatrix.from_condensed(400, D), cfg,
+                   lambda r, it, c: trace.append((r, it, c)))
+    ref_trace = []
+    med, asg, cost = kref(D, 400, cfg, lambda r, it, c: ref_trace.append((r, it, c)))
+    assert got.medoids == list(med) and got.assignment == list(asg) and got.total_cost == cost
+    assert trace == ref_trace
