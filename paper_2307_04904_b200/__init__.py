@@ -10,6 +10,6 @@ from .api import (  # noqa: F401
     DistanceMatrixInvalidError, EmptyDatasetError, Engine, Error, IndexOutOfRangeError,
     InvalidArgumentsError, InvalidSeriesError, KMedoidsConfig, KOutOfRangeError, ScoreReport,
     SingleClusterUndefinedError, TimeSeries, WarpWindow, assign_to_medoids, assignment_cost,
-    build_matrix, build_matrix_packed, engine, kmedoids, silhouette_scores, update_medoids,
+    build_matrix, build_matrix_packed, dtw_distance, engine, kmedoids, silhouette_scores, update_medoids,
     validate, validate_dataset,
 )

@@ -511,6 +511,21 @@ def _wrap(cond: np.ndarray, p: int, eng: Engine) -> DistanceMatrix:
     return m
 
 
+def dtw_distance(x: TimeSeries, y: TimeSeries, w: WarpWindow, *, device: int = 0) -> float:
+    """dtw.hpp:40-75 for one pair on the GPU: validate both series, then the band's
+    feasibility (BandInfeasibleError without a pair), then the bit-identical distance."""
+    validate(x)
+    validate(y)
+    n, m = len(x.samples), len(y.samples)
+    if not w.feasible_for(n, m):
+        raise BandInfeasibleError(
+            f"half-width {w.half_width()} is narrower than the length gap of {abs(n - m)} "
+            f"(lengths {n} and {m})")
+    samples = np.concatenate([np.asarray(x.samples, np.float64), np.asarray(y.samples, np.float64)])
+    offsets = np.array([0, n, n + m], dtype=np.int64)
+    return float(engine(device).build_condensed(samples, offsets, w.native, False, 1, FP64)[0])
+
+
 def build_matrix_packed(samples: np.ndarray, offsets: np.ndarray, w: WarpWindow,
                         auto_widen: bool = False, *, precision: int = FP64,
                         device: int = 0, devices: Optional[Sequence[int]] = None

@@ -65,6 +65,20 @@ int main() {
        [] { return same_matrix(walks(3, 50, 50, 700), WarpWindow::banded(30), true); }},
       {"matrix: short series (many pairs)",
        [] { return same_matrix(walks(4, 300, 30, 46), WarpWindow::unlimited(), false); }},
+      {"dtw_distance: one pair, same value and errors",
+       [] {
+         const auto ds = walks(9, 2, 3000, 3500);
+         for (const WarpWindow& w : {WarpWindow::unlimited(), WarpWindow::banded(600)}) {
+           const double a = dtwclust::dtw_distance(ds[0], ds[1], w);
+           const double b = dtwgpu::dtw_distance(ds[0], ds[1], w);
+           require(a == b, "distance differs");
+         }
+         std::string e1, e2;
+         try { dtwclust::dtw_distance(ds[0], ds[1], WarpWindow::banded(1)); } catch (const BandInfeasibleError& e) { e1 = e.what(); }
+         try { dtwgpu::dtw_distance(ds[0], ds[1], WarpWindow::banded(1)); } catch (const BandInfeasibleError& e) { e2 = e.what(); }
+         require(!e1.empty() && e1 == e2, "errors differ: " + e1 + " / " + e2);
+         return "3000-3500 samples, unlimited and banded(600) equal; '" + e2 + "'";
+       }},
       {"errors: first band-infeasible pair",
        [] {
          const std::vector<TimeSeries> ds = {testing::make_series("a", {1, 2}),

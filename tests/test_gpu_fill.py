@@ -450,3 +450,18 @@ def test_multi_device_context_edge_cases():
     finally:
         multi.close()
         single.close()
+
+
+def test_single_pair_dtw_distance_api():
+    """api.dtw_distance (dtw.hpp:40-75 on the GPU): KATs, a long pair, and the error."""
+    assert api.dtw_distance(ts("a", [0]), ts("b", [5]), U) == 25.0
+    assert api.dtw_distance(ts("a", [0, 0, 0, 10]), ts("b", [10, 0, 0, 0]),
+                            WarpWindow.banded(0)) == 200.0
+    rng = ScalarRng(0xD7)
+    from tests.helpers import random_walk_series
+    x, y = random_walk_series(rng, 6000), random_walk_series(rng, 5200)
+    assert api.dtw_distance(ts("x", x), ts("y", y), WarpWindow.banded(900)) == \
+        oracle.dtw(x, y, 900)
+    with pytest.raises(BandInfeasibleError) as ei:
+        api.dtw_distance(ts("x", x), ts("y", y), WarpWindow.banded(10))
+    assert not ei.value.has_pair() and "length gap of 800" in str(ei.value)
