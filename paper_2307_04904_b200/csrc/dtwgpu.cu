@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <functional>
 #include <map>
 #include <string>
 #include <thread>
@@ -1280,8 +1281,10 @@ int dtwg_synchronize(dtwg_ctx* ctx) {
   return DTWG_OK;
 }
 
-int dtwg_upload_series(dtwg_ctx* ctx, const double* samples, const int64_t* offsets, int64_t p) {
-  if (!ctx) return DTWG_INVALID_ARGUMENTS;
+// Starts the upload (async H2D on the context's stream) without the per-series checks;
+// dtwg_upload_series adds them, dtwg_build_matrix overlaps them with the fill.
+static int upload_begin(dtwg_ctx* ctx, const double* samples, const int64_t* offsets,
+                        int64_t p) {
   cudaSetDevice(ctx->device);
   if (p <= 0) return ctx->fail(DTWG_EMPTY_DATASET, "dataset contains no series");
   if (!offsets || (offsets[p] > 0 && !samples))
@@ -1317,11 +1320,21 @@ int dtwg_upload_series(dtwg_ctx* ctx, const double* samples, const int64_t* offs
   CU(cudaMemcpyAsync(ctx->d_offsets.ptr, ctx->h_offsets.data(), (p + 1) * sizeof(int64_t),
                      cudaMemcpyHostToDevice, ctx->stream),
      "H2D offsets");
-  // time_series.hpp:24-33 on the host while the (pinned) copy runs
-  const int rc = validate_series(ctx, samples, offsets, p);
-  CU(cudaStreamSynchronize(ctx->stream), "sync");
-  if (rc) return rc;
   ctx->p = p;
+  return DTWG_OK;
+}
+
+int dtwg_upload_series(dtwg_ctx* ctx, const double* samples, const int64_t* offsets, int64_t p) {
+  if (!ctx) return DTWG_INVALID_ARGUMENTS;
+  int rc = upload_begin(ctx, samples, offsets, p);
+  if (rc) return rc;
+  // time_series.hpp:24-33 on the host while the (pinned) copy runs
+  rc = validate_series(ctx, samples, offsets, p);
+  CU(cudaStreamSynchronize(ctx->stream), "sync");
+  if (rc) {
+    ctx->p = 0;  // nothing uploaded is usable
+    return rc;
+  }
   return DTWG_OK;
 }
 
@@ -1514,7 +1527,8 @@ void parallel_copy(double* dst, const double* src, int64_t n) {
 
 // Slots [sb, se) of the matrix (all when se < 0) into out[sb, se).
 static int build_streamed(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, double* out,
-                          bool chunk_fill, int64_t sb = 0, int64_t se = -1) {
+                          bool chunk_fill, int64_t sb = 0, int64_t se = -1,
+                          const std::function<int()>& host_work = {}) {
   const int64_t all = ctx->p * (ctx->p - 1) / 2;
   if (se < 0) se = all;
   const int64_t total = se - sb;  // slots of this range
@@ -1565,6 +1579,13 @@ static int build_streamed(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precisi
       return fail(ctx->fail(DTWG_CUDA_ERROR, "event record"));
   }
   cudaEventRecord(ctx->ev1, ctx->stream);
+  if (host_work) {  // e.g. the per-series checks, overlapping the fill just enqueued
+    rc = host_work();
+    if (rc) {
+      cudaStreamSynchronize(ctx->stream);
+      return fail(rc);
+    }
+  }
   auto enqueue_copy = [&](int64_t c) -> int {
     const int64_t b = sb + c * chunk, e = std::min(se, b + chunk);
     if (cudaStreamWaitEvent(ctx->copy_stream, filled[c], 0) != cudaSuccess ||
@@ -1664,10 +1685,35 @@ int dtwg_build_matrix(dtwg_ctx* ctx, const double* samples, const int64_t* offse
   // pairwise.hpp:65-67: EmptyDataset, then workers, then series validation.
   if (p <= 0) return ctx->fail(DTWG_EMPTY_DATASET, "dataset contains no series");
   if (workers == 0) return ctx->fail(DTWG_INVALID_ARGUMENTS, "workers must be >= 1");
-  int rc = dtwg_upload_series(ctx, samples, offsets, p);
-  if (rc) return rc;
   const int64_t total = p * (p - 1) / 2;
   const int64_t out_bytes = total * (int64_t)sizeof(double);
+  const bool staged = ctx->devs.empty() && out_condensed && total > 0 &&
+                      out_bytes >= env_or("DTWGPU_STREAM_MIN_BYTES", kStreamMinBytes);
+  if (staged) {
+    // H2D, fill and D2H are enqueued first; the per-series checks (pairwise.hpp:65-67)
+    // run on the host meanwhile and decide before anything is returned
+    int rc = upload_begin(ctx, samples, offsets, p);
+    if (rc) return rc;
+    rc = check_band(ctx, half_width, auto_widen);
+    if (rc) {
+      cudaStreamSynchronize(ctx->stream);
+      const int vr = validate_series(ctx, samples, offsets, p);  // earlier in the order
+      ctx->p = vr ? 0 : ctx->p;
+      return vr ? vr : rc;
+    }
+    const bool chunk_fill =
+        ctx->uniform && out_bytes >= env_or("DTWGPU_CHUNK_FILL_MIN_BYTES", kChunkFillMinBytes);
+    rc = build_streamed(ctx, half_width, auto_widen, precision, out_condensed, chunk_fill, 0, -1,
+                        [&] { return validate_series(ctx, samples, offsets, p); });
+    if (rc) {
+      if (rc == DTWG_INVALID_SERIES || rc == DTWG_INVALID_ARGUMENTS) ctx->p = 0;
+      return rc;
+    }
+    if (evaluations) *evaluations = (uint64_t)total;
+    return DTWG_OK;
+  }
+  int rc = dtwg_upload_series(ctx, samples, offsets, p);
+  if (rc) return rc;
   if (!ctx->devs.empty() && out_condensed && total > 0) {
     // every device fills its slot range and copies it straight into the caller's buffer
     rc = check_band(ctx, half_width, auto_widen);  // first infeasible pair, row-major
@@ -1683,15 +1729,6 @@ int dtwg_build_matrix(dtwg_ctx* ctx, const double* samples, const int64_t* offse
                             c->uniform && (bnd[d + 1] - bnd[d]) * 8 >= kChunkFillMinBytes,
                             bnd[d], bnd[d + 1]);
     });
-    if (rc) return rc;
-    if (evaluations) *evaluations = (uint64_t)total;
-    return DTWG_OK;
-  }
-  if (out_condensed && total > 0 &&
-      out_bytes >= env_or("DTWGPU_STREAM_MIN_BYTES", kStreamMinBytes)) {
-    const bool chunk_fill =
-        ctx->uniform && out_bytes >= env_or("DTWGPU_CHUNK_FILL_MIN_BYTES", kChunkFillMinBytes);
-    rc = build_streamed(ctx, half_width, auto_widen, precision, out_condensed, chunk_fill);
     if (rc) return rc;
     if (evaluations) *evaluations = (uint64_t)total;
     return DTWG_OK;

@@ -465,3 +465,21 @@ def test_single_pair_dtw_distance_api():
     with pytest.raises(BandInfeasibleError) as ei:
         api.dtw_distance(ts("x", x), ts("y", y), WarpWindow.banded(10))
     assert not ei.value.has_pair() and "length gap of 800" in str(ei.value)
+
+
+def test_staged_build_validation_order(eng):
+    """Outputs >= 1 MB overlap the per-series checks with the fill; the errors and their
+    order stay the reference's (pairwise.hpp:65-79): InvalidSeries before BandInfeasible."""
+    rng = np.random.default_rng(4)
+    rows = [rng.normal(size=int(rng.integers(20, 60))) for _ in range(700)]  # 244 650 pairs
+    s, o = pack(rows)
+    got = eng.build_condensed(s, o, -1)
+    assert_bitwise(got[:5000], oracle.build_condensed(s, o, -1)[:5000])
+    bad = s.copy()
+    bad[o[400] + 3] = np.nan
+    with pytest.raises(InvalidSeriesError):
+        eng.build_condensed(bad, o, 2)          # infeasible band too: the series error wins
+    with pytest.raises(BandInfeasibleError) as ei:
+        eng.build_condensed(s, o, 2)
+    assert ei.value.has_pair()
+    assert_bitwise(eng.build_condensed(s, o, -1), got)  # the context is usable afterwards
