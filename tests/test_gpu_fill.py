@@ -483,3 +483,48 @@ def test_staged_build_validation_order(eng):
         eng.build_condensed(s, o, 2)
     assert ei.value.has_pair()
     assert_bitwise(eng.build_condensed(s, o, -1), got)  # the context is usable afterwards
+
+
+def test_acceptance_band_properties():
+    """acceptance_main.cpp:129-149 (criterion 2) at its size: 1000 pairs (seed 0xBA2D, up to
+    24 samples) -- cost non-increasing as the band widens from the gap to max(n, m), and
+    equal to the unlimited window at saturation. All pairs go through the GPU together,
+    one build per half-width (auto-widen keeps the cross pairs feasible)."""
+    rng = ScalarRng(0xBA2D)
+    pairs = [(random_int_series(rng, 24, -5, 5), random_int_series(rng, 24, -5, 5))
+             for _ in range(1000)]
+    rows = [r for xy in pairs for r in xy]
+    s, o = pack(rows)
+    p = len(rows)
+    slot = [2 * t * p - 2 * t * (2 * t + 1) // 2 for t in range(len(pairs))]  # (2t, 2t+1)
+    unl = api.engine(0).build_condensed(s, o, -1)
+    prev = np.full(len(pairs), np.inf)
+    for hw in range(0, 25):
+        d = api.engine(0).build_condensed(s, o, hw, True)
+        for t, (x, y) in enumerate(pairs):
+            gap, sat = abs(len(x) - len(y)), max(len(x), len(y))
+            if hw < gap or hw > sat:
+                continue
+            c = d[slot[t]]
+            assert c <= prev[t], (t, hw)
+            prev[t] = c
+            if hw == sat:
+                assert c == unl[slot[t]], (t, hw)
+
+
+@pytest.mark.slow
+def test_acceptance_memory_at_scale():
+    """acceptance_main.cpp:153-187 (criterion 3): the 1e5-sample random-walk pair (seed 0x3E),
+    through the strip pipeline, finite, the p = 2 build equal to dtw_distance, and bit-
+    identical to the reference (one CPU core, ~30 s)."""
+    from tests.helpers import random_walk_series
+    rng = ScalarRng(0x3E)
+    x = random_walk_series(rng, 100000)
+    y = random_walk_series(rng, 100000)
+    d = api.dtw_distance(ts("x", x), ts("y", y), U)
+    s, o = pack([x, y])
+    e = api.engine(0)
+    assert e.build_condensed(s, o, -1)[0] == d and "strip[" in e.last_plan()
+    assert np.isfinite(d) and d >= 0.0
+    want = oracle.ref_dtw(x, y, -1) if oracle.have_ref() else oracle.dtw(x, y, -1)
+    assert d == want

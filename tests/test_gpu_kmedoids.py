@@ -259,3 +259,19 @@ def test_restart_workers_identical(monkeypatch, workers):
     med, asg, cost = kref(D, 400, cfg, lambda r, it, c: ref_trace.append((r, it, c)))
     assert got.medoids == list(med) and got.assignment == list(asg) and got.total_cost == cost
     assert trace == ref_trace
+
+
+def test_acceptance_silhouette_fuzz():
+    """acceptance_main.cpp:420-436 (criterion 9): 200 fuzzed instances (seed 0x9C, p in
+    [3, 12], k in [2, p]) -- silhouettes in [-1, 1] and bit-identical to the reference."""
+    rng = ScalarRng(0x9C)
+    for trial in range(200):
+        p = 3 + rng.next_below(10)
+        D = random_condensed(rng, p)
+        k = 2 + rng.next_below(p - 1)
+        m = DistanceMatrix.from_condensed(p, D)
+        res = kmedoids(m, KMedoidsConfig(k=k, seed=trial))
+        rep = api.silhouette_scores(m, res)
+        assert all(-1.0 <= v <= 1.0 for v in rep.silhouette)
+        sil, mean = sref(D, p, res.medoids, res.assignment)
+        assert np.array_equal(np.array(rep.silhouette), sil) and rep.mean_silhouette == mean
