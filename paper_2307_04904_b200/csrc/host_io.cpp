@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -122,6 +123,13 @@ inline char* format_double(char* p, char* end, double v) {
   return std::to_chars(p, end, v).ptr;
 }
 
+// Text block size for streaming loads (DTWGPU_IO_BLOCK bytes; tests use small blocks).
+int64_t env_block_bytes() {
+  const char* v = std::getenv("DTWGPU_IO_BLOCK");
+  const int64_t b = v && *v ? std::strtoll(v, nullptr, 10) : (int64_t)64 << 20;
+  return std::max<int64_t>(b, 16);
+}
+
 struct Err {  // first error of a range, in file order
   int64_t line = -1;
   int code = 0;
@@ -190,180 +198,202 @@ int dtwg_save_matrix_text(const double* condensed, int64_t p, const char* path, 
 }
 
 // distance_matrix.hpp:127-192. On success *condensed_out is malloc'ed (dtwg_free).
+// The file is read in blocks of whole lines (bounded memory: the matrix plus one block of
+// text and its parsed rows -- c3-sized files are ~10 GB of text); each block's rows are
+// parsed by several threads and checked against the rows before them; the first error in
+// file order is the one the sequential reference raises.
 int dtwg_load_matrix_text(const char* path, int threads, int64_t* p_out, double** condensed_out) {
   if (!path || !p_out || !condensed_out)
     return io_fail(DTWG_INVALID_ARGUMENTS, "load_matrix: bad arguments");
   *condensed_out = nullptr;
-  std::string text;
-  {
-    std::FILE* f = std::fopen(path, "rb");
-    if (!f) return io_fail(3, std::string("cannot open '") + path + "' for reading");
-    std::fclose(f);
-    if (!read_file(path, text)) return io_fail(3, std::string("failed reading '") + path + "'");
-  }
-  const std::vector<int64_t> st = line_starts(text);
-  const int64_t nlines = (int64_t)st.size() - 1;
+  std::FILE* f = std::fopen(path, "rb");
+  if (!f) return io_fail(3, std::string("cannot open '") + path + "' for reading");
+  struct Closer {
+    std::FILE* f;
+    ~Closer() { std::fclose(f); }
+  } closer{f};
   auto fv = [](int64_t line, const std::string& m) { return io_fail(9, m, line); };
-  if (nlines < 1) return fv(1, "missing 'p=<count>' header");
-  const std::string_view head = line_at(text, st, 0);
-  if (head.rfind("p=", 0) != 0) return fv(1, "expected 'p=<count>' header");
+  // block reader: text holds [consumed, size) of not-yet-parsed data
+  std::string text;
+  size_t head = 0;
+  bool eof = false;
+  const size_t kBlock = (size_t)env_block_bytes();
+  auto refill = [&]() -> bool {  // append one block (no erase: spans stay valid)
+    if (eof) return true;
+    const size_t old = text.size();
+    text.resize(old + kBlock);
+    const size_t got = std::fread(&text[old], 1, kBlock, f);
+    text.resize(old + got);
+    if (got < kBlock) {
+      if (std::ferror(f)) return false;
+      eof = true;
+    }
+    return true;
+  };
+  // next complete line [b, e) after head (without '\n'); false at EOF with nothing left
+  auto next_line = [&](size_t& b, size_t& e, bool& had_nl) -> bool {
+    for (;;) {
+      const void* nl = std::memchr(text.data() + head, '\n', text.size() - head);
+      if (nl) {
+        b = head;
+        e = (size_t)((const char*)nl - text.data());
+        head = e + 1;
+        had_nl = true;
+        return true;
+      }
+      if (eof) {
+        if (head >= text.size()) return false;
+        b = head;
+        e = text.size();
+        head = e;
+        had_nl = false;
+        return true;
+      }
+      if (!refill()) return false;
+    }
+  };
+  auto strip_cr = [&](size_t b, size_t e) {
+    if (e > b && text[e - 1] == '\r') --e;
+    return std::string_view(text.data() + b, e - b);
+  };
+  size_t lb = 0, le = 0;
+  bool nl = false;
+  if (!refill()) return io_fail(3, std::string("failed reading '") + path + "'");
+  if (!next_line(lb, le, nl)) return fv(1, "missing 'p=<count>' header");
+  const std::string head_line(strip_cr(lb, le));
+  if (head_line.rfind("p=", 0) != 0) return fv(1, "expected 'p=<count>' header");
   std::size_t pz = 0;
   {
-    const char* b = head.data() + 2;
-    const char* e = head.data() + head.size();
-    const auto r = std::from_chars(b, e, pz);
-    if (r.ec != std::errc() || r.ptr != e || pz == 0)
-      return fv(1, "header count '" + std::string(head.substr(2)) + "' is not a positive integer");
+    const char* b0 = head_line.data() + 2;
+    const char* e0 = head_line.data() + head_line.size();
+    const auto r = std::from_chars(b0, e0, pz);
+    if (r.ec != std::errc() || r.ptr != e0 || pz == 0)
+      return fv(1, "header count '" + head_line.substr(2) + "' is not a positive integer");
   }
   const int64_t p = (int64_t)pz;
-  const int64_t rows_avail = std::min<int64_t>(p, nlines - 1);
   const int64_t total = p * (p - 1) / 2;
   double* cond = (double*)std::malloc((size_t)std::max<int64_t>(total, 1) * sizeof(double));
-  // (i, j < i) as written in row i, row-major (row i at i(i-1)/2): sequential writes while
-  // parsing, compared against the upper triangle afterwards
-  std::vector<double> lower((size_t)std::max<int64_t>(total, 1));
-  auto loff = [](int64_t i) { return i * (i - 1) / 2; };
   if (!cond) return io_fail(3, "out of host memory");
+  struct Freer {
+    double*& c;
+    bool keep = false;
+    ~Freer() {
+      if (!keep) std::free(c);
+    }
+  } freer{cond};
   auto off = [p](int64_t i) { return i * p - i * (i + 1) / 2; };
-  const int nt = thread_count(threads, rows_avail);
-  std::vector<Err> errs(nt);
-  // phase 1: tokenise and check each row on its own (syntax, diagonal, finiteness)
-  parallel_ranges(nt, rows_avail, [&](int t, int64_t b, int64_t e) {
-    std::vector<double> row((size_t)p);
-    for (int64_t i = b; i < e; ++i) {
-      const int64_t line_no = i + 2;
-      const std::string_view line = line_at(text, st, i + 1);
-      int64_t cell = 0;
-      size_t start = 0;
-      std::string err;
-      while (true) {
-        const size_t comma = line.find(',', start);
-        const std::string_view tok =
-            line.substr(start, (comma == std::string_view::npos ? line.size() : comma) - start);
-        if (cell >= p) {
-          err = "row has more than " + std::to_string(p) + " cells";
-          break;
+  const int nt0 = threads > 0 ? threads : (int)std::max(1u, std::thread::hardware_concurrency());
+  // rows per block: about one block of text, at least the threads
+  const int64_t rows_per_block = std::max<int64_t>(
+      std::min<int64_t>(nt0, 64), std::min<int64_t>(p, (int64_t)(kBlock / (size_t)(8 * p + 1)) + 1));
+  std::vector<double> rows((size_t)(rows_per_block * p));
+  std::vector<std::pair<size_t, size_t>> spans((size_t)rows_per_block);
+  struct RowErr {
+    int kind = 0;  // 0 none, 1 syntax/count, 2 value error at column `col`
+    int64_t col = 0;
+    std::string msg;
+  };
+  std::vector<RowErr> rerr((size_t)rows_per_block);
+  std::vector<int64_t> asym((size_t)rows_per_block);
+  int64_t done = 0;
+  while (done < p) {
+    // drop the text already parsed, then gather the next block of complete lines
+    text.erase(0, head);
+    head = 0;
+    int64_t nb = 0;
+    while (nb < rows_per_block && done + nb < p) {
+      if (!next_line(lb, le, nl)) break;
+      spans[(size_t)nb++] = {lb, le};
+    }
+    if (nb == 0) {
+      if (!eof) return io_fail(3, std::string("failed reading '") + path + "'");
+      return fv(done + 2, "expected " + std::to_string(p) + " matrix rows");
+    }
+    const int nt = thread_count(threads, nb);
+    // phase 1: tokenise + diagonal/finiteness; upper triangle into cond
+    parallel_ranges(nt, nb, [&](int, int64_t b0, int64_t e0) {
+      for (int64_t r = b0; r < e0; ++r) {
+        const int64_t i = done + r;
+        double* row = &rows[(size_t)(r * p)];
+        const std::string_view line = strip_cr(spans[(size_t)r].first, spans[(size_t)r].second);
+        RowErr& E = rerr[(size_t)r];
+        E = RowErr{};
+        asym[(size_t)r] = -1;
+        int64_t cell = 0;
+        size_t start = 0;
+        while (true) {
+          const size_t comma = line.find(',', start);
+          const std::string_view tok =
+              line.substr(start, (comma == std::string_view::npos ? line.size() : comma) - start);
+          if (cell >= p) {
+            E = RowErr{1, 0, "row has more than " + std::to_string(p) + " cells"};
+            break;
+          }
+          double v = 0.0;
+          const auto res = std::from_chars(tok.data(), tok.data() + tok.size(), v);
+          if (res.ec != std::errc() || res.ptr != tok.data() + tok.size() || tok.empty()) {
+            E = RowErr{1, 0, "cell '" + std::string(tok) + "' is not a decimal value"};
+            break;
+          }
+          row[cell++] = v;
+          if (comma == std::string_view::npos) break;
+          start = comma + 1;
         }
-        double v = 0.0;
-        const auto r = std::from_chars(tok.data(), tok.data() + tok.size(), v);
-        if (r.ec != std::errc() || r.ptr != tok.data() + tok.size() || tok.empty()) {
-          err = "cell '" + std::string(tok) + "' is not a decimal value";
-          break;
-        }
-        row[(size_t)cell++] = v;
-        if (comma == std::string_view::npos) break;
-        start = comma + 1;
-      }
-      if (err.empty() && cell != p)
-        err = "row has " + std::to_string(cell) + " cells, expected " + std::to_string(p);
-      if (err.empty()) {
-        for (int64_t j = 0; j < p && err.empty(); ++j) {
-          const double v = row[(size_t)j];
+        if (E.kind == 0 && cell != p)
+          E = RowErr{1, 0, "row has " + std::to_string(cell) + " cells, expected " + std::to_string(p)};
+        if (E.kind != 0) continue;
+        for (int64_t j = 0; j < p; ++j) {
+          const double v = row[j];
           if (i == j) {
-            if (v != 0.0) err = "diagonal entry must be exactly 0";
+            if (v != 0.0) {
+              E = RowErr{2, j, "diagonal entry must be exactly 0"};
+              break;
+            }
             continue;
           }
           if (!(std::isfinite(v) && v >= 0.0)) {
-            err = "entries must be finite and non-negative";
+            E = RowErr{2, j, "entries must be finite and non-negative"};
             break;
           }
           if (j > i) cond[off(i) + (j - i - 1)] = v;
-          else lower[(size_t)(loff(i) + j)] = v;
         }
       }
-      if (!err.empty()) {
-        errs[t] = Err{line_no, 9, err};
-        return;
+    });
+    // first row of the block with a syntax error: rows after it are never compared
+    int64_t stop = nb;
+    for (int64_t r = 0; r < nb; ++r)
+      if (rerr[(size_t)r].kind != 0) {
+        stop = r + 1;
+        break;
       }
-    }
-  });
-  // first row-local error, in file order
-  int64_t bad_row = -1;
-  std::string bad_msg;
-  for (auto& e : errs)
-    if (e.set()) {
-      bad_row = e.line - 2;
-      bad_msg = e.msg;
-      break;
-    }
-  // phase 2: symmetry (row i, column j < i against row j's stored value), rows before the
-  // first row-local error only; the reference meets them in the same row order, and within
-  // a row a finiteness/diagonal error at column j' and an asymmetry at j compete by column.
-  const int64_t sym_rows = bad_row >= 0 ? bad_row + 1 : rows_avail;
-  std::vector<Err> serrs(nt);
-  parallel_ranges(nt, sym_rows, [&](int t, int64_t b, int64_t e) {
-    for (int64_t i = b; i < e; ++i) {
-      for (int64_t j = 0; j < i; ++j) {
-        if (i == bad_row) break;  // handled below (needs the column of the row-local error)
-        if (lower[(size_t)(loff(i) + j)] != cond[off(j) + (i - j - 1)]) {
-          serrs[t] = Err{i + 2, 9,
-                         "matrix is not symmetric at (" + std::to_string(i) + ", " +
-                             std::to_string(j) + ")",
-                         j};
-          return;
-        }
+    // phase 2: symmetry (row i, column j < i, against row j's stored value); a row with
+    // a value error at column j' competes by column (j < j' wins)
+    parallel_ranges(thread_count(threads, stop), stop, [&](int, int64_t b0, int64_t e0) {
+      for (int64_t r = b0; r < e0; ++r) {
+        const RowErr& E = rerr[(size_t)r];
+        if (E.kind == 1) continue;
+        const int64_t i = done + r;
+        const double* row = &rows[(size_t)(r * p)];
+        const int64_t jmax = E.kind == 2 ? std::min<int64_t>(E.col, i) : i;
+        for (int64_t j = 0; j < jmax; ++j)
+          if (row[j] != cond[off(j) + (i - j - 1)]) {
+            asym[(size_t)r] = j;
+            break;
+          }
       }
+    });
+    for (int64_t r = 0; r < stop; ++r) {
+      const int64_t i = done + r;
+      if (asym[(size_t)r] >= 0)
+        return fv(i + 2, "matrix is not symmetric at (" + std::to_string(i) + ", " +
+                             std::to_string(asym[(size_t)r]) + ")");
+      if (rerr[(size_t)r].kind != 0) return fv(i + 2, rerr[(size_t)r].msg);
     }
-  });
-  int64_t sym_row = -1;
-  std::string sym_msg;
-  for (auto& e : serrs)
-    if (e.set()) {
-      sym_row = e.line - 2;
-      sym_msg = e.msg;
-      break;
-    }
-  if (sym_row >= 0 && (bad_row < 0 || sym_row < bad_row)) {
-    std::free(cond);
-    return fv(sym_row + 2, sym_msg);
-  }
-  if (bad_row >= 0) {
-    // Row bad_row has a row-local error; if it parsed (value error at column j'), an
-    // asymmetry at a smaller column j < min(j', bad_row) comes first in the reference.
-    const std::string_view line = line_at(text, st, bad_row + 1);
-    (void)line;
-    bool value_err = bad_msg == "diagonal entry must be exactly 0" ||
-                     bad_msg == "entries must be finite and non-negative";
-    if (value_err) {
-      // recompute the failing column
-      std::vector<double> row((size_t)p);
-      size_t start = 0;
-      for (int64_t c = 0; c < p; ++c) {
-        const size_t comma = line.find(',', start);
-        const std::string_view tok =
-            line.substr(start, (comma == std::string_view::npos ? line.size() : comma) - start);
-        std::from_chars(tok.data(), tok.data() + tok.size(), row[(size_t)c]);
-        start = comma + 1;
-      }
-      int64_t jbad = 0;
-      for (; jbad < p; ++jbad) {
-        const double v = row[(size_t)jbad];
-        if (bad_row == jbad) {
-          if (v != 0.0) break;
-          continue;
-        }
-        if (!(std::isfinite(v) && v >= 0.0)) break;
-      }
-      for (int64_t j = 0; j < std::min(jbad, bad_row); ++j) {
-        if (row[(size_t)j] != cond[off(j) + (bad_row - j - 1)]) {
-          std::free(cond);
-          return fv(bad_row + 2, "matrix is not symmetric at (" + std::to_string(bad_row) +
-                                     ", " + std::to_string(j) + ")");
-        }
-      }
-    }
-    std::free(cond);
-    return fv(bad_row + 2, bad_msg);
-  }
-  if (rows_avail < p) {
-    std::free(cond);
-    return fv(rows_avail + 2, "expected " + std::to_string(p) + " matrix rows");
+    done += nb;
   }
   // the reference reads the next line raw here (no '\r' stripping): "\r" alone is content
-  if (nlines > p + 1 && st[p + 2] - st[p + 1] - (text[st[p + 2] - 1] == '\n' ? 1 : 0) > 0) {
-    std::free(cond);
-    return fv(p + 2, "unexpected content after the last matrix row");
-  }
+  if (next_line(lb, le, nl) && le > lb) return fv(p + 2, "unexpected content after the last matrix row");
+  freer.keep = true;
   *p_out = p;
   *condensed_out = cond;
   return DTWG_OK;

@@ -23,7 +23,10 @@ def write(path, text, mode="w"):
 # ---------------------------------------------------------------- matrix text / binary
 @needs_ref
 @pytest.mark.parametrize("p,threads", [(1, 1), (2, 1), (7, 3), (64, 8), (301, 0)])
-def test_save_matrix_byte_identical_and_round_trip(tmp_path, p, threads):
+@pytest.mark.parametrize("block", [None, "4096"])
+def test_save_matrix_byte_identical_and_round_trip(tmp_path, monkeypatch, p, threads, block):
+    if block:
+        monkeypatch.setenv("DTWGPU_IO_BLOCK", block)
     D = random_condensed(ScalarRng(p), p, 0.0, 1e6) if p > 1 else np.zeros(0)
     if p > 3:
         D[::5] = np.round(D[::5])  # integral values print without a fraction
@@ -70,8 +73,12 @@ BAD_MATRICES = {
 
 @needs_ref
 @pytest.mark.parametrize("name", sorted(BAD_MATRICES))
-@pytest.mark.parametrize("threads", [1, 4])
-def test_load_matrix_errors_match_reference(tmp_path, name, threads):
+@pytest.mark.parametrize("threads,block", [(1, None), (4, None), (3, "16")])
+def test_load_matrix_errors_match_reference(tmp_path, monkeypatch, name, threads, block):
+    """block: the streaming reader's text block (DTWGPU_IO_BLOCK); 16 bytes puts line and
+    block boundaries everywhere."""
+    if block:
+        monkeypatch.setenv("DTWGPU_IO_BLOCK", block)
     path = write(tmp_path / f"{name}.txt", BAD_MATRICES[name], "w" if "\r" not in
                  BAD_MATRICES[name] else "w")
     with open(path, "wb") as f:
