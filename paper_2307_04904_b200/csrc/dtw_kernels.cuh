@@ -181,10 +181,14 @@ struct FullRows {
   }
 };
 
+#ifndef DTWG_FULL_MINB_N  // resident CTAs the Full kernels' registers are capped for
+#define DTWG_FULL_MINB_N 1
+#endif
+#define DTWG_FULL_MINB(G, R, TR) DTWG_FULL_MINB_N
 // Full family. TR rows per step (ILP TR), warp-uniform loops, multi-pass over column
 // strips of width G*R with a per-group boundary column between passes.
 template <int G, int R, int TR, bool MASK, class Ar>
-__global__ void __launch_bounds__(kThreads) dtw_full_kernel(const FillArgs A) {
+__global__ void __launch_bounds__(kThreads, DTWG_FULL_MINB(G, R, TR)) dtw_full_kernel(const FillArgs A) {
   using T = typename Ar::T;
   constexpr bool kF32 = sizeof(T) == 4;
   constexpr int GPW = 32 / G;
