@@ -181,14 +181,18 @@ struct FullRows {
   }
 };
 
-#ifndef DTWG_FULL_MINB_N  // resident CTAs the Full kernels' registers are capped for
-#define DTWG_FULL_MINB_N 1
+// Experiments only (-DDTWG_FULL_MINB_N=k caps the Full kernels' registers for k CTAs per
+// SM). The default passes no minimum: an explicit 1 lets ptxas take more registers
+// (186 instead of <= 170 for G=32 R=16 T=2), dropping residency from 3 to 2 CTAs per SM.
+#ifdef DTWG_FULL_MINB_N
+#define DTWG_FULL_BOUNDS __launch_bounds__(kThreads, DTWG_FULL_MINB_N)
+#else
+#define DTWG_FULL_BOUNDS __launch_bounds__(kThreads)
 #endif
-#define DTWG_FULL_MINB(G, R, TR) DTWG_FULL_MINB_N
 // Full family. TR rows per step (ILP TR), warp-uniform loops, multi-pass over column
 // strips of width G*R with a per-group boundary column between passes.
 template <int G, int R, int TR, bool MASK, class Ar>
-__global__ void __launch_bounds__(kThreads, DTWG_FULL_MINB(G, R, TR)) dtw_full_kernel(const FillArgs A) {
+__global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
   using T = typename Ar::T;
   constexpr bool kF32 = sizeof(T) == 4;
   constexpr int GPW = 32 / G;
@@ -886,11 +890,13 @@ __device__ __forceinline__ void ring_steps(int nst, int& i1, const typename Ar::
   }
 }
 
-#ifndef DTWG_RING_MINB
-#define DTWG_RING_MINB 1
+#ifdef DTWG_RING_MINB  // experiments only; see DTWG_FULL_BOUNDS
+#define DTWG_RING_BOUNDS __launch_bounds__(kThreads, DTWG_RING_MINB)
+#else
+#define DTWG_RING_BOUNDS __launch_bounds__(kThreads)
 #endif
 template <int G, int R, int KR, class Ar>
-__global__ void __launch_bounds__(kThreads, DTWG_RING_MINB) dtw_bandring_kernel(const FillArgs A) {
+__global__ void DTWG_RING_BOUNDS dtw_bandring_kernel(const FillArgs A) {
   static_assert(R >= 2, "band family needs R >= 2");
   static_assert(G * R - G <= kRing - 33, "ring too small for this band width");
   // Lane l's window starts l*(R-1) slots after lane 0's: with R-1 odd the 8-byte reads

@@ -1,0 +1,379 @@
+// planner.cu -- which kernel family and (G, R) instantiation fills each pair shape, and
+// the slot lists of the resulting pair classes ("Planner").
+#include "host_ctx.cuh"
+
+namespace dtwgpu {
+namespace host {
+
+// ---- planner ------------------------------------------------------------------------
+// Candidate instantiations with their measured throughput in computed lane-cells per
+// ns on one B200 (tools/sweep.py, profiles/round1_sweep.md): the cost of a shape is
+// the lane-cells a configuration computes (band waste, wavefront fill/drain, padding
+// columns, masked rows all included) divided by that rate. Multi-pass Full fills with
+// few lanes pay an extra per-pass boundary-column cost (measured on c4).
+struct Cand {
+  int G, R;
+  double rate;  // computed lane-cells / ns
+  int P = 1;    // band family: pairs per lane group
+  int TR = 2;   // full family: rows per step
+  bool ring = false;  // band family: shared-memory y ring
+  int U = 1;          // ring variant: units per lane
+};
+const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026},
+                      {4, 12, 1956, 1, 4},   {8, 8, 1804},         {8, 8, 1700, 1, 4},
+                      {16, 8, 1800},         {16, 16, 1850},       {16, 16, 1850, 1, 4},
+                      {32, 4, 1300},         {32, 8, 1650},        {32, 12, 1950},
+                      {32, 15, 2000},        {32, 15, 2150, 1, 4}, {32, 16, 2100},
+                      {32, 16, 2050, 1, 4}};
+const Cand kBand[] = {{16, 7, 1500},    {16, 9, 1600},    {16, 11, 1700},  {16, 13, 1800},
+                      {32, 3, 1000},    {32, 5, 1250},    {32, 7, 1490},   {32, 9, 1500},
+                      {32, 13, 1450},   {32, 3, 600, 2},  {32, 5, 600, 2},  {32, 7, 700, 2},
+                      {8, 16, 1900, 1, 2, true},  {8, 26, 2221, 1, 2, true},
+                      {16, 8, 1500, 1, 2, true},  {16, 14, 2105, 1, 2, true},
+                      {32, 6, 1300, 1, 2, true},
+                      // ring with U units per lane (c2 sweep, round 1)
+                      {8, 26, 2286, 1, 2, true, 3}, {8, 26, 2198, 1, 2, true, 5},
+                      {16, 14, 2166, 1, 2, true, 3}, {16, 13, 2128, 1, 2, true, 2},
+                      // wide bands (512-slot ring)
+                      {16, 20, 2186, 1, 2, true, 3}, {16, 26, 2220, 1, 2, true, 3},
+                      {32, 20, 2150, 1, 2, true, 3}, {32, 26, 2170, 1, 2, true, 3}};
+
+// fp32 mode: the cell is FADD FMUL FMNMX3 FADD, so the Full family runs ~2.15x the fp64
+// rate while the Band family (shuffle-heavy per step) gains ~1.45x (measured on c2 after the warp-uniform renormalisation).
+constexpr double kFp32Full = 2.15, kFp32Band = 1.45;
+
+// Masked Full fills: rows where the strip lies entirely inside the band run the plain
+// cell; rows crossing a band edge run the masked cell at 1.79x the cost (least-squares fit
+// over hw = 101..400 at n = m = 1000, tools: exp/band_rates.py, profiles/round1_sweep.md).
+constexpr double kMaskedRowCost = 1.79;
+
+double full_cost(const Shape& s, const Cand& c, bool mask, bool fp32) {
+  const int64_t W = (int64_t)c.G * c.R;
+  const int64_t npass = (s.m + W - 1) / W;
+  double cells = 0;
+  for (int64_t p = 0; p < npass; ++p) {
+    const int64_t c0 = p * W;
+    int64_t rs = 1, re = s.n;
+    if (mask) {
+      rs = std::max<int64_t>(1, c0 + 1 - s.hw);
+      re = std::min<int64_t>(s.n, c0 + W + s.hw);
+    }
+    // TR rows per step, G-1 steps of wavefront fill/drain
+    const int64_t rows = ((re - rs + c.TR) / c.TR) * c.TR;
+    double eff_rows = double(rows);
+    if (mask) {
+      const int64_t fast = std::max<int64_t>(
+          0, std::min<int64_t>(re, c0 + 1 + s.hw) - std::max<int64_t>(rs, c0 + W - s.hw) + 1);
+      const int64_t masked = std::max<int64_t>(0, rows - fast);
+      eff_rows = double(rows - masked) + kMaskedRowCost * double(masked);
+    }
+    cells += (eff_rows + c.TR * (c.G - 1)) * double(W);
+  }
+  double rate = c.rate * (fp32 ? kFp32Full : 1.0);
+  if (npass > 1) {  // boundary-column round trips per pass (measured on c4)
+    // The per-group boundary columns stay in L2 up to ~n = 1500 (c5, L = 1000 sweeps);
+    // the c4-measured penalties apply beyond.
+    const bool l2_resident = s.n <= 1500;
+    if (c.G == 2) rate *= c.TR == 4 ? 0.68 : 0.59;
+    else if (c.G == 4) rate *= (c.TR == 4 && l2_resident) ? 1.05 : (c.TR == 4 ? 0.92 : 0.78);
+    else if (c.G == 8) rate *= c.TR == 4 ? 1.0 : 0.95;
+  }
+  return cells / rate;
+}
+
+double band_cost(const Shape& s, const Cand& c, bool fp32) {
+  // fp32 / fp64 throughput ratios measured on c2 (G=8 R=26: 1.69 ring, 2.06 units;
+  // G=16 R=14: 1.52 ring, 1.72 units; register-rotation band 1.45)
+  const double f32 = c.ring ? (c.U > 1 ? 1.9 : 1.6) : kFp32Band;
+  // wavefront fill/drain: one step per unit of the group
+  return double(s.n + c.G * c.U - 1) * double(c.G * c.R) / (c.rate * (fp32 ? f32 : 1.0));
+}
+
+KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out, int64_t count, int sms);
+
+// Planner entry (choose_cfg, below): a forced (family, G, R) wins when it can legally run the shape.
+
+// Fraction of the GPU a class of `count` pairs can keep busy with G lanes per pair: about
+// 8 warps per SM are needed to cover the cell chain (c1: 4950 pairs fill it with G = 32,
+// not with G = 4 -- 1765 against 946 GCUPS). count = 0: unknown (ragged classes).
+double fill_factor(int64_t count, int G, int sms) {
+  if (count <= 0) return 1.0;
+  const double warps = double(count) * G / 32.0;
+  return std::min(1.0, warps / (8.0 * sms));
+}
+
+KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out, int64_t count = 0,
+                           int sms = 148) {
+  KernelCfg best{Family::Full, 32, 16, true, fp32};
+  double bc = 1e300;
+  const bool mask = s.hw < s.n - 1;  // a band that excludes some cell
+  for (const Cand& c : kFull) {
+    const double cst = full_cost(s, c, mask, fp32) / fill_factor(count, c.G, sms);
+    if (cst < bc) {
+      bc = cst;
+      best = KernelCfg{Family::Full, c.G, c.R, mask, fp32, -1, 1, c.TR};
+    }
+  }
+  if (mask) {
+    const int64_t K = 2 * s.hw + 1;
+    for (const Cand& c : kBand) {
+      if ((int64_t)c.G * c.R < K) continue;
+      const double cst = band_cost(s, c, fp32) / fill_factor(count, c.G, sms);
+      if (cst < bc) {
+        bc = cst;
+        // static kill position: fp64 everywhere, fp32 for the unit-ring variant
+        const bool static_kr = !fp32 || (c.ring && c.U > 1);
+        best = KernelCfg{Family::Band, c.G, c.R, false, fp32, static_kr ? (int)(K % c.R) : -1,
+                         c.P, 2, c.ring, c.U};
+      }
+    }
+  }
+  if (cost_out) *cost_out = bc;
+  return best;
+}
+
+const char* family_name(Family f) {
+  return f == Family::Full ? "full" : (f == Family::Band ? "band" : "strip");
+}
+
+KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cost_out,
+                     int64_t count) {
+  const bool mask = s.hw < s.n - 1;
+  if (ctx->force_family >= 0) {
+    // 0: full (2 rows/step), 1: band P=1, 2: band P=2, 3: full (4 rows/step), 4: band ring,
+    // 10 + U: band ring with U units per lane
+    const int ff = ctx->force_family;
+    if (ff == 5) {  // strip family (long pairs spread over warps), G = 32, 4 rows per step
+      KernelCfg f{Family::Strip, 32, ctx->force_R, mask, fp32, -1, 1, 4};
+      if (dtwgpu::fill_cfg_supported(f)) {
+        if (cost_out) *cost_out = 1.0;
+        return f;
+      }
+    }
+    const bool band = ff == 1 || ff == 2 || ff == 4 || ff > 10;
+    KernelCfg f{band ? Family::Band : Family::Full, ctx->force_G, ctx->force_R,
+                band ? false : mask, fp32,
+                (band && (!fp32 || ff > 10) && ctx->force_R > 0) ? (int)((2 * s.hw + 1) % ctx->force_R)
+                                                                  : -1,
+                ff == 2 ? 2 : 1, ff == 3 ? 4 : 2, ff == 4 || ff > 10, ff > 10 ? ff - 10 : 1};
+    const bool ok = dtwgpu::fill_cfg_supported(f) &&
+                    (f.family == Family::Full ||
+                     (mask && f.R >= 2 && (int64_t)f.G * f.R >= 2 * s.hw + 1));
+    if (ok) {
+      if (cost_out) *cost_out = 1.0;
+      return f;
+    }
+  }
+  return choose_cfg_model(s, fp32, cost_out, count, ctx->num_sms);
+}
+
+Shape shape_of(const dtwg_ctx* ctx, int64_t a, int64_t b, int64_t hw, int auto_widen) {
+  int64_t la = ctx->h_len[a], lb = ctx->h_len[b];
+  Shape s;
+  s.n = std::max(la, lb);
+  s.m = std::min(la, lb);
+  if (hw < 0) {
+    s.hw = s.n;
+  } else {
+    const int64_t gap = s.n - s.m;
+    s.hw = (auto_widen && gap > hw) ? gap : hw;
+  }
+  if (s.hw > s.n) s.hw = s.n;  // a band at least max(n,m) wide is the unlimited window
+  return s;
+}
+
+// A Full-family class of few, long pairs leaves most of the GPU idle (one lane group per
+// pair, passes in sequence). Such classes become Strip classes: every column strip of
+// every pair is a work item for a full warp, pipelined along the pair (dtw_strip_kernel).
+// Rule: at most 4 pairs per SM with >= 2 strips per pair, or at most 16 pairs per SM with
+// >= 8 strips per pair (c1's 4950 pairs of 2 strips stay Full: 1763 against 776 GCUPS).
+// m_uniform < 0: ragged class (lengths per slot).
+constexpr int kStripR = 15;
+void maybe_strip(dtwg_ctx* ctx, PlanClass& pc, int64_t count, int64_t m_uniform) {
+  if (count <= 0) return;
+  const bool forced = pc.cfg.family == Family::Strip;  // dtwg_force_kernel(5, ., R)
+  KernelCfg sc = pc.cfg;
+  if (!forced) {
+    if (pc.cfg.family != Family::Full || ctx->force_family >= 0) return;
+    if (count > 16 * (int64_t)ctx->num_sms) return;  // enough pairs to fill the GPU already
+    sc = KernelCfg{Family::Strip, 32, kStripR, pc.cfg.mask, pc.cfg.fp32, -1, 1, 4};
+    if (!dtwgpu::fill_cfg_supported(sc)) return;
+  }
+  const int64_t W = 32 * (int64_t)sc.R;
+  const int64_t min_strips = count <= 4 * (int64_t)ctx->num_sms ? 2 : 8;  // strips per pair
+  if (m_uniform >= 0) {
+    const int64_t S = (m_uniform + W - 1) / W;
+    if (S < min_strips && !forced) return;
+    pc.strips_per_pair = (int)S;
+  } else {
+    std::vector<int64_t> base(count + 1, 0);
+    const int64_t p = ctx->p;
+    for (int64_t q = 0; q < count; ++q) {
+      const int64_t slot = pc.slots[q];
+      int64_t lo = 0, hi = p - 1;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) / 2;
+        if (row_off(mid, p) <= slot) lo = mid;
+        else hi = mid - 1;
+      }
+      const int64_t i = lo, j = i + 1 + (slot - row_off(i, p));
+      const int64_t m = std::min(ctx->h_len[i], ctx->h_len[j]);
+      base[q + 1] = base[q] + (m + W - 1) / W;
+    }
+    if (base[count] < min_strips * count && !forced) return;
+    pc.strip_base = std::move(base);
+  }
+  pc.cfg = sc;
+}
+
+std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool fp32,
+                                 int64_t sb, int64_t se) {
+  std::vector<PlanClass> plan;
+  if (se <= sb) return plan;
+  const int64_t p = ctx->p;
+  if (ctx->uniform) {
+    PlanClass pc;
+    const Shape s = shape_of(ctx, 0, 1, hw, auto_widen);
+    pc.cfg = choose_cfg(ctx, s, fp32, &pc.cost, se - sb);
+    pc.max_n = s.n;
+    plan.push_back(pc);
+    maybe_strip(ctx, plan[0], se - sb, s.m);
+    return plan;
+  }
+  // Ragged dataset: classify every pair by shape (memoised on (n, m)), then bucket the
+  // slots of each class by (passes, rows) with a counting sort -- longest first (LPT),
+  // and pairs of equal pass count and row count adjacent, so the lane groups of one warp
+  // run in lockstep. O(pairs); no comparison sort.
+  int64_t maxlen = 0;
+  for (int64_t t = 0; t < p; ++t) maxlen = std::max(maxlen, ctx->h_len[t]);
+  const int64_t L1 = maxlen + 1;
+  std::vector<int> cls_tab;
+  const bool use_tab = L1 * L1 <= (int64_t)1 << 26;
+  if (use_tab) cls_tab.assign((size_t)(L1 * L1), -1);
+  std::map<Shape, int> cls_of_shape;
+  std::map<std::tuple<int, int, int, bool, int, int, int>, int> cls_of_cfg;
+  auto class_of = [&](int64_t a, int64_t b, Shape& s) -> int {
+    s = shape_of(ctx, a, b, hw, auto_widen);
+    int* slotp = use_tab ? &cls_tab[(size_t)(s.n * L1 + s.m)] : nullptr;
+    if (slotp && *slotp >= 0) return *slotp;
+    if (!slotp) {
+      auto it = cls_of_shape.find(s);
+      if (it != cls_of_shape.end()) return it->second;
+    }
+    double cst = 0;
+    const KernelCfg cfg = choose_cfg(ctx, s, fp32, &cst);
+    const auto key = std::make_tuple((int)cfg.family * 2 + (int)cfg.ring + 4 * cfg.U, cfg.G, cfg.R, cfg.mask,
+                                     cfg.kr, cfg.P, cfg.TR);
+    int cls;
+    auto ic = cls_of_cfg.find(key);
+    if (ic == cls_of_cfg.end()) {
+      PlanClass pc;
+      pc.cfg = cfg;
+      plan.push_back(pc);
+      cls = (int)plan.size() - 1;
+      cls_of_cfg[key] = cls;
+    } else {
+      cls = ic->second;
+    }
+    if (slotp) *slotp = cls;
+    else cls_of_shape[s] = cls;
+    return cls;
+  };
+  auto bucket_of = [&](int cls, const Shape& s) -> int64_t {
+    const KernelCfg& cc = plan[cls].cfg;
+    const int64_t W = (int64_t)cc.G * cc.R;
+    const int64_t npass = cc.family == Family::Full ? (s.m + W - 1) / W : 1;
+    return npass * L1 + s.n;  // larger = earlier
+  };
+  int64_t i0;
+  {
+    int64_t lo = 0, hi = p - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) / 2;
+      if (row_off(mid, p) <= sb) lo = mid;
+      else hi = mid - 1;
+    }
+    i0 = lo;
+  }
+  const int64_t j0 = i0 + 1 + (sb - row_off(i0, p));
+  // pass 1: classes, bucket counts
+  std::vector<std::vector<int64_t>> counts;
+  {
+    int64_t i = i0, j = j0;
+    Shape s;
+    for (int64_t slot = sb; slot < se; ++slot) {
+      const int cls = class_of(i, j, s);
+      if ((int)counts.size() <= cls) counts.resize(cls + 1);
+      const int64_t bk = bucket_of(cls, s);
+      if ((int64_t)counts[cls].size() <= bk) counts[cls].resize(bk + 1, 0);
+      counts[cls][bk]++;
+      plan[cls].max_n = std::max(plan[cls].max_n, s.n);
+      plan[cls].cost += double(s.n) * double(s.m);
+      plan[cls].cells += double(pair_cells(s.n, s.m, s.hw));
+      if (++j == p) {
+        ++i;
+        j = i + 1;
+      }
+    }
+  }
+  // descending bucket order -> start offsets
+  std::vector<std::vector<int64_t>> start(plan.size());
+  for (size_t c = 0; c < plan.size(); ++c) {
+    auto& cn = counts[c];
+    start[c].assign(cn.size(), 0);
+    int64_t acc = 0;
+    for (int64_t b = (int64_t)cn.size() - 1; b >= 0; --b) {
+      start[c][b] = acc;
+      acc += cn[b];
+    }
+    plan[c].slots.resize(acc);
+  }
+  // pass 2: place slots (and remember each one's shorter length)
+  std::vector<std::vector<int32_t>> mkey(plan.size());
+  for (size_t c = 0; c < plan.size(); ++c) mkey[c].resize(plan[c].slots.size());
+  {
+    int64_t i = i0, j = j0;
+    Shape s;
+    for (int64_t slot = sb; slot < se; ++slot) {
+      const int cls = class_of(i, j, s);
+      const int64_t at = start[cls][bucket_of(cls, s)]++;
+      plan[cls].slots[at] = slot;
+      mkey[cls][at] = (int32_t)s.m;
+      if (++j == p) {
+        ++i;
+        j = i + 1;
+      }
+    }
+  }
+  // pass 3: inside each (passes, rows) bucket, order by the shorter length too, so the
+  // lane groups of a warp mostly share one (n, m) -- same band geometry, same masked
+  // steps, same trip counts. Counting sort per bucket (start[c][b] now marks its end).
+  {
+    std::vector<int64_t> cnt(L1 + 1);
+    std::vector<int64_t> tmp;
+    for (size_t c = 0; c < plan.size(); ++c) {
+      auto& cn = counts[c];
+      auto& sl = plan[c].slots;
+      auto& mk = mkey[c];
+      for (int64_t b = 0; b < (int64_t)cn.size(); ++b) {
+        const int64_t e = start[c][b], a = e - cn[b];
+        if (e - a < 2) continue;
+        std::fill(cnt.begin(), cnt.end(), 0);
+        for (int64_t t = a; t < e; ++t) cnt[mk[t]]++;
+        int64_t acc = a;
+        for (int64_t v = L1; v >= 0; --v) {  // descending m
+          const int64_t k = cnt[v];
+          cnt[v] = acc;
+          acc += k;
+        }
+        tmp.assign(sl.begin() + a, sl.begin() + e);
+        for (int64_t t = a; t < e; ++t) sl[cnt[mk[t]]++] = tmp[t - a];
+      }
+    }
+  }
+  for (auto& pc : plan) maybe_strip(ctx, pc, (int64_t)pc.slots.size(), -1);
+  return plan;
+}
+
+}  // namespace host
+}  // namespace dtwgpu
