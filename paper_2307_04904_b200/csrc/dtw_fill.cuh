@@ -58,6 +58,7 @@ struct KernelCfg {
   int TR = 2;   // Full family: rows per step (independent chains per lane)
   bool ring = false;  // Band family: y window in a shared-memory ring instead of registers
   int U = 1;          // ring variant: units per lane (independent cell chains per lane)
+  bool mp = true;     // Full family: some pair needs several strips (boundary column)
 };
 
 // Launches cfg over args on stream with `blocks` CTAs of kThreads threads.

@@ -190,8 +190,10 @@ struct FullRows {
 #define DTWG_FULL_BOUNDS __launch_bounds__(kThreads)
 #endif
 // Full family. TR rows per step (ILP TR), warp-uniform loops, multi-pass over column
-// strips of width G*R with a per-group boundary column between passes.
-template <int G, int R, int TR, bool MASK, class Ar>
+// strips of width G*R with a per-group boundary column between passes. MP = false: every
+// pair of the launch fits one strip (m <= G*R), so the boundary-column machinery and its
+// registers are compiled out (c3: 198 -> fewer registers per thread).
+template <int G, int R, int TR, bool MASK, class Ar, bool MP = true>
 __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
   using T = typename Ar::T;
   constexpr bool kF32 = sizeof(T) == 4;
@@ -213,8 +215,8 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
     const T* X = S + P.xoff;
     const T* Y = S + P.yoff;
     const int n = P.n, m = P.m, hw = P.hw;
-    const int npass_g = (m + W - 1) / W;
-    const int npass = __reduce_max_sync(kFull, npass_g);
+    const int npass_g = MP ? (m + W - 1) / W : 1;
+    const int npass = MP ? __reduce_max_sync(kFull, npass_g) : 1;
     int written_hi = 0;
     double result = 0.0;
 
@@ -249,8 +251,8 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
       const bool last_pass = pass == npass_g - 1;
       const bool hold = pvalid && last_pass && ((m - 1 - c0) / R) == gl;
       const int r_res = hold ? (m - 1 - c0) % R : -1;
-      const bool wb = pvalid && !last_pass && gl == G - 1;
-      const bool use_bnd = gl == 0 && pass > 0;
+      const bool wb = MP && pvalid && !last_pass && gl == G - 1;
+      const bool use_bnd = MP && gl == 0 && pass > 0;
 
       int r0 = rs - TR * gl;  // this lane's first row at step 0
       // Rows outside [1, n] read the zero guard around the packed series (never used).
@@ -259,7 +261,8 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
 #pragma unroll
       for (int t = 0; t < TR; ++t) {
         xq[t] = __ldg(X + (r0 + t - 1));
-        bq[t] = (use_bnd && r0 + t <= written_hi) ? bnd[r0 + t] : (double)Ar::inf();
+        if constexpr (MP) bq[t] = (use_bnd && r0 + t <= written_hi) ? bnd[r0 + t] : (double)Ar::inf();
+        else bq[t] = (double)Ar::inf();
       }
 
       for (int s = 0; s < nsteps; ++s, r0 += TR) {
@@ -268,9 +271,10 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
 #pragma unroll
         for (int t = 0; t < TR; ++t) {
           x[t] = xq[t];
-          b[t] = bq[t];
+          b[t] = MP ? bq[t] : (double)Ar::inf();  // single strip: column 0 is +inf
           xq[t] = __ldg(X + (r0 + TR + t - 1));
-          if (use_bnd) bq[t] = (r0 + TR + t <= written_hi) ? bnd[r0 + TR + t] : (double)Ar::inf();
+          if constexpr (MP)
+            if (use_bnd) bq[t] = (r0 + TR + t <= written_hi) ? bnd[r0 + TR + t] : (double)Ar::inf();
           L[t] = __shfl_up_sync(kFull, send[t], 1, G);
         }
         if constexpr (kF32) {

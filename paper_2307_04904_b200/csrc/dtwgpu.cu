@@ -186,7 +186,7 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
       continue;
     }
     const int64_t W = (int64_t)pc.cfg.G * pc.cfg.R;
-    const bool multipass = pc.cfg.family == Family::Full &&
+    const bool multipass = pc.cfg.family == Family::Full && pc.cfg.mp &&
                            (ctx->uniform ? (ctx->h_len[0] > W) : true);
     if (multipass && count > 0) {
       scratch_off[c] = scratch_total;
@@ -268,7 +268,9 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
                pc.cfg.kr >= 0 ? (",kr=" + std::to_string(pc.cfg.kr)).c_str() : "", pc.cfg.P,
                pc.cfg.ring ? ",ring" : "",
                pc.cfg.U > 1 ? (",U=" + std::to_string(pc.cfg.U)).c_str() : "");
-    if (pc.cfg.family != Family::Band) snprintf(krs, sizeof(krs), ",T=%d", pc.cfg.TR);
+    if (pc.cfg.family != Family::Band)
+      snprintf(krs, sizeof(krs), ",T=%d%s", pc.cfg.TR,
+               pc.cfg.family == Family::Full && !pc.cfg.mp ? ",1strip" : "");
     char cellsb[32] = "";
     if (pc.cells > 0) snprintf(cellsb, sizeof(cellsb), " cells=%.4g", pc.cells);
     snprintf(buf, sizeof(buf), "%s%s[G=%d,R=%d%s%s%s] pairs=%lld%s blocks=%lld(%d/SM)",

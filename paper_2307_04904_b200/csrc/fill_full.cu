@@ -4,14 +4,20 @@
 
 namespace dtwgpu {
 
-const void* full_kernel_ptr(int G, int R, int TR, bool mask, bool fp32) {
+const void* full_kernel_ptr(int G, int R, int TR, bool mask, bool fp32, bool mp) {
   using namespace kern;
-#define DTWG_F(g, r, tr)                                                          \
-  if (G == g && R == r && TR == tr) {                                             \
-    if (fp32) return mask ? (const void*)dtw_full_kernel<g, r, tr, true, F32>     \
-                          : (const void*)dtw_full_kernel<g, r, tr, false, F32>;   \
-    return mask ? (const void*)dtw_full_kernel<g, r, tr, true, F64>               \
-                : (const void*)dtw_full_kernel<g, r, tr, false, F64>;             \
+#define DTWG_F(g, r, tr)                                                                    \
+  if (G == g && R == r && TR == tr) {                                                       \
+    if (mp) {                                                                               \
+      if (fp32) return mask ? (const void*)dtw_full_kernel<g, r, tr, true, F32, true>       \
+                            : (const void*)dtw_full_kernel<g, r, tr, false, F32, true>;     \
+      return mask ? (const void*)dtw_full_kernel<g, r, tr, true, F64, true>                 \
+                  : (const void*)dtw_full_kernel<g, r, tr, false, F64, true>;               \
+    }                                                                                       \
+    if (fp32) return mask ? (const void*)dtw_full_kernel<g, r, tr, true, F32, false>        \
+                          : (const void*)dtw_full_kernel<g, r, tr, false, F32, false>;      \
+    return mask ? (const void*)dtw_full_kernel<g, r, tr, true, F64, false>                  \
+                : (const void*)dtw_full_kernel<g, r, tr, false, F64, false>;                \
   }
   DTWG_FULL_CFGS(DTWG_F)
 #undef DTWG_F

@@ -17,7 +17,7 @@
   X(16, 26, 3) X(32, 20, 3) X(32, 26, 3)
 
 namespace dtwgpu {
-const void* full_kernel_ptr(int G, int R, int TR, bool mask, bool fp32);
+const void* full_kernel_ptr(int G, int R, int TR, bool mask, bool fp32, bool mp);
 const void* band16_kernel_ptr(int R, int kr, int P, bool fp32);
 const void* band32_kernel_ptr(int R, int kr, int P, bool fp32);
 const void* ring_kernel_ptr(int G, int R, int kr, bool fp32);

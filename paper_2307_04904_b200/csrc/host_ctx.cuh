@@ -86,6 +86,7 @@ struct PlanClass {
   std::vector<int64_t> slots;  // empty + range mode when uniform
   double cost = 0;
   int64_t max_n = 0;
+  int64_t max_m = 0;  // longest shorter series: decides single- vs multi-strip Full kernels
   double cells = 0;  // in-band cells of the class (diagnostics: dtwg_last_plan)
   // Strip family: strips per pair (uniform) or prefix sums over `slots` (ragged)
   int strips_per_pair = 0;

@@ -226,6 +226,12 @@ void maybe_strip(dtwg_ctx* ctx, PlanClass& pc, int64_t count, int64_t m_uniform)
   pc.cfg = sc;
 }
 
+// Full classes whose every pair fits one strip (m <= G*R) use the single-strip kernels:
+// no boundary column, fewer registers (c1's G=32 R=16: 126 instead of 168, 4 CTAs/SM).
+void set_single_strip(PlanClass& pc) {
+  if (pc.cfg.family == Family::Full && pc.max_m <= (int64_t)pc.cfg.G * pc.cfg.R) pc.cfg.mp = false;
+}
+
 std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool fp32,
                                  int64_t sb, int64_t se) {
   std::vector<PlanClass> plan;
@@ -236,8 +242,10 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
     const Shape s = shape_of(ctx, 0, 1, hw, auto_widen);
     pc.cfg = choose_cfg(ctx, s, fp32, &pc.cost, se - sb);
     pc.max_n = s.n;
+    pc.max_m = s.m;
     plan.push_back(pc);
     maybe_strip(ctx, plan[0], se - sb, s.m);
+    set_single_strip(plan[0]);
     return plan;
   }
   // Ragged dataset: classify every pair by shape (memoised on (n, m)), then bucket the
@@ -308,6 +316,7 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
       if ((int64_t)counts[cls].size() <= bk) counts[cls].resize(bk + 1, 0);
       counts[cls][bk]++;
       plan[cls].max_n = std::max(plan[cls].max_n, s.n);
+      plan[cls].max_m = std::max(plan[cls].max_m, s.m);
       plan[cls].cost += double(s.n) * double(s.m);
       plan[cls].cells += double(pair_cells(s.n, s.m, s.hw));
       if (++j == p) {
@@ -371,7 +380,10 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
       }
     }
   }
-  for (auto& pc : plan) maybe_strip(ctx, pc, (int64_t)pc.slots.size(), -1);
+  for (auto& pc : plan) {
+    maybe_strip(ctx, pc, (int64_t)pc.slots.size(), -1);
+    set_single_strip(pc);
+  }
   return plan;
 }
 
