@@ -78,6 +78,7 @@ __device__ __forceinline__ void decode_slot(int64_t s, int64_t p, int64_t& i, in
 // ---- arithmetic policies ----------------------------------------------------------
 struct F64 {
   using T = double;
+  static constexpr bool kFp32 = false;
   static __device__ __forceinline__ T inf() { return CUDART_INF; }
   static __device__ __forceinline__ T mn(T a, T b) { return b < a ? b : a; }
   // (x - y)^2 + best, each op rounded separately (dtw.hpp:16-19, :69).
@@ -91,6 +92,7 @@ struct F64 {
 
 struct F32 {
   using T = float;
+  static constexpr bool kFp32 = true;
   static __device__ __forceinline__ T inf() { return CUDART_INF_F; }
   static __device__ __forceinline__ T mn(T a, T b) { return fminf(a, b); }
   static __device__ __forceinline__ T cell(T x, T y, T best) {
@@ -1118,8 +1120,14 @@ __device__ __forceinline__ void unit_steps(int nst, int& i1, const typename Ar::
 #ifndef DTWG_UNIT_MINB20
 #define DTWG_UNIT_MINB20 4
 #endif
+#ifdef DTWG_UNIT_MINB32_N
+#define DTWG_UNIT_MINB32(R) DTWG_UNIT_MINB32_N
+#else
+#define DTWG_UNIT_MINB32(R) DTWG_UNIT_MINB(R)
+#endif
 template <int G, int R, int U, int KR, class Ar>
-__global__ void __launch_bounds__(kThreads, DTWG_UNIT_MINB(R)) dtw_bandunit_kernel(const FillArgs A) {
+__global__ void __launch_bounds__(kThreads, Ar::kFp32 ? DTWG_UNIT_MINB32(R) : DTWG_UNIT_MINB(R))
+    dtw_bandunit_kernel(const FillArgs A) {
   static_assert(U >= 1 && R / U >= 2, "units need >= 2 columns");
   // ring slots: a power of two holding the group's window (G*(R-U)+1) plus one chunk ahead
   constexpr int RING = G * (R - U) <= 256 - 33 ? 256 : (G * (R - U) <= 512 - 33 ? 512 : 1024);

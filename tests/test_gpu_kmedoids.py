@@ -79,6 +79,17 @@ def test_observer_trace_matches_and_descends():
         assert all(b <= a for a, b in zip(costs, costs[1:]))
 
 
+def test_best_of_restarts_monotone():
+    """More restarts never raise the best cost (test_kmedoids.cpp:141-154): restart r's
+    stream does not depend on the restart count, and the best is kept by strict <."""
+    D = random_condensed(ScalarRng(31), 60)
+    m = DistanceMatrix.from_condensed(60, D)
+    costs = [kmedoids(m, KMedoidsConfig(k=5, restarts=r, seed=7)).total_cost
+             for r in range(1, 9)]
+    assert all(b <= a for a, b in zip(costs, costs[1:]))
+    assert costs[-1] == kref(D, 60, KMedoidsConfig(k=5, restarts=8, seed=7))[2]
+
+
 def test_duplicates_and_fixed_point():
     data = [TimeSeries(f"dup{i}", [1.0, 2.0, 3.0]) for i in range(6)]
     m = build_matrix(data, WarpWindow.unlimited(), 1)
