@@ -143,17 +143,44 @@ __device__ __forceinline__ Pair load_pair(const FillArgs& A, int64_t item) {
 // ===================================================================================
 // Full family: column strips, two rows per step, multi-pass, optional band mask.
 // ===================================================================================
-template <int R, int NR, bool MASK, class Ar>
+// Band edges in the Full family ("kill" semantics). With |i - j| <= hw, only ONE cell per
+// row and edge has to be forced to +inf: the cell just past the lower edge, (i, i-hw-1),
+// and the one just past the upper edge, (i, i+hw+1). Every other out-of-band cell then
+// comes out +inf by itself, because all three of its inputs are out-of-band cells of the
+// current or previous row (or the +inf column 0 / row rs-1 borders): left of the lower
+// kill cell the diag/up/left inputs lie left of the previous rows' kill cells, right of
+// the upper one they lie right of them. Moreover the kill cells' own inputs are known:
+// the lower kill cell's diag and left inputs are +inf and only `up` (the edge cell above)
+// is finite; the upper kill cell's diag and up inputs are +inf and only `left` is finite.
+// So in fp64 the kill folds into the two compares of the min: "take up" is ANDed with
+// "not the lower kill", "take left" with "not the upper kill" (DSETP with a predicate
+// operand), i.e. one integer compare per cell and edge instead of two compares and two
+// 64-bit selects per cell. KILL: bit 0 lower edge, bit 1 upper edge.
+// (b < a && k != C) ? b : a -- fp64; the kill test is the compare's predicate operand
+// (one ISETP + DSETP.LT.AND + 2 FSEL), which the compiler does not form from C++.
+__device__ __forceinline__ double min_unless(double a, double b, int k, int c) {
+  double r;
+  asm("{\n\t.reg .pred q, p;\n\t"
+      "setp.ne.s32 q, %3, %4;\n\t"
+      "setp.lt.and.f64 p, %2, %1, q;\n\t"
+      "selp.f64 %0, %2, %1, p;\n\t}"
+      : "=d"(r)
+      : "d"(a), "d"(b), "r"(k), "r"(c));
+  return r;
+}
+
+template <int R, int NR, int KILL, class Ar>
 struct FullRows {
   using T = typename Ar::T;
   // NR consecutive rows r0 .. r0+NR-1 of this lane's R-column strip. Row t's cell at
   // column r needs (row t-1, col r-1) [diag], (row t-1, col r) [up] and (row t, col r-1)
   // [left]; row -1 is the previous step's last row, held in pv. The unrolled NR x R
   // block is a 2-D wavefront, so the compiler interleaves NR independent chains (ILP NR).
-  // In: diag0 = (r0-1, jl-1); L[t] = (r0+t, jl-1) from lane l-1. Out: out[t] = (r0+t,
-  // last column); pv becomes row r0+NR-1.
+  // In: diag0 = (r0-1, jl-1); L[t] = (r0+t, jl-1) from lane l-1; klo = column (0-based in
+  // the strip) of row r0's lower kill cell, khi = of its upper kill cell (row t: +t).
+  // Out: out[t] = (r0+t, last column); pv becomes row r0+NR-1.
   static __device__ __forceinline__ void run(T (&pv)[R], const T (&yv)[R], const T (&x)[NR],
-                                             T diag0, const T (&L)[NR], int jl, int r0, int hw,
+                                             T diag0, const T (&L)[NR], int klo, int khi,
                                              T (&out)[NR]) {
     const T INF = Ar::inf();
     T d[NR], l[NR];
@@ -167,10 +194,17 @@ struct FullRows {
       T up = pv[r];
 #pragma unroll
       for (int t = 0; t < NR; ++t) {
-        T v = Ar::cell(x[t], yv[r], Ar::mn(Ar::mn(d[t], up), l[t]));
-        if (MASK) {
-          const int j = jl + r, i = r0 + t;
-          v = (j >= i - hw && j <= i + hw) ? v : INF;
+        T v;
+        if constexpr (KILL == 0) {
+          v = Ar::cell(x[t], yv[r], Ar::mn(Ar::mn(d[t], up), l[t]));
+        } else if constexpr (Ar::kFp32) {
+          v = Ar::cell(x[t], yv[r], Ar::mn(Ar::mn(d[t], up), l[t]));
+          const bool k = ((KILL & 1) && r - t == klo) || ((KILL & 2) && r - t == khi);
+          v = k ? INF : v;
+        } else {
+          const T m1 = (KILL & 1) ? min_unless(d[t], up, klo, r - t) : Ar::mn(d[t], up);
+          const T m = (KILL & 2) ? min_unless(m1, l[t], khi, r - t) : Ar::mn(m1, l[t]);
+          v = Ar::cell(x[t], yv[r], m);
         }
         d[t] = up;  // (t-1, r) is the diagonal of (t, r+1)
         l[t] = v;
@@ -182,6 +216,16 @@ struct FullRows {
     for (int t = 0; t < NR; ++t) out[t] = l[t];
   }
 };
+
+// Which kill edges a step of NR rows needs in this lane: bit 0 when a lower kill cell of
+// rows r0 .. r0+NR-1 falls in the lane's R columns, bit 1 for an upper one. klo/khi are
+// row r0's kill columns relative to the lane's first column; the kill columns move right
+// by one per row, so row t's are klo + t and khi + t.
+template <int R, int NR>
+__device__ __forceinline__ int kill_need(int klo, int khi) {
+  return ((klo <= R - 1 && klo + NR - 1 >= 0) ? 1 : 0) |
+         ((khi <= R - 1 && khi + NR - 1 >= 0) ? 2 : 0);
+}
 
 // Experiments only (-DDTWG_FULL_MINB_N=k caps the Full kernels' registers for k CTAs per
 // SM). The default passes no minimum: an explicit 1 lets ptxas take more registers
@@ -263,8 +307,9 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
 #pragma unroll
       for (int t = 0; t < TR; ++t) {
         xq[t] = __ldg(X + (r0 + t - 1));
-        if constexpr (MP) bq[t] = (use_bnd && r0 + t <= written_hi) ? bnd[r0 + t] : (double)Ar::inf();
-        else bq[t] = (double)Ar::inf();
+        bq[t] = (double)Ar::inf();
+        if constexpr (MP)
+          if (use_bnd) bq[t] = bnd[r0 + t];
       }
 
       for (int s = 0; s < nsteps; ++s, r0 += TR) {
@@ -275,8 +320,10 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
           x[t] = xq[t];
           b[t] = MP ? bq[t] : (double)Ar::inf();  // single strip: column 0 is +inf
           xq[t] = __ldg(X + (r0 + TR + t - 1));
+          // Rows past the previous pass's last row hold +inf (written at its end), so
+          // lane 0 loads its boundary rows unconditionally: a predicated load, no branch.
           if constexpr (MP)
-            if (use_bnd) bq[t] = (r0 + TR + t <= written_hi) ? bnd[r0 + TR + t] : (double)Ar::inf();
+            if (use_bnd) bq[t] = bnd[r0 + TR + t];
           L[t] = __shfl_up_sync(kFull, send[t], 1, G);
         }
         if constexpr (kF32) {
@@ -296,20 +343,25 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
           }
         }
         const bool work = s >= gl && r0 <= re;
-        bool fast = true;
+        // Band-edge kill cells of this step (see FullRows), warp-uniform variant choice.
+        const int klo = r0 - hw - 1 - jl, khi = r0 + hw + 1 - jl;
+        int need = 0;
         if (MASK) {
-          // All TR rows entirely inside |i-j| <= hw for every working lane of the warp?
-          const bool in = (jl >= r0 + TR - 1 - hw) && (jl + R - 1 <= r0 + hw);
-          fast = __all_sync(kFull, in || !work);
+          const int mine = work ? kill_need<R, TR>(klo, khi) : 0;
+          need = (__any_sync(kFull, mine & 1) ? 1 : 0) | (__any_sync(kFull, mine & 2) ? 2 : 0);
         }
         if (work) {
           T out[TR];
           const int nr = min(TR, re - r0 + 1);  // rows of this step inside [rs, re]
           if (nr == TR) {
-            if (!MASK || fast)
-              FullRows<R, TR, false, Ar>::run(pv, yv, x, diag0, L, jl, r0, hw, out);
+            if (need == 0)
+              FullRows<R, TR, 0, Ar>::run(pv, yv, x, diag0, L, klo, khi, out);
+            else if (need == 1)
+              FullRows<R, TR, 1, Ar>::run(pv, yv, x, diag0, L, klo, khi, out);
+            else if (need == 2)
+              FullRows<R, TR, 2, Ar>::run(pv, yv, x, diag0, L, klo, khi, out);
             else
-              FullRows<R, TR, MASK, Ar>::run(pv, yv, x, diag0, L, jl, r0, hw, out);
+              FullRows<R, TR, 3, Ar>::run(pv, yv, x, diag0, L, klo, khi, out);
             diag0 = L[TR - 1];
           } else {
             // Tail of the pass: the remaining rows one at a time.
@@ -319,7 +371,7 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
                 const T xt[1] = {x[t]};
                 const T Lt[1] = {L[t]};
                 T ot[1];
-                FullRows<R, 1, MASK, Ar>::run(pv, yv, xt, diag0, Lt, jl, r0 + t, hw, ot);
+                FullRows<R, 1, MASK ? 3 : 0, Ar>::run(pv, yv, xt, diag0, Lt, klo + t, khi + t, ot);
                 out[t] = ot[0];
                 diag0 = L[t];
               } else {
@@ -359,6 +411,12 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
             result = (double)rv + (kF32 ? off : 0.0);
           }
         }
+      }
+      if constexpr (MP && MASK) {
+        // The next pass ends at most W rows lower; its rows past this pass's last one
+        // lie outside the band at this pass's last column (+inf).
+        if (wb)
+          for (int r = re + 1; r <= min(n, re + W); ++r) bnd[r] = (double)INF;
       }
       written_hi = re;
       __syncwarp();
@@ -518,19 +576,24 @@ __global__ void __launch_bounds__(kThreads) dtw_strip_kernel(const FillArgs A) {
         }
       }
       const bool work = st >= gl && r0 <= re;
-      bool fast = true;
+      const int klo = r0 - hw - 1 - jl, khi = r0 + hw + 1 - jl;  // band-edge kill cells
+      int need = 0;
       if (MASK) {
-        const bool in = (jl >= r0 + TR - 1 - hw) && (jl + R - 1 <= r0 + hw);
-        fast = __all_sync(kFull, in || !work);
+        const int mine = work ? kill_need<R, TR>(klo, khi) : 0;
+        need = (__any_sync(kFull, mine & 1) ? 1 : 0) | (__any_sync(kFull, mine & 2) ? 2 : 0);
       }
       if (work) {
         T out[TR];
         const int nr = min(TR, re - r0 + 1);
         if (nr == TR) {
-          if (!MASK || fast)
-            FullRows<R, TR, false, Ar>::run(pv, yv, x, diag0, L, jl, r0, hw, out);
+          if (need == 0)
+            FullRows<R, TR, 0, Ar>::run(pv, yv, x, diag0, L, klo, khi, out);
+          else if (need == 1)
+            FullRows<R, TR, 1, Ar>::run(pv, yv, x, diag0, L, klo, khi, out);
+          else if (need == 2)
+            FullRows<R, TR, 2, Ar>::run(pv, yv, x, diag0, L, klo, khi, out);
           else
-            FullRows<R, TR, MASK, Ar>::run(pv, yv, x, diag0, L, jl, r0, hw, out);
+            FullRows<R, TR, 3, Ar>::run(pv, yv, x, diag0, L, klo, khi, out);
           diag0 = L[TR - 1];
         } else {
 #pragma unroll
@@ -539,7 +602,7 @@ __global__ void __launch_bounds__(kThreads) dtw_strip_kernel(const FillArgs A) {
               const T xt[1] = {x[t]};
               const T Lt[1] = {L[t]};
               T ot[1];
-              FullRows<R, 1, MASK, Ar>::run(pv, yv, xt, diag0, Lt, jl, r0 + t, hw, ot);
+              FullRows<R, 1, MASK ? 3 : 0, Ar>::run(pv, yv, xt, diag0, Lt, klo + t, khi + t, ot);
               out[t] = ot[0];
               diag0 = L[t];
             } else {

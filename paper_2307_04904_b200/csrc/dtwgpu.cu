@@ -19,6 +19,11 @@
 namespace dtwgpu {
 namespace host {
 
+// Rows of padding after each group's boundary column: lane 0 of a multi-pass Full group
+// prefetches its boundary rows unconditionally, up to TR * (G + 2) rows past the pair's
+// last row.
+constexpr int64_t kScratchPad = 160;
+
 // time_series.hpp:24-33 per-series checks (ids are the caller's; see dtwgpu.hpp).
 int validate_series(dtwg_ctx* ctx, const double* samples, const int64_t* offsets, int64_t p) {
   for (int64_t i = 0; i < p; ++i) {
@@ -190,7 +195,7 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
                            (ctx->uniform ? (ctx->h_len[0] > W) : true);
     if (multipass && count > 0) {
       scratch_off[c] = scratch_total;
-      scratch_total += (pc.max_n + 2) * blocks_of[c] * groups_per_block;
+      scratch_total += (pc.max_n + kScratchPad) * blocks_of[c] * groups_per_block;
     }
   }
   if (scratch_total) CU(ctx->d_scratch.reserve((size_t)scratch_total), "cudaMalloc scratch");
@@ -243,7 +248,7 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
     a.out = d_out;
     if (scratch_off[c] >= 0) {
       a.scratch = ctx->d_scratch.ptr + scratch_off[c];
-      a.scratch_stride = pc.max_n + 2;
+      a.scratch_stride = pc.max_n + kScratchPad;
     }
     if (ctx->exchange_open && d_out - out_base == ctx->d_cond.ptr) {  // resident, global slots
       a.n_peer = (int)ctx->peers.size();

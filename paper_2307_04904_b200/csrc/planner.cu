@@ -43,9 +43,15 @@ const Cand kBand[] = {{16, 7, 1500},    {16, 9, 1600},    {16, 11, 1700},  {16, 
 constexpr double kFp32Full = 2.15, kFp32Band = 1.45;
 
 // Masked Full fills: rows where the strip lies entirely inside the band run the plain
-// cell; rows crossing a band edge run the masked cell at 1.79x the cost (least-squares fit
+// cell; rows crossing a band edge ran the masked cell at 1.79x the cost (least-squares fit
 // over hw = 101..400 at n = m = 1000, tools: exp/band_rates.py, profiles/round1_sweep.md).
-constexpr double kMaskedRowCost = 1.79;
+// The kill-cell edges (dtw_kernels.cuh, FullRows) made those rows ~1.1x, but planning
+// with 1.1 moved 0.7 M c5 pairs into the masked Full class at no net gain (2214 against
+// 2210 ms), so the planner keeps the original weight.
+#ifndef DTWG_MASKED_ROW_COST
+#define DTWG_MASKED_ROW_COST 1.79
+#endif
+constexpr double kMaskedRowCost = DTWG_MASKED_ROW_COST;
 
 double full_cost(const Shape& s, const Cand& c, bool mask, bool fp32) {
   const int64_t W = (int64_t)c.G * c.R;
