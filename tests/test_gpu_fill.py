@@ -151,6 +151,24 @@ def test_full_family_every_instantiation(eng, G, R, fam, fp32):
             assert_bitwise(got, want, f"full G={G} R={R} hw={hw}")
 
 
+@pytest.mark.parametrize("G,R,fam", [(4, 12, 0), (4, 12, 3), (2, 23, 3), (8, 8, 0), (32, 4, 0),
+                                     (32, 15, 3)])
+def test_full_family_band_edge_kill_cells(eng, G, R, fam):
+    """Banded Full fills force only the cell just past each band edge per row to +inf (the
+    rest of the out-of-band region comes out +inf by itself, dtw_kernels.cuh FullRows):
+    narrow bands where both kill cells sit in one lane's strip (2hw+2 < R), bands around
+    the strip width, equal and near-equal lengths (no auto-widening), multi-pass pairs."""
+    W = G * R
+    lengths = [1, 2, 5, W - 1, W, W + 1, 2 * W + 3, 150, 150, 151, 300, 301, 303]
+    samples, offsets = _walks(4242 + G * R, lengths)
+    for hw in (0, 1, 2, 5, R - 1, R, W // 2, W - 1, W, W + 1, 149):
+        eng.force_kernel(fam, G, R)
+        got = eng.build_condensed(samples, offsets, hw, True)
+        assert f"full[G={G},R={R}" in eng.last_plan(), eng.last_plan()
+        want = oracle.build_condensed(samples, offsets, hw, True)
+        assert_bitwise(got, want, f"full G={G} R={R} fam={fam} hw={hw}")
+
+
 RING = [(8, 16), (8, 26), (16, 8), (16, 14), (32, 6)]
 UNIT = [(8, 26, 3), (8, 26, 5), (16, 14, 3), (16, 13, 2), (16, 20, 3), (16, 26, 3), (32, 20, 3),
         (32, 26, 3)]  # ring with U units per lane

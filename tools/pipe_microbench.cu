@@ -7,6 +7,7 @@
 //   cell_lds : cell body + one LDS.64 per cell  (as the ring kernels)
 //   cell_int : cell with both mins done on the integer pipe (non-negative doubles order
 //              like their int64 bit patterns): 3 fp64 + 4 ISETP + 4 SEL
+//   cell_mix : one min on the integer pipe, one DSETP: 4 fp64 + 2 ISETP + 4 SEL
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o pipe_microbench pipe_microbench.cu
 #include <cuda_runtime.h>
 
@@ -54,6 +55,10 @@ __global__ void bench(const double* in, double* out, int iters) {
         const double d = __dsub_rn(x, yy);
         double m;
         if constexpr (MODE == 5) m = imin(imin(a[c], b[c]), y[c]);
+        else if constexpr (MODE == 6) {
+          const double m1 = imin(a[c], b[c]);
+          m = y[c] < m1 ? y[c] : m1;
+        }
         else {
           const double m1 = b[c] < a[c] ? b[c] : a[c];
           m = y[c] < m1 ? y[c] : m1;
@@ -110,5 +115,6 @@ int main() {
   run<3>("cell", 1, "warp_cell");
   run<4>("cell_lds", 1, "warp_cell");
   run<5>("cell_int", 1, "warp_cell");
+  run<6>("cell_mix", 1, "warp_cell");
   return 0;
 }
