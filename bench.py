@@ -103,6 +103,17 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU arms
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference_sample(ds, budget_s: float):
     """Time the reference's build_matrix (oracle/_ref, all host threads) on the first q
     series of the workload, q sized for ~budget_s of CPU work. Falls back to the C
@@ -129,7 +140,7 @@ def cpu_reference_sample(ds, budget_s: float):
         oracle.build_condensed(sub.samples, sub.offsets, sub.half_width, sub.auto_widen)
     dt = time.perf_counter() - t0
     return {"value": cells / dt / 1e9, "unit": UNIT, "cores": cores if kind == "reference" else 1,
-            "kind": kind,
+            "kind": kind, "cpu_model": _cpu_model(),
             "sample": f"first {q} series of {ds.name} ({q * (q - 1) // 2} of {total_pairs} pairs, "
                       f"{cells:.3e} cells, {dt:.2f} s)",
             "seconds": dt, "cells": cells}
@@ -370,9 +381,19 @@ def run_gpu_arm(a, ds):
                 "assign_kernel": {"ms": st["assign_ms"], "algorithmic_bytes": st["assign_bytes"],
                                   "achieved_gbs": st["assign_bytes"] / max(st["assign_ms"], 1e-9) / 1e6}}
         if rank == 0 and a.check and p <= 5000:
+            # Parity against the reference's own kmedoids (oracle/_ref; the C restatement
+            # when it was not built), timed: its single-threaded restart loop over the same
+            # host matrix is the k-medoids CPU baseline.
             import oracle
             D = eng.download(p) if exchange == "p2p" else cond.cpu().numpy()
-            med, asg, cost = oracle.kmedoids(D, p, ds.k, ds.restarts, 100, 0)
+            km_kind = "reference" if oracle.have_ref() else "port"
+            t1 = time.perf_counter()
+            if km_kind == "reference":
+                med, asg, cost = oracle.ref_kmedoids(D, p, ds.k, ds.restarts, 100, 0)
+            else:
+                med, asg, cost = oracle.kmedoids(D, p, ds.k, ds.restarts, 100, 0)
+            kmed["cpu_baseline"] = {"seconds": time.perf_counter() - t1, "kind": km_kind,
+                                    "cores": 1, "sample": "the whole k-medoids run"}
             kmed["parity"] = bool(list(med) == list(best[2]) and list(asg) == list(best[3])
                                   and cost == best[0])
 
