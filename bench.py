@@ -103,6 +103,25 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU arms
+def _copy_ms(src, dst) -> float:
+    """One copy of `src` to `dst` ("cpu": pinned host), timed with CUDA events (best of 3)."""
+    import torch
+
+    if dst == "cpu":
+        out = torch.empty(src.shape, dtype=src.dtype).pin_memory()
+    else:
+        out = torch.empty(src.shape, dtype=src.dtype, device=dst)
+    best = float("inf")
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out.copy_(src, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    return best
+
+
 def _cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -350,6 +369,14 @@ def run_gpu_arm(a, ds):
         e2e = {"value": all_cells * a.steps / dt / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(ds.samples.nbytes + ds.offsets.nbytes),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": dt / a.steps * 1e3}
+        if world == 1:
+            # The parts of a call: the last call's fill on the device, and
+            # standalone pinned copies of its inputs and its matrix (inside the call the
+            # D2H is streamed behind the fill and the host checks overlap the H2D).
+            e2e["fill_ms"] = float(eng.last_fill_ms())
+            e2e["h2d_ms"] = _copy_ms(pin_s, dev) + _copy_ms(pin_o, dev)
+            e2e["d2h_ms"] = _copy_ms(torch.empty(int(d2h) // 8, dtype=torch.float64, device=dev),
+                                     "cpu")
 
     # k-medoids sweeps over the device-resident matrix (the second hot loop), restarts
     # sharded over ranks and reduced in restart order.

@@ -387,9 +387,9 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
               if (mnv != INF) {
 #pragma unroll
                 for (int r = 0; r < R; ++r) pv[r] = __fsub_rn(pv[r], mnv);
-                diag0 = (diag0 == INF) ? INF : __fsub_rn(diag0, mnv);
+                diag0 = __fsub_rn(diag0, mnv);  // +inf stays +inf (mnv finite)
 #pragma unroll
-                for (int t = 0; t < TR; ++t) out[t] = (out[t] == INF) ? INF : __fsub_rn(out[t], mnv);
+                for (int t = 0; t < TR; ++t) out[t] = __fsub_rn(out[t], mnv);
                 off += (double)mnv;
               }
             }
@@ -399,7 +399,7 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
           for (int t = 0; t < TR; ++t) {
             send[t] = out[t];
             if (wb && t < nr) {
-              if constexpr (kF32) bnd[r0 + t] = (out[t] == INF) ? (double)INF : (double)out[t] + off;
+              if constexpr (kF32) bnd[r0 + t] = (double)out[t] + off;  // +inf + off = +inf
               else bnd[r0 + t] = out[t];
             }
           }
@@ -618,9 +618,9 @@ __global__ void __launch_bounds__(kThreads) dtw_strip_kernel(const FillArgs A) {
             if (mnv != INF) {
 #pragma unroll
               for (int r = 0; r < R; ++r) pv[r] = __fsub_rn(pv[r], mnv);
-              diag0 = (diag0 == INF) ? INF : __fsub_rn(diag0, mnv);
+              diag0 = __fsub_rn(diag0, mnv);  // +inf stays +inf (mnv finite)
 #pragma unroll
-              for (int t = 0; t < TR; ++t) out[t] = (out[t] == INF) ? INF : __fsub_rn(out[t], mnv);
+              for (int t = 0; t < TR; ++t) out[t] = __fsub_rn(out[t], mnv);
               off += (double)mnv;
             }
           }
@@ -630,7 +630,7 @@ __global__ void __launch_bounds__(kThreads) dtw_strip_kernel(const FillArgs A) {
         for (int t = 0; t < TR; ++t) {
           send[t] = out[t];
           if (wb && t < nr) {
-            if constexpr (kF32) bout[r0 + t] = (out[t] == INF) ? (double)INF : (double)out[t] + off;
+            if constexpr (kF32) bout[r0 + t] = (double)out[t] + off;  // +inf + off = +inf
             else bout[r0 + t] = out[t];
           }
         }
