@@ -21,6 +21,15 @@ const void* full_kernel_ptr(int G, int R, int TR, bool mask, bool fp32, bool mp)
   }
   DTWG_FULL_CFGS(DTWG_F)
 #undef DTWG_F
+#define DTWG_F32(g, r, tr)                                                                  \
+  if (fp32 && G == g && R == r && TR == tr) {                                               \
+    if (mp) return mask ? (const void*)dtw_full_kernel<g, r, tr, true, F32, true>           \
+                        : (const void*)dtw_full_kernel<g, r, tr, false, F32, true>;         \
+    return mask ? (const void*)dtw_full_kernel<g, r, tr, true, F32, false>                  \
+                : (const void*)dtw_full_kernel<g, r, tr, false, F32, false>;                \
+  }
+  DTWG_FULL_CFGS_F32(DTWG_F32)
+#undef DTWG_F32
   return nullptr;
 }
 

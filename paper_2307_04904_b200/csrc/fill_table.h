@@ -6,6 +6,9 @@
   X(2, 23, 2) X(4, 12, 2) X(8, 8, 2) X(16, 8, 2) X(16, 16, 2) X(32, 4, 2) X(32, 8, 2)    \
   X(32, 12, 2) X(32, 15, 2) X(32, 16, 2) X(2, 23, 4) X(4, 12, 4) X(8, 8, 4) X(16, 16, 4) \
   X(32, 15, 4) X(32, 16, 4)
+// Full family, fp32 only (wide strips: half the per-row overhead per cell; the fp64
+// instantiation would need > 255 registers)
+#define DTWG_FULL_CFGS_F32(X) X(16, 30, 4)
 #define DTWG_BAND_CFGS_G16(X) X(16, 7) X(16, 9) X(16, 11) X(16, 13)
 #define DTWG_BAND_CFGS_G32(X) X(32, 3) X(32, 5) X(32, 7) X(32, 9) X(32, 13)
 // Band family, shared-memory y ring variant

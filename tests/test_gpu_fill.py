@@ -151,6 +151,26 @@ def test_full_family_every_instantiation(eng, G, R, fam, fp32):
             assert_bitwise(got, want, f"full G={G} R={R} hw={hw}")
 
 
+def test_full_family_fp32_only_instantiations(eng):
+    """fp32-only Full instantiations (fill_table.h DTWG_FULL_CFGS_F32): every mask/pass
+    variant within the fp32 tolerance; fp64 requests fall back to the planner."""
+    G, R = 16, 30
+    rng = np.random.default_rng(1630)
+    lengths = rng.integers(1, 1100, size=12)
+    lengths[:3] = [1, G * R, G * R + 1]
+    samples, offsets = _walks(1630, lengths)
+    for hw, aw in ((-1, False), (40, True), (3, True)):
+        eng.force_kernel(3, G, R)
+        got = eng.build_condensed(samples, offsets, hw, aw, precision=1)
+        assert f"full[G={G},R={R}" in eng.last_plan(), eng.last_plan()
+        want = oracle.build_condensed(samples, offsets, hw, aw)
+        np.testing.assert_allclose(got, want, rtol=1e-5, atol=0)
+        eng.force_kernel(3, G, R)
+        got64 = eng.build_condensed(samples, offsets, hw, aw, precision=0)
+        assert f"full[G={G},R={R}" not in eng.last_plan(), eng.last_plan()
+        assert_bitwise(got64, want, f"fp64 fallback hw={hw}")
+
+
 @pytest.mark.parametrize("G,R,fam", [(4, 12, 0), (4, 12, 3), (2, 23, 3), (8, 8, 0), (32, 4, 0),
                                      (32, 15, 3)])
 def test_full_family_band_edge_kill_cells(eng, G, R, fam):
@@ -392,9 +412,11 @@ def test_full_size_matrix_bitwise_vs_reference(eng, cfg, q):
     assert_bitwise(got, want, f"c{cfg} (p={ds.p}) plan={plan[:200]}")
 
 
-@pytest.mark.parametrize("cfg,expect", [(1, "full[G=32,R=16"), (2, "band[G=8,R=26,kr=19,P=1,ring,U=3]"),
-                                        (4, "full[G=32,R=15,T=4]")])
-def test_planner_picks_the_measured_best(eng, cfg, expect):
+@pytest.mark.parametrize("cfg,prec,expect", [(1, 0, "full[G=32,R=16"),
+                                             (2, 0, "band[G=8,R=26,kr=19,P=1,ring,U=3]"),
+                                             (4, 0, "full[G=32,R=15,T=4]"),
+                                             (4, 1, "full[G=16,R=30,fp32,T=4]")])
+def test_planner_picks_the_measured_best(eng, cfg, prec, expect):
     """The cost model's choices on the benchmark configs (profiles/round1_*: the sweeps
     that calibrated it); guards against a model change silently regressing a config."""
     ds = gen.make_config(cfg)
@@ -402,7 +424,7 @@ def test_planner_picks_the_measured_best(eng, cfg, expect):
     p = ds.p
     import torch
     out = torch.empty(p * (p - 1) // 2, dtype=torch.float64, device="cuda")
-    eng.fill_slots(ds.half_width, ds.auto_widen, 0, 0, p * (p - 1) // 2, out.data_ptr())
+    eng.fill_slots(ds.half_width, ds.auto_widen, prec, 0, p * (p - 1) // 2, out.data_ptr())
     assert expect in eng.last_plan(), eng.last_plan()
 
 
