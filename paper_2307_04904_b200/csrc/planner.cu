@@ -27,7 +27,10 @@ const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026}
                       {32, 15, 2000},        {32, 15, 2150, 1, 4}, {32, 16, 2100},
                       {32, 16, 2050, 1, 4},
                       // fp32 only: c4 fp32 5340 GCUPS against 4598 for (32, 15, 4)
-                      {16, 30, 2570, 1, 4, false, 1, true}};
+                      {16, 30, 2570, 1, 4, false, 1, true},
+                      // fp32 only, one lane per pair (no shuffles, no wavefront fill/drain),
+                      // single strip only (m <= 46): c3 fp32 5649 against 4403 for (2, 23, 4)
+                      {1, 46, 2740, 1, 4, false, 1, true}};
 const Cand kBand[] = {{16, 7, 1500},    {16, 9, 1600},    {16, 11, 1700},  {16, 13, 1800},
                       {32, 3, 1000},    {32, 5, 1250},    {32, 7, 1490},   {32, 9, 1500},
                       {32, 13, 1450},   {32, 3, 600, 2},  {32, 5, 600, 2},  {32, 7, 700, 2},
@@ -120,6 +123,7 @@ KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out, int64_t 
   const bool mask = s.hw < s.n - 1;  // a band that excludes some cell
   for (const Cand& c : kFull) {
     if (c.f32_only && !fp32) continue;
+    if (c.G == 1 && s.m > c.R) continue;  // one lane per pair: single strip only
     const double cst = full_cost(s, c, mask, fp32) / fill_factor(count, c.G, sms);
     if (cst < bc) {
       bc = cst;

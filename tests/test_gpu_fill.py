@@ -151,14 +151,15 @@ def test_full_family_every_instantiation(eng, G, R, fam, fp32):
             assert_bitwise(got, want, f"full G={G} R={R} hw={hw}")
 
 
-def test_full_family_fp32_only_instantiations(eng):
+@pytest.mark.parametrize("G,R,maxlen", [(16, 30, 1100), (1, 46, 200)])
+def test_full_family_fp32_only_instantiations(eng, G, R, maxlen):
     """fp32-only Full instantiations (fill_table.h DTWG_FULL_CFGS_F32): every mask/pass
-    variant within the fp32 tolerance; fp64 requests fall back to the planner."""
-    G, R = 16, 30
-    rng = np.random.default_rng(1630)
-    lengths = rng.integers(1, 1100, size=12)
+    variant within the fp32 tolerance (G = 1: one lane per pair, multi-pass when forced);
+    fp64 requests fall back to the planner."""
+    rng = np.random.default_rng(1630 + G)
+    lengths = rng.integers(1, maxlen, size=12)
     lengths[:3] = [1, G * R, G * R + 1]
-    samples, offsets = _walks(1630, lengths)
+    samples, offsets = _walks(1630 + G, lengths)
     for hw, aw in ((-1, False), (40, True), (3, True)):
         eng.force_kernel(3, G, R)
         got = eng.build_condensed(samples, offsets, hw, aw, precision=1)
@@ -415,7 +416,8 @@ def test_full_size_matrix_bitwise_vs_reference(eng, cfg, q):
 @pytest.mark.parametrize("cfg,prec,expect", [(1, 0, "full[G=32,R=16"),
                                              (2, 0, "band[G=8,R=26,kr=19,P=1,ring,U=3]"),
                                              (4, 0, "full[G=32,R=15,T=4]"),
-                                             (4, 1, "full[G=16,R=30,fp32,T=4]")])
+                                             (4, 1, "full[G=16,R=30,fp32,T=4]"),
+                                             (3, 1, "full[G=1,R=46,fp32,T=4,1strip]")])
 def test_planner_picks_the_measured_best(eng, cfg, prec, expect):
     """The cost model's choices on the benchmark configs (profiles/round1_*: the sweeps
     that calibrated it); guards against a model change silently regressing a config."""
