@@ -19,6 +19,8 @@ struct Cand {
   bool ring = false;  // band family: shared-memory y ring
   int U = 1;          // ring variant: units per lane
   bool f32_only = false;  // full family: instantiated for fp32 only (fill_table.h)
+  bool mp_rate = false;   // full family: rate measured on multi-pass shapes (no penalty)
+  bool f64_only = false;  // full family: planned for fp64 only
 };
 const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026},
                       {4, 12, 1956, 1, 4},   {8, 8, 1804},         {8, 8, 1700, 1, 4},
@@ -26,6 +28,11 @@ const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026}
                       {32, 4, 1300},         {32, 8, 1650},        {32, 12, 1950},
                       {32, 15, 2000},        {32, 15, 2150, 1, 4}, {32, 16, 2100},
                       {32, 16, 2050, 1, 4},
+                      // narrow masked strips for wide auto-widened bands (W = 32: 1.08x the
+                      // in-band cells against 1.12x at W = 48), rate measured on c5's
+                      // multi-pass shapes directly: c5 1795 -> 1829 GCUPS (fp32 c5 prefers
+                      // 23-column lanes: 3770 against 3624 with this candidate)
+                      {2, 16, 2000, 1, 4, false, 1, false, true, true},
                       // fp32 only: c4 fp32 5340 GCUPS against 4598 for (32, 15, 4)
                       {16, 30, 2570, 1, 4, false, 1, true},
                       // fp32 only, one lane per pair (no shuffles, no wavefront fill/drain),
@@ -82,10 +89,11 @@ double full_cost(const Shape& s, const Cand& c, bool mask, bool fp32) {
     cells += (eff_rows + c.TR * (c.G - 1)) * double(W);
   }
   double rate = c.rate * (fp32 ? kFp32Full : 1.0);
-  if (npass > 1) {  // boundary-column round trips per pass (measured on c4)
-    // The per-group boundary columns stay in L2 up to ~n = 1500 (c5, L = 1000 sweeps);
-    // the c4-measured penalties apply beyond.
-    const bool l2_resident = s.n <= 1500;
+  // The per-group boundary columns stay in L2 up to ~n = 1500 (c5, L = 1000 sweeps);
+  // the c4-measured penalties apply beyond. Rates measured on multi-pass c5 shapes
+  // (mp_rate) already include the L2-resident boundary traffic.
+  const bool l2_resident = s.n <= 1500;
+  if (npass > 1 && !(c.mp_rate && l2_resident)) {  // boundary-column round trips per pass
     // fp32 with L2-resident boundary columns pays no G = 2 penalty: its 4-instruction cell
     // gains most from the 23-column lanes (c5 fp32 3359 -> 3773 GCUPS; fp64 1795 -> 1670).
     if (c.G == 2) rate *= (c.TR == 4 && l2_resident && fp32) ? 1.0 : (c.TR == 4 ? 0.68 : 0.59);
@@ -122,7 +130,7 @@ KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out, int64_t 
   double bc = 1e300;
   const bool mask = s.hw < s.n - 1;  // a band that excludes some cell
   for (const Cand& c : kFull) {
-    if (c.f32_only && !fp32) continue;
+    if ((c.f32_only && !fp32) || (c.f64_only && fp32)) continue;
     if (c.G == 1 && s.m > c.R) continue;  // one lane per pair: single strip only
     const double cst = full_cost(s, c, mask, fp32) / fill_factor(count, c.G, sms);
     if (cst < bc) {

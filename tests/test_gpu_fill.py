@@ -129,7 +129,7 @@ def _walks(seed, lengths):
     return pack(rows)
 
 
-FULL4 = [(2, 23), (4, 12), (8, 8), (16, 16), (32, 15), (32, 16)]
+FULL4 = [(2, 23), (4, 12), (8, 8), (16, 16), (32, 15), (32, 16), (2, 16)]
 
 
 @pytest.mark.parametrize("G,R,fam", [(g, r, 0) for g, r in FULL] + [(g, r, 3) for g, r in FULL4])
