@@ -179,7 +179,10 @@ struct FullRows {
   // In: diag0 = (r0-1, jl-1); L[t] = (r0+t, jl-1) from lane l-1; klo = column (0-based in
   // the strip) of row r0's lower kill cell, khi = of its upper kill cell (row t: +t).
   // Out: out[t] = (r0+t, last column); pv becomes row r0+NR-1.
-  static __device__ __forceinline__ void run(T (&pv)[R], const T (&yv)[R], const T (&x)[NR],
+  // yv: the strip's R y samples -- a register array, or a pointer into shared memory
+  // (dtw_lane_kernel), indexed with compile-time offsets either way.
+  template <class YV>
+  static __device__ __forceinline__ void run(T (&pv)[R], const YV& yv, const T (&x)[NR],
                                              T diag0, const T (&L)[NR], int klo, int khi,
                                              T (&out)[NR]) {
     const T INF = Ar::inf();
@@ -423,6 +426,98 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
     }
     const int last_c0 = (npass_g - 1) * W;
     if (valid && ((m - 1 - last_c0) / R) == gl) store_result(A, P.slot, result);
+  }
+}
+
+// ===================================================================================
+// One lane per pair (fp64, single strip: m <= R). The Full family with G = 1, except
+// that the pair's R y samples live in shared memory (a lane's 2R row registers do not fit
+// in fp64): each lane stages its own y once per pair and reads it with immediate-offset
+// LDS, one per cell. No neighbour shuffles, no boundary column and no wavefront
+// fill/drain: each pair's rows run back to back (c3: 1.0x the in-band cells computed
+// instead of 1.09x for G = 2). Lanes of a warp run their own pairs in lockstep up to the
+// warp's longest pair; band edges use the Full family's kill cells.
+// ===================================================================================
+template <int R, int TR, bool MASK, class Ar>
+__global__ void __launch_bounds__(kThreads) dtw_lane_kernel(const FillArgs A) {
+  using T = typename Ar::T;
+  constexpr int YS = (R % 2) ? R : R + 1;  // odd stride (doubles): conflict-free LDS.64
+  __shared__ T ysm[kThreads * YS];
+  // volatile: one LDS per cell, not hoisted into (2R more) registers
+  volatile T* ys = ysm + threadIdx.x * YS;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const T INF = Ar::inf();
+  const T* S = Ar::base(A);
+  const int64_t base0 = tid - (threadIdx.x & 31);  // the warp's first item
+
+  for (int64_t base = base0; base < A.count; base += nthreads) {
+    const int64_t item = base + (threadIdx.x & 31);
+    const bool valid = item < A.count;
+    const Pair P = load_pair(A, valid ? item : base);
+    const T* X = S + P.xoff;
+    const T* Y = S + P.yoff;
+    const int n = valid ? P.n : 0, m = P.m, hw = P.hw;
+#pragma unroll
+    for (int r = 0; r < R; ++r) ys[r] = (r < m) ? __ldg(Y + r) : T(0);  // this lane's own
+    T pv[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) pv[r] = INF;
+    T diag0 = T(0);  // cell (0, 0); column 0 is +inf below it
+    T L[TR];
+#pragma unroll
+    for (int t = 0; t < TR; ++t) L[t] = INF;
+    const int rows = __reduce_max_sync(kFull, n);
+    double result = 0.0;
+    T xq[TR];
+#pragma unroll
+    for (int t = 0; t < TR; ++t) xq[t] = __ldg(X + t);
+    for (int r0 = 1; r0 <= rows; r0 += TR) {
+      T x[TR];
+#pragma unroll
+      for (int t = 0; t < TR; ++t) {
+        x[t] = xq[t];
+        xq[t] = __ldg(X + (r0 + TR + t - 1));  // rows past n read the zero guard (unused)
+      }
+      const int klo = r0 - hw - 2, khi = r0 + hw;  // kill columns of row r0, 0-based
+      int need = 0;
+      if (MASK) {
+        const int mine = (r0 <= n) ? kill_need<R, TR>(klo, khi) : 0;
+        need = (__any_sync(kFull, mine & 1) ? 1 : 0) | (__any_sync(kFull, mine & 2) ? 2 : 0);
+      }
+      T out[TR];
+      if (r0 + TR - 1 <= n) {
+        if (need == 0) FullRows<R, TR, 0, Ar>::run(pv, ys, x, diag0, L, klo, khi, out);
+        else if (need == 1) FullRows<R, TR, 1, Ar>::run(pv, ys, x, diag0, L, klo, khi, out);
+        else if (need == 2) FullRows<R, TR, 2, Ar>::run(pv, ys, x, diag0, L, klo, khi, out);
+        else FullRows<R, TR, 3, Ar>::run(pv, ys, x, diag0, L, klo, khi, out);
+        if (r0 + TR - 1 == n) {
+          T rv = pv[0];
+#pragma unroll
+          for (int r = 1; r < R; ++r) rv = (r == m - 1) ? pv[r] : rv;
+          result = (double)rv;
+        }
+      } else if (r0 <= n) {
+        // The pair's last n - r0 + 1 < TR rows, one at a time.
+        T dg = diag0;
+#pragma unroll
+        for (int t = 0; t < TR - 1; ++t) {
+          if (r0 + t <= n) {
+            const T xt[1] = {x[t]};
+            const T Lt[1] = {INF};
+            T ot[1];
+            FullRows<R, 1, MASK ? 3 : 0, Ar>::run(pv, ys, xt, dg, Lt, klo + t, khi + t, ot);
+            dg = INF;
+          }
+        }
+        T rv = pv[0];
+#pragma unroll
+        for (int r = 1; r < R; ++r) rv = (r == m - 1) ? pv[r] : rv;
+        result = (double)rv;
+      }
+      diag0 = INF;  // column 0 below row 0
+    }
+    if (valid) store_result(A, P.slot, result);
   }
 }
 

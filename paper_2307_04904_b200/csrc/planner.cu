@@ -37,7 +37,10 @@ const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026}
                       {16, 30, 2570, 1, 4, false, 1, true},
                       // fp32 only, one lane per pair (no shuffles, no wavefront fill/drain),
                       // single strip only (m <= 46): c3 fp32 5649 against 4403 for (2, 23, 4)
-                      {1, 46, 2740, 1, 4, false, 1, true}};
+                      {1, 46, 2740, 1, 4, false, 1, true},
+                      // fp64: one lane per pair, y in shared memory (dtw_lane_kernel),
+                      // single strip only: c3 2041 -> 2278 GCUPS
+                      {1, 46, 2270, 1, 2, false, 1, false, false, true}};
 const Cand kBand[] = {{16, 7, 1500},    {16, 9, 1600},    {16, 11, 1700},  {16, 13, 1800},
                       {32, 3, 1000},    {32, 5, 1250},    {32, 7, 1490},   {32, 9, 1500},
                       {32, 13, 1450},   {32, 3, 600, 2},  {32, 5, 600, 2},  {32, 7, 700, 2},
@@ -180,7 +183,7 @@ KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cos
                 (band && (!fp32 || ff > 10) && ctx->force_R > 0) ? (int)((2 * s.hw + 1) % ctx->force_R)
                                                                   : -1,
                 ff == 2 ? 2 : 1, ff == 3 ? 4 : 2, ff == 4 || ff > 10, ff > 10 ? ff - 10 : 1};
-    const bool ok = dtwgpu::fill_cfg_supported(f) &&
+    const bool ok = dtwgpu::fill_cfg_supported(f) && (f.G > 1 || s.m <= f.R) &&
                     (f.family == Family::Full ||
                      (mask && f.R >= 2 && (int64_t)f.G * f.R >= 2 * s.hw + 1));
     if (ok) {

@@ -168,7 +168,7 @@ def test_full_family_fp32_only_instantiations(eng, G, R, maxlen):
         np.testing.assert_allclose(got, want, rtol=1e-5, atol=0)
         eng.force_kernel(3, G, R)
         got64 = eng.build_condensed(samples, offsets, hw, aw, precision=0)
-        assert f"full[G={G},R={R}" not in eng.last_plan(), eng.last_plan()
+        assert f"full[G={G},R={R},T=4" not in eng.last_plan(), eng.last_plan()
         assert_bitwise(got64, want, f"fp64 fallback hw={hw}")
 
 
@@ -413,11 +413,32 @@ def test_full_size_matrix_bitwise_vs_reference(eng, cfg, q):
     assert_bitwise(got, want, f"c{cfg} (p={ds.p}) plan={plan[:200]}")
 
 
+@pytest.mark.parametrize("fp32", [False, True])
+def test_one_lane_per_pair_kernels(eng, fp32):
+    """One lane per pair (fp64: dtw_lane_kernel, y in shared memory; fp32: the Full
+    family with G = 1): ragged lengths up to the strip width, unlimited, banded (kill
+    cells) and auto-widened windows, pairs shorter than a row step; bit-exact in fp64."""
+    rng = np.random.default_rng(46)
+    lengths = rng.integers(1, 47, size=40)
+    lengths[:6] = [1, 2, 3, 45, 46, 46]
+    samples, offsets = _walks(4646, lengths)
+    for hw, aw in ((-1, False), (0, True), (1, True), (5, True), (20, True), (45, True)):
+        eng.force_kernel(3 if fp32 else 0, 1, 46)
+        got = eng.build_condensed(samples, offsets, hw, aw, precision=1 if fp32 else 0)
+        assert "full[G=1,R=46" in eng.last_plan(), eng.last_plan()
+        want = oracle.build_condensed(samples, offsets, hw, aw)
+        if fp32:
+            np.testing.assert_allclose(got, want, rtol=1e-5, atol=0)
+        else:
+            assert_bitwise(got, want, f"lane kernel hw={hw}")
+
+
 @pytest.mark.parametrize("cfg,prec,expect", [(1, 0, "full[G=32,R=16"),
                                              (2, 0, "band[G=8,R=26,kr=19,P=1,ring,U=3]"),
                                              (4, 0, "full[G=32,R=15,T=4]"),
                                              (4, 1, "full[G=16,R=30,fp32,T=4]"),
-                                             (3, 1, "full[G=1,R=46,fp32,T=4,1strip]")])
+                                             (3, 1, "full[G=1,R=46,fp32,T=4,1strip]"),
+                                             (3, 0, "full[G=1,R=46,T=2,1strip]")])
 def test_planner_picks_the_measured_best(eng, cfg, prec, expect):
     """The cost model's choices on the benchmark configs (profiles/round1_*: the sweeps
     that calibrated it); guards against a model change silently regressing a config."""
