@@ -30,11 +30,13 @@ const void* full_kernel_ptr(int G, int R, int TR, bool mask, bool fp32, bool mp)
   }
   DTWG_FULL_CFGS_F32(DTWG_F32)
 #undef DTWG_F32
-  // (single strip only: the planner takes G = 1 for m <= R shapes alone)
 #define DTWG_L64(r, tr)                                                                     \
-  if (!fp32 && G == 1 && R == r && TR == tr)                                                \
+  if (!fp32 && G == 1 && R == r && TR == tr) {                                              \
+    if (mp) return mask ? (const void*)dtw_lanemp_kernel<r, tr, true, F64>                  \
+                        : (const void*)dtw_lanemp_kernel<r, tr, false, F64>;                \
     return mask ? (const void*)dtw_lane_kernel<r, tr, true, F64>                            \
-                : (const void*)dtw_lane_kernel<r, tr, false, F64>;
+                : (const void*)dtw_lane_kernel<r, tr, false, F64>;                          \
+  }
   DTWG_LANE_CFGS_F64(DTWG_L64)
 #undef DTWG_L64
   return nullptr;

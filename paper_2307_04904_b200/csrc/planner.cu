@@ -183,7 +183,7 @@ KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cos
                 (band && (!fp32 || ff > 10) && ctx->force_R > 0) ? (int)((2 * s.hw + 1) % ctx->force_R)
                                                                   : -1,
                 ff == 2 ? 2 : 1, ff == 3 ? 4 : 2, ff == 4 || ff > 10, ff > 10 ? ff - 10 : 1};
-    const bool ok = dtwgpu::fill_cfg_supported(f) && (f.G > 1 || s.m <= f.R) &&
+    const bool ok = dtwgpu::fill_cfg_supported(f) &&
                     (f.family == Family::Full ||
                      (mask && f.R >= 2 && (int64_t)f.G * f.R >= 2 * s.hw + 1));
     if (ok) {
