@@ -546,7 +546,9 @@ __global__ void __launch_bounds__(kThreads) dtw_lanemp_kernel(const FillArgs A) 
   const T INF = Ar::inf();
   const T* S = Ar::base(A);
   const int64_t base0 = tid - (threadIdx.x & 31);  // the warp's first item
-  double* bnd = MP ? A.scratch + tid * A.scratch_stride : nullptr;
+  // The warp's 32 boundary columns interleaved by row (bnd[row * 32]), so a warp's
+  // boundary loads and stores of one row are one coalesced 256-byte access.
+  double* bnd = MP ? A.scratch + (tid >> 5) * 32 * A.scratch_stride + (tid & 31) : nullptr;
 
   for (int64_t base = base0; base < A.count; base += nthreads) {
     const int64_t item = base + (threadIdx.x & 31);
@@ -574,7 +576,7 @@ __global__ void __launch_bounds__(kThreads) dtw_lanemp_kernel(const FillArgs A) 
 #pragma unroll
       for (int r = 0; r < R; ++r) pv[r] = INF;
       // cell (rs - 1, c0): row 0 -> (0, 0) = 0 or +inf; else the previous pass's column
-      T diag0 = (rs == 1) ? (pass == 0 ? T(0) : INF) : (MP ? (T)bnd[rs - 1] : INF);
+      T diag0 = (rs == 1) ? (pass == 0 ? T(0) : INF) : (MP ? (T)bnd[(rs - 1) * 32] : INF);
       const int steps = __reduce_max_sync(kFull, re >= rs ? (re - rs + TR) / TR : 0);
       int r0 = rs;
       T xq[TR];
@@ -582,7 +584,7 @@ __global__ void __launch_bounds__(kThreads) dtw_lanemp_kernel(const FillArgs A) 
 #pragma unroll
       for (int t = 0; t < TR; ++t) {
         xq[t] = __ldg(X + (min(r0 + t, n) - 1));
-        bq[t] = (MP && pass > 0) ? bnd[r0 + t] : (double)INF;
+        bq[t] = (MP && pass > 0) ? bnd[(r0 + t) * 32] : (double)INF;
       }
       for (int s = 0; s < steps; ++s, r0 += TR) {
         T x[TR], L[TR];
@@ -591,7 +593,7 @@ __global__ void __launch_bounds__(kThreads) dtw_lanemp_kernel(const FillArgs A) 
           x[t] = xq[t];
           L[t] = (T)bq[t];
           xq[t] = __ldg(X + (min(r0 + TR + t, n) - 1));
-          if (MP && pass > 0) bq[t] = bnd[r0 + TR + t];
+          if (MP && pass > 0) bq[t] = bnd[(r0 + TR + t) * 32];
         }
         const int klo = r0 - hw - 2 - c0, khi = r0 + hw - c0;  // kill columns of row r0
         int need = 0;
@@ -626,7 +628,7 @@ __global__ void __launch_bounds__(kThreads) dtw_lanemp_kernel(const FillArgs A) 
         if (wb) {
 #pragma unroll
           for (int t = 0; t < TR; ++t)
-            if (t < done) bnd[r0 + t] = (double)out[t];
+            if (t < done) bnd[(r0 + t) * 32] = (double)out[t];
         }
         if (last && done > 0 && r0 + done - 1 == n) {
           T rv = pv[0];
@@ -639,7 +641,7 @@ __global__ void __launch_bounds__(kThreads) dtw_lanemp_kernel(const FillArgs A) 
         // Rows the next pass may read past this pass's last one lie outside the band at
         // this pass's last column (+inf).
         if (wb)
-          for (int r = re + 1; r <= min(n, re + R); ++r) bnd[r] = (double)INF;
+          for (int r = re + 1; r <= min(n, re + R); ++r) bnd[r * 32] = (double)INF;
       }
     }
     if (valid) store_result(A, P.slot, result);
