@@ -435,6 +435,23 @@ def test_one_lane_per_pair_kernels(eng, fp32):
             assert_bitwise(got, want, f"lane kernel hw={hw}")
 
 
+@pytest.mark.parametrize("fam,G,R,prec", [(0, 1, 46, 0), (3, 1, 46, 1), (3, 16, 30, 1),
+                                         (3, 2, 16, 0)])
+def test_new_instantiations_on_tiny_inputs(eng, fam, G, R, prec):
+    """Partial warps and single pairs through the one-lane, wide-lane and W = 32 kernels
+    (p = 2, 3, 5; equal and unequal lengths; unlimited and auto-widened windows)."""
+    for lens in ([7, 7], [1, 30], [46, 3, 17], [45, 46, 40, 12, 2]):
+        samples, offsets = _walks(sum(lens), lens)
+        for hw, aw in ((-1, False), (2, True)):
+            eng.force_kernel(fam, G, R)
+            got = eng.build_condensed(samples, offsets, hw, aw, precision=prec)
+            want = oracle.build_condensed(samples, offsets, hw, aw)
+            if prec:
+                np.testing.assert_allclose(got, want, rtol=1e-5, atol=0)
+            else:
+                assert_bitwise(got, want, f"{G},{R} lens={lens} hw={hw}")
+
+
 @pytest.mark.parametrize("cfg,prec,expect", [(1, 0, "full[G=32,R=16"),
                                              (2, 0, "band[G=8,R=26,kr=19,P=1,ring,U=3]"),
                                              (4, 0, "full[G=32,R=15,T=4]"),
