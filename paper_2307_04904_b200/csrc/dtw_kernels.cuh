@@ -1429,7 +1429,10 @@ __global__ void __launch_bounds__(kThreads, Ar::kFp32 ? DTWG_UNIT_MINB32(R) : DT
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const T INF = Ar::inf();
   const T* S = Ar::bbase(A);
-  constexpr int kStride = ((RING + R + 7) / 16) * 16 + 8;
+  // Per-group ring stride: 8 mod 16 words keeps the G = 8/16/32 groups of a warp on
+  // distinct banks; G = 4 (8 groups of 4 lanes) needs 4 mod 32.
+  constexpr int kStride = G == 4 ? ((RING + R + 1 - 4 + 31) / 32) * 32 + 4
+                                 : ((RING + R + 7) / 16) * 16 + 8;
   __shared__ T rings[kThreads / G][kStride];
   T* ring = rings[threadIdx.x / G];
   constexpr int JOFF = 4 * RING;

@@ -18,6 +18,9 @@
 // Band family, ring variant with U units per lane: (G, R, U), R - U odd
 // Strip family (G = 32): (R, rows per step)
 #define DTWG_STRIP_CFGS(X) X(15, 4) X(8, 4)
+// Band ring with U units, fp32 only (wide lanes: half the per-step shuffle and offset
+// work per cell; fp64 would spill): (G, R, U)
+#define DTWG_UNIT_CFGS_F32(X) X(4, 52, 3)
 #define DTWG_UNIT_CFGS(X) X(8, 26, 3) X(8, 26, 5) X(16, 14, 3) X(16, 13, 2) X(16, 20, 3) \
   X(16, 26, 3) X(32, 20, 3) X(32, 26, 3)
 

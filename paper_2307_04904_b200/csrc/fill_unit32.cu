@@ -17,6 +17,8 @@ struct Unit32Table {
 };
 }  // namespace
 
+const void* unit32w_kernel_ptr(int G, int R, int U, int kr);  // fill_unit32w.cu
+
 const void* unit32_kernel_ptr(int G, int R, int U, int kr) {
 #define DTWG_UN32(g, r, u)                                                        \
   if (G == g && R == r && U == u) {                                               \
@@ -25,7 +27,7 @@ const void* unit32_kernel_ptr(int G, int R, int U, int kr) {
   }
   DTWG_UNIT_CFGS(DTWG_UN32)
 #undef DTWG_UN32
-  return nullptr;
+  return unit32w_kernel_ptr(G, R, U, kr);
 }
 
 }  // namespace dtwgpu

@@ -219,6 +219,22 @@ def test_band_family_every_instantiation(eng, G, R, fp32, family):
             assert_bitwise(got, want, f"band G={G} R={R} hw={hw} plan={plan}")
 
 
+def test_band_unit_fp32_only_wide_lanes(eng):
+    """fp32-only unit-ring band kernel with wide lanes (fill_table.h DTWG_UNIT_CFGS_F32:
+    G=4 R=52 U=3), over kill positions from hw = 0 to the widest band it covers."""
+    G, R, U = 4, 52, 3
+    rng = np.random.default_rng(452)
+    for hw in (0, 1, 7, 40, 100, 101, 103):
+        base = int(rng.integers(hw + 2, max(400, hw + 3)))
+        lengths = [max(base + int(d), 1) for d in rng.integers(-hw, hw + 1, size=10)]
+        samples, offsets = _walks(23 + hw, lengths)
+        eng.force_kernel(10 + U, G, R)
+        got = eng.build_condensed(samples, offsets, hw, True, precision=1)
+        assert f"band[G={G},R={R},fp32" in eng.last_plan(), eng.last_plan()
+        want = oracle.build_condensed(samples, offsets, hw, True)
+        np.testing.assert_allclose(got, want, rtol=1e-5, atol=0)
+
+
 STRIP = [15, 8]
 
 
@@ -457,7 +473,8 @@ def test_new_instantiations_on_tiny_inputs(eng, fam, G, R, prec):
                                              (4, 0, "full[G=32,R=15,T=4]"),
                                              (4, 1, "full[G=16,R=30,fp32,T=4]"),
                                              (3, 1, "full[G=1,R=46,fp32,T=4,1strip]"),
-                                             (3, 0, "full[G=1,R=46,T=2,1strip]")])
+                                             (3, 0, "full[G=1,R=46,T=2,1strip]"),
+                                             (2, 1, "band[G=4,R=52,fp32,kr=45,P=1,ring,U=3]")])
 def test_planner_picks_the_measured_best(eng, cfg, prec, expect):
     """The cost model's choices on the benchmark configs (profiles/round1_*: the sweeps
     that calibrated it); guards against a model change silently regressing a config."""
