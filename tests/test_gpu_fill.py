@@ -451,6 +451,24 @@ def test_one_lane_per_pair_kernels(eng, fp32):
             assert_bitwise(got, want, f"lane kernel hw={hw}")
 
 
+@pytest.mark.parametrize("prec", [0, 1])
+def test_planner_mixed_classes_short_and_long(eng, prec):
+    """Default planner over a ragged set whose short pairs (m <= 46) take the one-lane
+    kernels and the rest the wavefront/band families, several classes in one fill."""
+    rng = np.random.default_rng(4647)
+    lengths = np.concatenate([rng.integers(2, 47, size=30), rng.integers(47, 400, size=20)])
+    samples, offsets = _walks(4647, lengths)
+    for hw, aw in ((-1, False), (12, True), (100, True)):
+        got = eng.build_condensed(samples, offsets, hw, aw, precision=prec)
+        want = oracle.build_condensed(samples, offsets, hw, aw)
+        if prec:
+            np.testing.assert_allclose(got, want, rtol=1e-5, atol=0)
+        else:
+            assert_bitwise(got, want, f"mixed hw={hw} plan={eng.last_plan()[:300]}")
+        if hw < 0:
+            assert "G=1,R=46" in eng.last_plan(), eng.last_plan()
+
+
 @pytest.mark.parametrize("fam,G,R,prec", [(0, 1, 46, 0), (3, 1, 46, 1), (3, 16, 30, 1),
                                          (3, 2, 16, 0)])
 def test_new_instantiations_on_tiny_inputs(eng, fam, G, R, prec):
