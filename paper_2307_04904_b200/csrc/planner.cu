@@ -35,6 +35,8 @@ const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026}
                       {2, 16, 2000, 1, 4, false, 1, false, true, true},
                       // fp32 only: c4 fp32 5340 GCUPS against 4598 for (32, 15, 4)
                       {16, 30, 2570, 1, 4, false, 1, true},
+                      // fp32 only: c1 fp32 4310 GCUPS against 3800 for (32, 16, 2)
+                      {16, 32, 2299, 1, 4, false, 1, true},
                       // fp32 only, one lane per pair (no shuffles, no wavefront fill/drain),
                       // single strip only (m <= 46): c3 fp32 5649 against 4403 for (2, 23, 4)
                       {1, 46, 2740, 1, 4, false, 1, true},

@@ -151,7 +151,7 @@ def test_full_family_every_instantiation(eng, G, R, fam, fp32):
             assert_bitwise(got, want, f"full G={G} R={R} hw={hw}")
 
 
-@pytest.mark.parametrize("G,R,maxlen", [(16, 30, 1100), (1, 46, 200)])
+@pytest.mark.parametrize("G,R,maxlen", [(16, 30, 1100), (1, 46, 200), (16, 32, 1100)])
 def test_full_family_fp32_only_instantiations(eng, G, R, maxlen):
     """fp32-only Full instantiations (fill_table.h DTWG_FULL_CFGS_F32): every mask/pass
     variant within the fp32 tolerance (G = 1: one lane per pair, multi-pass when forced);
@@ -492,6 +492,7 @@ def test_new_instantiations_on_tiny_inputs(eng, fam, G, R, prec):
                                              (4, 1, "full[G=16,R=30,fp32,T=4]"),
                                              (3, 1, "full[G=1,R=46,fp32,T=4,1strip]"),
                                              (3, 0, "full[G=1,R=46,T=2,1strip]"),
+                                             (1, 1, "full[G=16,R=32,fp32,T=4,1strip]"),
                                              (2, 1, "band[G=4,R=52,fp32,kr=45,P=1,ring,U=3]")])
 def test_planner_picks_the_measured_best(eng, cfg, prec, expect):
     """The cost model's choices on the benchmark configs (profiles/round1_*: the sweeps
