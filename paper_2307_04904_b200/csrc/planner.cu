@@ -40,6 +40,9 @@ const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026}
                       // fp32 only, one lane per pair (no shuffles, no wavefront fill/drain),
                       // single strip only (m <= 46): c3 fp32 5649 against 4403 for (2, 23, 4)
                       {1, 46, 2740, 1, 4, false, 1, true},
+                      // ... and multi-pass (each lane its own boundary column): c4 fp32 5545
+                      // against 5334 for (16, 30, 4)
+                      {1, 46, 2587, 1, 4, false, 1, true, true},
                       // fp64: one lane per pair, y in shared memory (dtw_lane_kernel),
                       // single strip only: c3 2041 -> 2278 GCUPS
                       {1, 46, 2270, 1, 2, false, 1, false, false, true}};
@@ -138,7 +141,7 @@ KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out, int64_t 
   const bool mask = s.hw < s.n - 1;  // a band that excludes some cell
   for (const Cand& c : kFull) {
     if ((c.f32_only && !fp32) || (c.f64_only && fp32)) continue;
-    if (c.G == 1 && s.m > c.R) continue;  // one lane per pair: single strip only
+    if (c.G == 1 && s.m > c.R && !c.mp_rate) continue;  // single strip unless measured multi-pass
     const double cst = full_cost(s, c, mask, fp32) / fill_factor(count, c.G, sms);
     if (cst < bc) {
       bc = cst;

@@ -489,7 +489,7 @@ def test_new_instantiations_on_tiny_inputs(eng, fam, G, R, prec):
 @pytest.mark.parametrize("cfg,prec,expect", [(1, 0, "full[G=32,R=16"),
                                              (2, 0, "band[G=8,R=26,kr=19,P=1,ring,U=3]"),
                                              (4, 0, "full[G=32,R=15,T=4]"),
-                                             (4, 1, "full[G=16,R=30,fp32,T=4]"),
+                                             (4, 1, "full[G=1,R=46,fp32,T=4]"),
                                              (3, 1, "full[G=1,R=46,fp32,T=4,1strip]"),
                                              (3, 0, "full[G=1,R=46,T=2,1strip]"),
                                              (1, 1, "full[G=16,R=32,fp32,T=4,1strip]"),
