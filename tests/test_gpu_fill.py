@@ -129,7 +129,7 @@ def _walks(seed, lengths):
     return pack(rows)
 
 
-FULL4 = [(2, 23), (4, 12), (8, 8), (16, 16), (32, 15), (32, 16), (2, 16)]
+FULL4 = [(2, 23), (4, 12), (8, 8), (16, 16), (32, 15), (32, 16), (2, 16), (1, 20)]
 
 
 @pytest.mark.parametrize("G,R,fam", [(g, r, 0) for g, r in FULL] + [(g, r, 3) for g, r in FULL4])
@@ -173,7 +173,7 @@ def test_full_family_fp32_only_instantiations(eng, G, R, maxlen):
 
 
 @pytest.mark.parametrize("G,R,fam", [(4, 12, 0), (4, 12, 3), (2, 23, 3), (8, 8, 0), (32, 4, 0),
-                                     (32, 15, 3)])
+                                     (32, 15, 3), (1, 20, 3), (2, 16, 3)])
 def test_full_family_band_edge_kill_cells(eng, G, R, fam):
     """Banded Full fills force only the cell just past each band edge per row to +inf (the
     rest of the out-of-band region comes out +inf by itself, dtw_kernels.cuh FullRows):
