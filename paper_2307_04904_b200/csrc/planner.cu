@@ -33,9 +33,12 @@ const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026}
                       // multi-pass shapes directly: c5 1795 -> 1829 GCUPS (fp32 c5 prefers
                       // 23-column lanes: 3770 against 3624 with this candidate)
                       {2, 16, 2000, 1, 4, false, 1, false, true, true},
-                      // one lane per pair, 20-column passes, each lane its own boundary
-                      // column (no shuffles, no fill/drain): c5 1829 -> 1909 GCUPS
+                      // one lane per pair in 20/24/28-column passes, each lane its own
+                      // boundary column (no shuffles, no fill/drain): c5 1829 -> 1925,
+                      // c4 2192 -> 2248 GCUPS
                       {1, 20, 2000, 1, 4, false, 1, false, true, true},
+                      {1, 24, 2050, 1, 4, false, 1, false, true, true},
+                      {1, 28, 2250, 1, 4, false, 1, false, true, true},
                       // fp32 only: c4 fp32 5340 GCUPS against 4598 for (32, 15, 4)
                       {16, 30, 2570, 1, 4, false, 1, true},
                       // fp32 only: c1 fp32 4310 GCUPS against 3800 for (32, 16, 2)

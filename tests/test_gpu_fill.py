@@ -129,7 +129,8 @@ def _walks(seed, lengths):
     return pack(rows)
 
 
-FULL4 = [(2, 23), (4, 12), (8, 8), (16, 16), (32, 15), (32, 16), (2, 16), (1, 20)]
+FULL4 = [(2, 23), (4, 12), (8, 8), (16, 16), (32, 15), (32, 16), (2, 16), (1, 20), (1, 24),
+         (1, 28)]
 
 
 @pytest.mark.parametrize("G,R,fam", [(g, r, 0) for g, r in FULL] + [(g, r, 3) for g, r in FULL4])
@@ -173,7 +174,7 @@ def test_full_family_fp32_only_instantiations(eng, G, R, maxlen):
 
 
 @pytest.mark.parametrize("G,R,fam", [(4, 12, 0), (4, 12, 3), (2, 23, 3), (8, 8, 0), (32, 4, 0),
-                                     (32, 15, 3), (1, 20, 3), (2, 16, 3)])
+                                     (32, 15, 3), (1, 20, 3), (2, 16, 3), (1, 28, 3)])
 def test_full_family_band_edge_kill_cells(eng, G, R, fam):
     """Banded Full fills force only the cell just past each band edge per row to +inf (the
     rest of the out-of-band region comes out +inf by itself, dtw_kernels.cuh FullRows):
@@ -488,7 +489,7 @@ def test_new_instantiations_on_tiny_inputs(eng, fam, G, R, prec):
 
 @pytest.mark.parametrize("cfg,prec,expect", [(1, 0, "full[G=32,R=16"),
                                              (2, 0, "band[G=8,R=26,kr=19,P=1,ring,U=3]"),
-                                             (4, 0, "full[G=32,R=15,T=4]"),
+                                             (4, 0, "full[G=1,R=28,T=4]"),
                                              (4, 1, "full[G=1,R=46,fp32,T=4]"),
                                              (3, 1, "full[G=1,R=46,fp32,T=4,1strip]"),
                                              (3, 0, "full[G=1,R=46,T=2,1strip]"),
