@@ -5,7 +5,7 @@
 #define DTWG_FULL_CFGS(X)                                                                  \
   X(2, 23, 2) X(4, 12, 2) X(8, 8, 2) X(16, 8, 2) X(16, 16, 2) X(32, 4, 2) X(32, 8, 2)    \
   X(32, 12, 2) X(32, 15, 2) X(32, 16, 2) X(2, 23, 4) X(4, 12, 4) X(8, 8, 4) X(16, 16, 4) \
-  X(32, 15, 4) X(32, 16, 4) X(2, 16, 4) X(1, 20, 4) X(1, 24, 4) X(1, 28, 4)
+  X(32, 15, 4) X(32, 16, 4) X(2, 16, 4) X(1, 20, 4) X(1, 24, 4) X(1, 28, 4) X(1, 32, 4)
 // Full family, fp32 only (wide strips: half the per-row overhead per cell; the fp64
 // instantiation would need > 255 registers)
 #define DTWG_FULL_CFGS_F32(X) X(16, 30, 4) X(1, 46, 4) X(16, 32, 4)

@@ -21,6 +21,7 @@ struct Cand {
   bool f32_only = false;  // full family: instantiated for fp32 only (fill_table.h)
   bool mp_rate = false;   // full family: rate measured on multi-pass shapes (no penalty)
   bool f64_only = false;  // full family: planned for fp64 only
+  bool unmasked = false;  // full family: planned for unlimited windows only
 };
 const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026},
                       {4, 12, 1956, 1, 4},   {8, 8, 1804},         {8, 8, 1700, 1, 4},
@@ -39,6 +40,8 @@ const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026}
                       {1, 20, 2000, 1, 4, false, 1, false, true, true},
                       {1, 24, 2050, 1, 4, false, 1, false, true, true},
                       {1, 28, 2250, 1, 4, false, 1, false, true, true},
+                      // unlimited windows only: c4 2246 -> 2358 (masked c5 strips: 1813)
+                      {1, 32, 2360, 1, 4, false, 1, false, true, true, true},
                       // fp32 only: c4 fp32 5340 GCUPS against 4598 for (32, 15, 4)
                       {16, 30, 2570, 1, 4, false, 1, true},
                       // fp32 only: c1 fp32 4310 GCUPS against 3800 for (32, 16, 2)
@@ -146,7 +149,7 @@ KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out, int64_t 
   double bc = 1e300;
   const bool mask = s.hw < s.n - 1;  // a band that excludes some cell
   for (const Cand& c : kFull) {
-    if ((c.f32_only && !fp32) || (c.f64_only && fp32)) continue;
+    if ((c.f32_only && !fp32) || (c.f64_only && fp32) || (c.unmasked && mask)) continue;
     if (c.G == 1 && s.m > c.R && !c.mp_rate) continue;  // single strip unless measured multi-pass
     const double cst = full_cost(s, c, mask, fp32) / fill_factor(count, c.G, sms);
     if (cst < bc) {

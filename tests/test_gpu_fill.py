@@ -130,7 +130,7 @@ def _walks(seed, lengths):
 
 
 FULL4 = [(2, 23), (4, 12), (8, 8), (16, 16), (32, 15), (32, 16), (2, 16), (1, 20), (1, 24),
-         (1, 28)]
+         (1, 28), (1, 32)]
 
 
 @pytest.mark.parametrize("G,R,fam", [(g, r, 0) for g, r in FULL] + [(g, r, 3) for g, r in FULL4])
@@ -489,7 +489,7 @@ def test_new_instantiations_on_tiny_inputs(eng, fam, G, R, prec):
 
 @pytest.mark.parametrize("cfg,prec,expect", [(1, 0, "full[G=32,R=16"),
                                              (2, 0, "band[G=8,R=26,kr=19,P=1,ring,U=3]"),
-                                             (4, 0, "full[G=1,R=28,T=4]"),
+                                             (4, 0, "full[G=1,R=32,T=4]"),
                                              (4, 1, "full[G=1,R=46,fp32,T=4]"),
                                              (3, 1, "full[G=1,R=46,fp32,T=4,1strip]"),
                                              (3, 0, "full[G=1,R=46,T=2,1strip]"),
