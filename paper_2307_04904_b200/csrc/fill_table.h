@@ -8,7 +8,7 @@
   X(32, 15, 4) X(32, 16, 4) X(2, 16, 4) X(1, 20, 4) X(1, 24, 4) X(1, 28, 4) X(1, 32, 4)
 // Full family, fp32 only (wide strips: half the per-row overhead per cell; the fp64
 // instantiation would need > 255 registers)
-#define DTWG_FULL_CFGS_F32(X) X(16, 30, 4) X(1, 46, 4) X(16, 32, 4)
+#define DTWG_FULL_CFGS_F32(X) X(16, 30, 4) X(1, 46, 4) X(16, 32, 4) X(1, 56, 4) X(1, 64, 4)
 // One lane per pair, fp64, single strip (dtw_lane_kernel): (R, rows per step)
 #define DTWG_LANE_CFGS_F64(X) X(46, 2)
 #define DTWG_BAND_CFGS_G16(X) X(16, 7) X(16, 9) X(16, 11) X(16, 13)

@@ -52,6 +52,10 @@ const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026}
                       // ... and multi-pass (each lane its own boundary column): c4 fp32 5545
                       // against 5334 for (16, 30, 4)
                       {1, 46, 2587, 1, 4, false, 1, true, true},
+                      // ... and wider passes for unlimited windows: c4 fp32 5516 -> 6129
+                      // (masked c5 strips at R = 64: 3000 against 3867)
+                      {1, 56, 2760, 1, 4, false, 1, true, true, false, true},
+                      {1, 64, 2888, 1, 4, false, 1, true, true, false, true},
                       // fp64: one lane per pair, y in shared memory (dtw_lane_kernel),
                       // single strip only: c3 2041 -> 2278 GCUPS
                       {1, 46, 2270, 1, 2, false, 1, false, false, true}};

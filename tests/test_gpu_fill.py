@@ -152,7 +152,8 @@ def test_full_family_every_instantiation(eng, G, R, fam, fp32):
             assert_bitwise(got, want, f"full G={G} R={R} hw={hw}")
 
 
-@pytest.mark.parametrize("G,R,maxlen", [(16, 30, 1100), (1, 46, 200), (16, 32, 1100)])
+@pytest.mark.parametrize("G,R,maxlen", [(16, 30, 1100), (1, 46, 200), (16, 32, 1100),
+                                        (1, 56, 300), (1, 64, 300)])
 def test_full_family_fp32_only_instantiations(eng, G, R, maxlen):
     """fp32-only Full instantiations (fill_table.h DTWG_FULL_CFGS_F32): every mask/pass
     variant within the fp32 tolerance (G = 1: one lane per pair, multi-pass when forced);
@@ -490,7 +491,7 @@ def test_new_instantiations_on_tiny_inputs(eng, fam, G, R, prec):
 @pytest.mark.parametrize("cfg,prec,expect", [(1, 0, "full[G=32,R=16"),
                                              (2, 0, "band[G=8,R=26,kr=19,P=1,ring,U=3]"),
                                              (4, 0, "full[G=1,R=32,T=4]"),
-                                             (4, 1, "full[G=1,R=46,fp32,T=4]"),
+                                             (4, 1, "full[G=1,R=64,fp32,T=4]"),
                                              (3, 1, "full[G=1,R=46,fp32,T=4,1strip]"),
                                              (3, 0, "full[G=1,R=46,T=2,1strip]"),
                                              (1, 1, "full[G=16,R=32,fp32,T=4,1strip]"),
