@@ -4,18 +4,24 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--precision fp64|fp32]
     python bench.py --impl reference ...      # the reference's own multithreaded CPU fill
 
-One step = the full distance-matrix fill of config C (default: configs[1] of
-BASELINE.json, "c2": N=1000 z-normalised Gaussian random walks, length 1000, Sakoe-Chiba
-window 100, fp64), sharded over N GPUs (one process per GPU, torchrun) with the slices
-assembled by an NCCL all-gather. Inputs are the seeded synthetic stand-ins for the UCR
-data the paper used (paper_2307_04904_b200/generators.py).
+One step = the full distance-matrix fill of config C (default: configs[3] of
+BASELINE.json, "c4": N=1000 z-normalised Gaussian random walks, length 2844, unlimited
+window, fp64 -- the largest single-GPU config, 4.04e12 cells), sharded over N GPUs (one
+process per GPU, torchrun) with every distance stored into every rank's matrix by the
+fill kernels themselves (fused P2P exchange; NCCL all-gather fallback). Inputs are the
+seeded synthetic stand-ins for the UCR data the paper used
+(paper_2307_04904_b200/generators.py).
 
 Prints one JSON line (rank 0). `value` = total in-band DP cells / max-over-ranks device
 time (GCUPS), inputs resident in HBM; `e2e` = the same metric through the public API
 (api.build_matrix_packed: pinned host series -> H2D -> fill -> validation -> D2H of the
-condensed matrix). `roofline` compares the fill kernel with the live-measured ceiling of
-the cell body itself (dtwg_measure_cell_peak); `cpu_baseline` times the reference's
-build_matrix (oracle/_ref, all host threads) on a bounded sample of the same workload.
+condensed matrix). `roofline` compares the fill kernel with the theoretical fp64 (fp32)
+pipe rate of SURVEY.md §8(d) at MEASURED_PEAKS.sm_max_mhz (3722 GCUPS fp64 at 1965 MHz),
+with the live-measured ceiling of the cell body as a secondary key; `cpu_baseline` times
+the reference's build_matrix (oracle/_ref, all host threads) on a bounded sample of the
+same workload. At N=1 the line also carries `all_configs` (one fill of each of c1-c5) and
+`kmedoids` (the c5 and c3 k-medoids runs over the resident matrix; c5 checked against the
+reference's own kmedoids).
 """
 from __future__ import annotations
 
@@ -179,6 +185,11 @@ def run_reference_arm(a, ds):
     value = total_cells / total_s / 1e9
     cb = dict(samples[-1])
     cb["value"] = value
+    from paper_2307_04904_b200 import generators as gen
+    cb["extrapolated_full_matrix_s"] = gen.total_cells(ds) / (value * 1e9)
+    cb["extrapolated_note"] = ("the reference's full-matrix time on these cores, extrapolated "
+                               "by in-band cells from the timed samples (exact: the reference "
+                               "has no data-dependent pruning)")
     cb.pop("seconds", None)
     cb.pop("cells", None)
     line = {
@@ -196,6 +207,112 @@ def run_reference_arm(a, ds):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+def theoretical_peak(prec: int):
+    """148 SMs x 64 fp64 lanes (128 fp32) x SM clock / ops per cell (5 fp64
+    pipe ops; FADD FMUL FMNMX3 FADD = 4 fp32), GCUPS, at MEASURED_PEAKS.sm_max_mhz."""
+    mhz, src = 1965.0, "fallback 1965 MHz (B200_PROFILING.md)"
+    try:
+        mhz = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"])
+        src = "MEASURED_PEAKS.json sm_max_mhz"
+    except (OSError, ValueError, KeyError):
+        pass
+    per = (148 * 64 / 5) if prec == 0 else (148 * 128 / 4)
+    return per * mhz * 1e6 / 1e9, f"theoretical {'fp64' if prec == 0 else 'fp32'} pipe rate " \
+        f"(SURVEY.md §8(d)) at {mhz:.0f} MHz ({src})"
+
+
+def _fill_once(eng, ds, prec, out_ptr):
+    """One device fill of the whole matrix (plan cached by a previous call); device ms."""
+    total = ds.p * (ds.p - 1) // 2
+    eng.fill_slots(ds.half_width, ds.auto_widen, prec, 0, total, out_ptr)
+    eng.synchronize()
+    return eng.last_fill_ms()
+
+
+def all_configs_block(eng, dev, a):
+    """One timed fill of each BASELINE config (fp64; c4 also fp32), plus the k-medoids runs
+    of c5 (parity against the reference's own kmedoids, timed as its CPU baseline) and c3,
+    each over the matrix its fill just left in HBM."""
+    import torch
+
+    from paper_2307_04904_b200 import api, generators as gen
+
+    out, kmed = {}, {}
+    peak64 = theoretical_peak(0)[0]
+    peak32 = theoretical_peak(1)[0]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for c, prec in ((1, 0), (2, 0), (3, 0), (4, 0), (5, 0), (4, 1)):
+        ds = gen.make_config(c)
+        total = ds.p * (ds.p - 1) // 2
+        buf = torch.empty(total, dtype=torch.float64, device=dev)
+        eng.upload(ds.samples, ds.offsets)
+        cells = eng.count_cells(ds.half_width, ds.auto_widen, 0, total)
+        t0 = time.perf_counter()
+        _fill_once(eng, ds, prec, buf.data_ptr())  # plans + warms
+        first_s = time.perf_counter() - t0
+        flush.zero_()
+        ms = _fill_once(eng, ds, prec, buf.data_ptr())
+        key = f"c{c}" + ("_fp32" if prec else "")
+        peak = peak32 if prec else peak64
+        out[key] = {"gcups": cells / (ms * 1e-3) / 1e9, "fill_ms": ms, "cells": cells,
+                    "pairs": total, "frac_of_peak": cells / (ms * 1e-3) / 1e9 / peak,
+                    "first_call_s": first_s, "plan": eng.last_plan()[:400]}
+        if c == 5 and prec == 0:
+            # cold first call through the public API on a fresh context (planning, H2D,
+            # fill, checks, D2H all inside)
+            fresh = api.Engine(dev.index)
+            t0 = time.perf_counter()
+            fresh.build_condensed(ds.samples, ds.offsets, ds.half_width, ds.auto_widen)
+            out[key]["cold_e2e_first_call_s"] = time.perf_counter() - t0
+            fresh.close()
+        if a.kmedoids and prec == 0 and c in (3, 5):
+            kmed[key] = kmedoids_run(eng, ds, buf, check=(c == 5 and a.check))
+        del buf
+        torch.cuda.empty_cache()
+    return out, kmed
+
+
+def kmedoids_run(eng, ds, cond, check):
+    """The config's k-medoids (kmedoids.hpp:148-189) over the matrix resident in HBM."""
+    p = ds.p
+    eng.adopt(None, p, on_device_ptr=cond.data_ptr())
+    eng._p_resident = p
+    eng.synchronize()
+    eng.km_stats(reset=True)
+    t0 = time.perf_counter()
+    med, asg, cost, br = eng.kmedoids(p, ds.k, ds.restarts, 100, 0)
+    km_s = time.perf_counter() - t0
+    st = eng.km_stats()
+    hbm = _hbm_peak()
+    upd_gbs = st["update_bytes"] / max(st["update_ms"], 1e-9) / 1e6
+    res = {"k": ds.k, "restarts": ds.restarts, "series": p, "seconds": km_s,
+           "sweeps": st["sweeps"], "total_cost": cost, "best_restart": br,
+           "includes": "square expansion + every restart (seeding, sweeps, host sums)",
+           "update_kernels": {"ms": st["update_ms"], "algorithmic_bytes": st["update_bytes"],
+                              "achieved_gbs": upd_gbs, "peak_gbs": hbm[0],
+                              "frac": upd_gbs / hbm[0], "peak_source": hbm[1]},
+           "assign_kernel": {"ms": st["assign_ms"], "algorithmic_bytes": st["assign_bytes"],
+                             "achieved_gbs": st["assign_bytes"] / max(st["assign_ms"], 1e-9) / 1e6}}
+    if check:
+        # Parity against the reference's own kmedoids (oracle/_ref; the C restatement when
+        # it was not built), timed: its single-threaded restart loop over the same host
+        # matrix is the k-medoids CPU baseline (SURVEY.md §8(d)).
+        import oracle
+        D = cond.cpu().numpy()
+        kind = "reference" if oracle.have_ref() else "port"
+        t1 = time.perf_counter()
+        if kind == "reference":
+            rmed, rasg, rcost = oracle.ref_kmedoids(D, p, ds.k, ds.restarts, 100, 0)
+        else:
+            rmed, rasg, rcost = oracle.kmedoids(D, p, ds.k, ds.restarts, 100, 0)
+        res["cpu_baseline"] = {"seconds": time.perf_counter() - t1, "kind": kind, "cores": 1,
+                               "sample": "the whole k-medoids run (single-threaded, as the "
+                                         "reference's kmedoids is)"}
+        res["parity"] = bool(list(rmed) == list(med) and list(rasg) == list(asg)
+                             and rcost == cost)
+    return res
+
+
 def run_gpu_arm(a, ds):
     import torch
     import torch.distributed as dist
@@ -214,6 +331,9 @@ def run_gpu_arm(a, ds):
         if gloo:
             dist.init_process_group("gloo")
         else:
+            # NCCL init lines (rank count, transport) in the log so the ranks can be checked
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -243,6 +363,8 @@ def run_gpu_arm(a, ds):
         exchange = a.exchange
         if exchange == "p2p" and not dd.open_p2p_exchange(eng, p, rank, world):
             exchange = "nccl (p2p unavailable)"
+    gather_ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    gather_ms = []
 
     def step():
         if exchange == "p2p":
@@ -251,12 +373,14 @@ def run_gpu_arm(a, ds):
         if e > b:
             eng.fill_slots(ds.half_width, ds.auto_widen, prec, b, e, mine.data_ptr())
         if world > 1:
+            gather_ev[0].record(stream)
             if gloo:
                 host = full.cpu()
                 dist.all_gather_into_tensor(host, host[rank * width:(rank + 1) * width].clone())
                 full.copy_(host)
             else:
                 dist.all_gather_into_tensor(full, mine)
+            gather_ev[1].record(stream)
 
     def assembled():
         """The gathered slices in condensed order (ragged shards are padded to `width`)."""
@@ -289,6 +413,9 @@ def run_gpu_arm(a, ds):
             step()
             evs[k][1].record(stream)
             fill_ms.append(eng.last_fill_ms() if e > b else 0.0)
+            if world > 1 and not exchange == "p2p":
+                gather_ev[1].synchronize()
+                gather_ms.append(gather_ev[0].elapsed_time(gather_ev[1]))
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -300,6 +427,15 @@ def run_gpu_arm(a, ds):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
     value = all_cells * a.steps / (max_ms * 1e-3) / 1e9
+    per_rank = None
+    if world > 1:
+        mine_stats = {"rank": rank, "slots": [b, e], "cells": my_cells,
+                      "step_ms_mean": my_ms / max(a.steps, 1),
+                      "fill_ms_mean": statistics.mean(fill_ms) if fill_ms else 0.0,
+                      "exchange_ms_mean": (statistics.mean(gather_ms) if gather_ms else
+                                           "fused into the fill kernels (P2P stores)")}
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine_stats)
 
     # Parity spot-check of the timed output against the C restatement (a few pairs).
     check = None
@@ -321,10 +457,13 @@ def run_gpu_arm(a, ds):
             g = got[s_ - lo]
             ok += int(g == want if prec == 0 else abs(g - want) <= 1e-5 * abs(want))
         check = f"{ok}/{len(picks)} sampled pairs match the oracle"
+    elif world > 1 and exchange == "p2p" and a.check:
+        eng.exchange_complete()
 
     # Roofline: the fill kernel (one launch per step for same-length series) against the
-    # live-measured ceiling of the cell body.
-    peak = eng.measure_cell_peak(prec) / 1e9
+    # theoretical fp64/fp32 pipe rate; the live-measured cell-body ceiling alongside.
+    peak, peak_src = theoretical_peak(prec)
+    live_peak = eng.measure_cell_peak(prec) / 1e9
     kernel_ms = statistics.mean(fill_ms) if fill_ms else None
     achieved = my_cells / (kernel_ms * 1e-3) / 1e9 if kernel_ms else None
     traffic = None
@@ -353,13 +492,18 @@ def run_gpu_arm(a, ds):
             dt = time.perf_counter() - t0
             d2h = m.condensed().nbytes
         else:
-            host = torch.empty(width, dtype=torch.float64).pin_memory()
+            # each rank: H2D of the series, its fill (+ exchange), D2H of its own slice --
+            # from the resident exchange matrix on the P2P path, from `mine` on NCCL
+            host = torch.empty(max(e - b, 1), dtype=torch.float64).pin_memory()
             dist.barrier()
             t0 = time.perf_counter()
             for _ in range(a.steps):
                 eng.upload(s_np, o_np)
                 step()
-                host[: e - b].copy_(mine[: e - b], non_blocking=True)
+                if exchange == "p2p":
+                    eng.download_range(b, e, host.numpy())
+                else:
+                    host[: e - b].copy_(mine[: e - b], non_blocking=True)
                 torch.cuda.synchronize()
             dt = time.perf_counter() - t0
             tt = torch.tensor([dt], dtype=torch.float64, device="cpu" if gloo else dev)
@@ -378,10 +522,10 @@ def run_gpu_arm(a, ds):
             e2e["d2h_ms"] = _copy_ms(torch.empty(int(d2h) // 8, dtype=torch.float64, device=dev),
                                      "cpu")
 
-    # k-medoids sweeps over the device-resident matrix (the second hot loop), restarts
-    # sharded over ranks and reduced in restart order.
+    # k-medoids over the headline config's own matrix, restarts sharded over ranks
+    # (restart r on rank r mod N) and reduced in restart order (--kmedoids, configs with k).
     kmed = None
-    if a.kmedoids and ds.k:
+    if a.kmedoids and ds.k and a.kmedoids_headline:
         if exchange == "p2p":
             eng.exchange_complete()  # resident already, written by all ranks' fills
         else:
@@ -392,43 +536,35 @@ def run_gpu_arm(a, ds):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
 
-        def run(rb, re_):
-            med, asg, cost, br = eng.kmedoids(p, ds.k, ds.restarts, 100, 0, rb, re_)
-            return (cost, br, med.tolist(), asg.tolist())
+        def run(rs):
+            best_ = None
+            for r in rs:
+                med, asg, cost, br = eng.kmedoids(p, ds.k, ds.restarts, 100, 0, r, r + 1)
+                if best_ is None or cost < best_[0]:
+                    best_ = (cost, br, med.tolist(), asg.tolist())
+            return best_
 
-        best = dd.kmedoids_restart_sharded(run, ds.restarts, rank, world)
-        km_s = time.perf_counter() - t0
-        st = eng.km_stats()
-        hbm = _hbm_peak()
-        kmed = {"k": ds.k, "restarts": ds.restarts, "seconds": km_s, "sweeps": st["sweeps"],
-                "total_cost": best[0], "best_restart": best[1],
-                "update_kernel": {"ms": st["update_ms"], "algorithmic_bytes": st["update_bytes"],
-                                  "achieved_gbs": st["update_bytes"] / max(st["update_ms"], 1e-9) / 1e6,
-                                  "peak_gbs": hbm[0], "peak_source": hbm[1]},
-                "assign_kernel": {"ms": st["assign_ms"], "algorithmic_bytes": st["assign_bytes"],
-                                  "achieved_gbs": st["assign_bytes"] / max(st["assign_ms"], 1e-9) / 1e6}}
-        if rank == 0 and a.check and p <= 5000:
-            # Parity against the reference's own kmedoids (oracle/_ref; the C restatement
-            # when it was not built), timed: its single-threaded restart loop over the same
-            # host matrix is the k-medoids CPU baseline.
-            import oracle
-            D = eng.download(p) if exchange == "p2p" else cond.cpu().numpy()
-            km_kind = "reference" if oracle.have_ref() else "port"
-            t1 = time.perf_counter()
-            if km_kind == "reference":
-                med, asg, cost = oracle.ref_kmedoids(D, p, ds.k, ds.restarts, 100, 0)
-            else:
-                med, asg, cost = oracle.kmedoids(D, p, ds.k, ds.restarts, 100, 0)
-            kmed["cpu_baseline"] = {"seconds": time.perf_counter() - t1, "kind": km_kind,
-                                    "cores": 1, "sample": "the whole k-medoids run"}
-            kmed["parity"] = bool(list(med) == list(best[2]) and list(asg) == list(best[3])
-                                  and cost == best[0])
+        best = dd.kmedoids_restart_round_robin(run, ds.restarts, rank, world)
+        kmed = {"headline_config": {"k": ds.k, "restarts": ds.restarts,
+                                    "seconds": time.perf_counter() - t0,
+                                    "total_cost": best[0], "best_restart": best[1],
+                                    "restarts_on_this_rank": list(range(rank, ds.restarts, world))}}
 
     cpu = None
     if rank == 0 and world == 1 and a.cpu_baseline:
         cpu = cpu_reference_sample(ds, a.ref_step_s)
+        cpu["extrapolated_full_matrix_s"] = all_cells / (cpu["value"] * 1e9)
+        cpu["extrapolated_note"] = ("the reference's full-matrix time on these cores, "
+                                    "extrapolated by in-band cells from the timed sample "
+                                    "(exact: the reference has no data-dependent pruning)")
         cpu.pop("seconds", None)
         cpu.pop("cells", None)
+
+    allc = None
+    if rank == 0 and world == 1 and a.all_configs:
+        allc, km_all = all_configs_block(eng, dev, a)
+        if km_all:
+            kmed = dict(kmed or {}, **km_all)
 
     if rank == 0:
         clocks = clk.summary()
@@ -448,18 +584,21 @@ def run_gpu_arm(a, ds):
                        "l2": "flushed (256 MB write) between timed steps",
                        "plan": eng.last_plan()},
             "pairs_per_s": total * a.steps / (max_ms * 1e-3),
-            "frac_of_theoretical_fp64_peak": value / (148 * 64 * 1.965e9 / 5 / 1e9)
-            if prec == 0 else None,
             "roofline": {"bound": "fp64" if prec == 0 else "fp32",
                          "achieved": achieved, "peak": peak,
                          "unit": "GCUPS (cell updates/s; fp64 cell = 5 fp64-pipe ops, fp32 cell = FADD FMUL FMNMX3 FADD)",
                          "frac": (achieved / peak) if achieved else None,
                          "traffic": traffic,
-                         "peak_source": "measured live: dtwg_measure_cell_peak (cell body, "
-                                        "8 independent chains/thread, all SMs)"},
+                         "peak_source": peak_src,
+                         "live_cell_ceiling": live_peak,
+                         "frac_of_live_ceiling": (achieved / live_peak) if achieved else None,
+                         "live_ceiling_source": "dtwg_measure_cell_peak (cell body, 8 "
+                                                "independent chains/thread, all SMs), measured now"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
+            "per_rank": per_rank,
+            "all_configs": allc,
             "kmedoids": kmed,
             "clocks": clocks,
             "parity": check,
@@ -496,7 +635,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-step-s", type=float, default=4.0,
@@ -511,8 +650,12 @@ def main():
                          "all-gather of the slices")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: diagnostic multi-rank run (ranks may share a GPU)")
-    ap.add_argument("--kmedoids", action="store_true",
-                    help="also run the config's k-medoids over the resident matrix")
+    ap.add_argument("--no-kmedoids", dest="kmedoids", action="store_false",
+                    help="skip the k-medoids runs (c5 with parity, c3) of the N=1 line")
+    ap.add_argument("--kmedoids-headline", action="store_true",
+                    help="also run the headline config's own k-medoids (restarts r mod N)")
+    ap.add_argument("--no-all-configs", dest="all_configs", action="store_false",
+                    help="skip the one-fill-per-config block of the N=1 line")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 0)
     from paper_2307_04904_b200 import generators as gen

@@ -124,6 +124,9 @@ const char* dtwg_last_plan(const dtwg_ctx* ctx);
 int dtwg_adopt_condensed(dtwg_ctx* ctx, const double* condensed, int64_t p, int on_device);
 /* Copy the resident condensed matrix to host memory (p(p-1)/2 doubles). */
 int dtwg_download_condensed(dtwg_ctx* ctx, double* out_condensed);
+/* Copy slots [slot_begin, slot_end) of the resident (or, during a fused exchange, the
+ * rank's own exchange) matrix to host memory -- a rank's own slice after its fill. */
+int dtwg_download_range(dtwg_ctx* ctx, int64_t slot_begin, int64_t slot_end, double* out);
 
 typedef void (*dtwg_observer_fn)(void* user, int64_t restart, int64_t iteration, double cost);
 
@@ -141,9 +144,12 @@ int dtwg_kmedoids(dtwg_ctx* ctx, int64_t k, int64_t restarts, int64_t max_iterat
                   dtwg_observer_fn observer, void* user, int64_t* medoids_out,
                   int64_t* assignment_out, double* cost_out, int64_t* best_restart_out);
 
-/* k-medoids sweep statistics since the last reset: out[0] sweeps, out[1] assignment
- * kernel ms, out[2] its algorithmic bytes (8 per distance read), out[3] update kernels
- * ms, out[4] their algorithmic bytes (8 * sum |C|^2 + index traffic). */
+/* k-medoids sweep statistics since the last reset (out: 7 doubles): out[0] sweeps,
+ * out[1] assignment kernel ms, out[2] its algorithmic bytes (8 per distance read), out[3]
+ * update kernels ms (device bucketing + candidate sums + selection), out[4] their
+ * algorithmic bytes (8 * sum |C|^2 + index traffic), out[5] ms spent preparing the sweep
+ * views (square expansion + cluster-ordered copy), out[6] 1 if the cluster-ordered copy
+ * is in use. With concurrent restart workers the per-sweep times overlap each other. */
 int dtwg_km_stats(dtwg_ctx* ctx, double* out, int reset);
 
 /*

@@ -27,7 +27,7 @@ EXPORTS = [
     "dtwg_create", "dtwg_destroy", "dtwg_last_error", "dtwg_last_error_pair", "dtwg_set_stream",
     "dtwg_synchronize", "dtwg_build_matrix", "dtwg_upload_series", "dtwg_fill_slots",
     "dtwg_count_cells", "dtwg_last_fill_ms", "dtwg_launch_count", "dtwg_last_plan",
-    "dtwg_adopt_condensed", "dtwg_download_condensed", "dtwg_kmedoids", "dtwg_km_nearest_update",
+    "dtwg_adopt_condensed", "dtwg_download_condensed", "dtwg_download_range", "dtwg_kmedoids", "dtwg_km_nearest_update",
     "dtwg_km_assign", "dtwg_km_update", "dtwg_force_kernel", "dtwg_measure_cell_peak", "dtwg_km_stats", "dtwg_silhouette",
     "dtwg_create_multi", "dtwg_device_count", "dtwg_visible_devices",
     "dtwg_exchange_export", "dtwg_exchange_open", "dtwg_exchange_fill", "dtwg_exchange_complete",
@@ -83,6 +83,7 @@ def lib() -> C.CDLL:
     L.dtwg_last_plan.restype = C.c_char_p
     L.dtwg_adopt_condensed.argtypes = [_vp, _vp, _i64, C.c_int]
     L.dtwg_download_condensed.argtypes = [_vp, _dp]
+    L.dtwg_download_range.argtypes = [_vp, _i64, _i64, _vp]
     L.dtwg_kmedoids.argtypes = [_vp, _i64, _i64, _i64, C.c_uint64, _i64, _i64, OBSERVER, _vp,
                                 _ip, _ip, P(C.c_double), P(_i64)]
     L.dtwg_km_nearest_update.argtypes = [_vp, _i64, _u8, _dp]
@@ -130,7 +131,7 @@ def lib() -> C.CDLL:
                                               "dtwg_build_matrix", "dtwg_upload_series",
                                               "dtwg_fill_slots", "dtwg_count_cells",
                                               "dtwg_last_fill_ms", "dtwg_adopt_condensed",
-                                              "dtwg_download_condensed", "dtwg_kmedoids",
+                                              "dtwg_download_condensed", "dtwg_download_range", "dtwg_kmedoids",
                                               "dtwg_km_nearest_update", "dtwg_km_assign",
                                               "dtwg_km_update", "dtwg_force_kernel",
                                               "dtwg_measure_cell_peak", "dtwg_km_stats",

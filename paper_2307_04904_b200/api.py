@@ -198,10 +198,11 @@ class Engine:
 
     def km_stats(self, reset: bool = False) -> dict:
         """Sweep count and device time / algorithmic bytes of the k-medoids kernels."""
-        out = np.zeros(5, dtype=np.float64)
+        out = np.zeros(7, dtype=np.float64)
         self.check(self.L.dtwg_km_stats(self.h, out, int(reset)))
         return {"sweeps": int(out[0]), "assign_ms": out[1], "assign_bytes": out[2],
-                "update_ms": out[3], "update_bytes": out[4]}
+                "update_ms": out[3], "update_bytes": out[4], "prep_ms": out[5],
+                "cluster_layout": bool(out[6])}
 
     def last_plan(self) -> str:
         return self.L.dtwg_last_plan(self.h).decode()
@@ -252,6 +253,13 @@ class Engine:
         out = np.empty(max(p * (p - 1) // 2, 1), dtype=np.float64)
         self.check(self.L.dtwg_download_condensed(self.h, out))
         return out[: p * (p - 1) // 2]
+
+    def download_range(self, b: int, e: int, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """Slots [b, e) of the resident matrix (a rank's own slice during an exchange)."""
+        if out is None:
+            out = np.empty(max(e - b, 1), dtype=np.float64)
+        self.check(self.L.dtwg_download_range(self.h, b, e, C.c_void_p(out.ctypes.data)))
+        return out[: e - b]
 
     def kmedoids(self, p, k, restarts, max_iterations, seed, restart_begin=0, restart_end=None,
                  observer=None):

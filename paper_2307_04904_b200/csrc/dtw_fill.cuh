@@ -95,5 +95,31 @@ cudaError_t launch_assign(const double* matrix, bool condensed, int64_t p,
 cudaError_t launch_update(const double* matrix, bool condensed, int64_t p,
                           const int32_t* members, const int64_t* cluster_begin, int64_t k,
                           int64_t* best_member, double* best_sum, cudaStream_t s);
+// round 2: device-side bucketing, slot-writing assignment, cluster-ordered square
+cudaError_t launch_assign_slots(const double* matrix, bool condensed, int64_t p,
+                                const int64_t* medoids, int64_t k, int64_t* assignment,
+                                double* dist, int32_t* lab, cudaStream_t s);
+cudaError_t launch_slots_of(const double* matrix, bool condensed, int64_t p,
+                            const int64_t* medoids, int64_t k, const int64_t* assignment,
+                            double* dist, int32_t* lab, cudaStream_t s);
+cudaError_t launch_seed_step(const double* matrix, bool condensed, int64_t p, int64_t current,
+                             uint8_t* chosen, double* nearest, cudaStream_t s);
+size_t bucket_temp_bytes(int64_t p);
+cudaError_t launch_iota(int32_t* out, int64_t n, cudaStream_t s);
+cudaError_t launch_fill_inf(double* out, int64_t n, cudaStream_t s);
+cudaError_t launch_bucket(const int32_t* lab, const int32_t* perm, const int32_t* iota, int64_t p,
+                          int64_t k, int32_t* keys_a, int32_t* keys_b, int32_t* members,
+                          int32_t* members_perm, int64_t* cb, void* tmp, size_t tmp_bytes,
+                          cudaStream_t s);
+cudaError_t launch_update2(const double* matrix, bool condensed, const double* psq,
+                           const int32_t* pinv, int64_t p, const int32_t* members,
+                           const int32_t* members_perm, const int64_t* cluster_begin,
+                           int64_t k, int64_t* best_member, double* best_sum, cudaStream_t s);
+cudaError_t launch_cluster_layout(const double* sq, int64_t p, int n_anchor, int64_t* anchors,
+                                  double* nearest, double* part_v, int64_t* part_i,
+                                  int64_t* asg_tmp, double* dist_tmp, int32_t* lab,
+                                  int32_t* keys_tmp, const int32_t* iota, int32_t* perm,
+                                  int32_t* pinv, double* psq, void* tmp, size_t tmp_bytes,
+                                  cudaStream_t s);
 
 }  // namespace dtwgpu

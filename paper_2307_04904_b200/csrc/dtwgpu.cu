@@ -67,7 +67,7 @@ int check_band(dtwg_ctx* ctx, int64_t hw, int auto_widen) {
 int ensure_fp32(dtwg_ctx* ctx) {
   if (ctx->have32) return DTWG_OK;
   // the whole guarded buffer, guards included (zeros stay zeros)
-  const int64_t total = ctx->h_offsets[ctx->p] + 2 * kGuard;
+  const int64_t total = ctx->h_offsets[ctx->p] + kGuard + ctx->tail_guard;
   CU(ctx->d_samples32.reserve(total), "cudaMalloc samples32");
   CU(dtwgpu::launch_to_f32(ctx->d_samples.ptr, total, ctx->d_samples32.ptr, ctx->stream),
      "to f32");
@@ -89,7 +89,9 @@ int ensure_band(dtwg_ctx* ctx, bool fp32) {
     pos += ctx->h_len[i] + 2 * pad;
   }
   boff[p] = pos;
-  const int64_t total = pos + pad;
+  // Lanes of a warp run to the warp's longest pair, so a shorter pair's lane streams past
+  // its series' end by up to the longest length: the tail past the last series covers it.
+  const int64_t total = pos + pad + ctx->max_len;
   CU(ctx->d_boffsets.reserve(p + 1), "cudaMalloc boffsets");
   CU(cudaMemcpyAsync(ctx->d_boffsets.ptr, boff.data(), (p + 1) * 8, cudaMemcpyHostToDevice,
                      ctx->stream),
@@ -102,6 +104,9 @@ int ensure_band(dtwg_ctx* ctx, bool fp32) {
     CU(ctx->d_bsamples.reserve(total), "cudaMalloc bsamples");
     out = ctx->d_bsamples.ptr;
   }
+  CU(cudaMemsetAsync(static_cast<char*>(out) + (pos - pad) * (fp32 ? 4 : 8), 0,
+                     (total - (pos - pad)) * (fp32 ? 4 : 8), ctx->stream),
+     "memset band tail");
   CU(dtwgpu::launch_band_pad(ctx->d_samples.ptr + kGuard, ctx->d_offsets.ptr, ctx->d_boffsets.ptr,
                              p, pad, out, fp32, ctx->stream),
      "band pad");
@@ -303,6 +308,7 @@ int ensure_resident(dtwg_ctx* ctx, int64_t p) {
   CU(ctx->d_cond.reserve(total), "cudaMalloc condensed");
   ctx->mat_p = p;
   ctx->square_valid = false;
+  ctx->layout_valid = ctx->layout_tried = false;
   return DTWG_OK;
 }
 
@@ -420,6 +426,24 @@ void dtwg_destroy(dtwg_ctx* ctx) {
   ctx->d_chosen.release();
   ctx->d_members.release();
   ctx->d_sil_cls.release();
+  ctx->d_psq.release();
+  ctx->d_perm.release();
+  ctx->d_pinv.release();
+  ctx->d_anchors.release();
+  ctx->d_fpt_i.release();
+  ctx->d_fpt_v.release();
+  ctx->d_lab.release();
+  ctx->d_keys_a.release();
+  ctx->d_keys_b.release();
+  ctx->d_iota.release();
+  ctx->d_members_p.release();
+  ctx->d_cub.release();
+  for (double*& h : ctx->h_km_dist)
+    if (h) cudaFreeHost(h);
+  if (ctx->h_km_nearest) cudaFreeHost(ctx->h_km_nearest);
+  if (ctx->h_km_best) cudaFreeHost(ctx->h_km_best);
+  if (ctx->h_km_cb) cudaFreeHost(ctx->h_km_cb);
+  if (ctx->h_km_med) cudaFreeHost(ctx->h_km_med);
   ctx->d_strip_base.release();
   ctx->d_prog.release();
   ctx->d_work.release();
@@ -435,6 +459,8 @@ void dtwg_destroy(dtwg_ctx* ctx) {
   if (ctx->fork) cudaEventDestroy(ctx->fork);
   if (ctx->km0) cudaEventDestroy(ctx->km0);
   if (ctx->km1) cudaEventDestroy(ctx->km1);
+  if (ctx->km2) cudaEventDestroy(ctx->km2);
+  if (ctx->km3) cudaEventDestroy(ctx->km3);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -490,16 +516,21 @@ static int upload_begin(dtwg_ctx* ctx, const double* samples, const int64_t* off
     if (ctx->h_len[i] != ctx->h_len[0]) ctx->uniform = false;
   }
   const int64_t n = ctx->h_offsets[p];
+  ctx->max_len = p ? *std::max_element(ctx->h_len.begin(), ctx->h_len.end()) : 0;
+  // Lanes of a warp run to the warp's longest pair and prefetch rows past their own
+  // series' end (unused values): the guard after the last series covers the longest one.
+  ctx->tail_guard = kGuard + ctx->max_len;
   ctx->have32 = false;
   ctx->have_band64 = ctx->have_band32 = false;
   // The plan depends only on the series lengths (and window/precision/range): keep it
   // when a new upload has the same lengths.
   if (ctx->plan_valid && ctx->plan_lens != ctx->h_len) ctx->plan_valid = false;
   if (!ctx->plan_valid) ctx->plan_lens = ctx->h_len;
-  CU(ctx->d_samples.reserve(n + 2 * kGuard), "cudaMalloc samples");
+  CU(ctx->d_samples.reserve(n + kGuard + ctx->tail_guard), "cudaMalloc samples");
   CU(ctx->d_offsets.reserve(p + 1), "cudaMalloc offsets");
   CU(cudaMemsetAsync(ctx->d_samples.ptr, 0, kGuard * sizeof(double), ctx->stream), "memset");
-  CU(cudaMemsetAsync(ctx->d_samples.ptr + kGuard + n, 0, kGuard * sizeof(double), ctx->stream),
+  CU(cudaMemsetAsync(ctx->d_samples.ptr + kGuard + n, 0, ctx->tail_guard * sizeof(double),
+                     ctx->stream),
      "memset");
   CU(cudaMemcpyAsync(ctx->d_samples.ptr + kGuard, samples + base, n * sizeof(double),
                      cudaMemcpyHostToDevice, ctx->stream),
@@ -900,7 +931,24 @@ int dtwg_exchange_complete(dtwg_ctx* ctx) {
   cudaSetDevice(ctx->device);
   ctx->cond_valid = true;
   ctx->square_valid = false;
+  ctx->layout_valid = ctx->layout_tried = false;
   return validate_resident(ctx);  // distance_matrix.hpp:34-38
+}
+int dtwg_download_range(dtwg_ctx* ctx, int64_t b, int64_t e, double* out) {
+  if (!ctx || (!out && e > b)) return DTWG_INVALID_ARGUMENTS;
+  if (!ctx->cond_valid && !ctx->exchange_open)
+    return ctx->fail(DTWG_INVALID_ARGUMENTS, "no resident distance matrix");
+  const int64_t total = ctx->mat_p * (ctx->mat_p - 1) / 2;
+  if (b < 0 || e > total || b > e)
+    return ctx->fail(DTWG_INVALID_ARGUMENTS, "slot range [%lld, %lld) outside [0, %lld)",
+                     (long long)b, (long long)e, (long long)total);
+  cudaSetDevice(ctx->device);
+  if (e > b) {
+    CU(cudaMemcpyAsync(out, ctx->d_cond.ptr + b, (e - b) * 8, cudaMemcpyDeviceToHost, ctx->stream),
+       "D2H");
+    CU(cudaStreamSynchronize(ctx->stream), "sync");
+  }
+  return DTWG_OK;
 }
 
 }  // extern "C"

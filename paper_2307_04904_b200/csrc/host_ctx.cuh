@@ -155,6 +155,8 @@ struct dtwg_ctx {
   int64_t p = 0;
   std::vector<int64_t> h_offsets;
   std::vector<int64_t> h_len;
+  int64_t max_len = 0;
+  int64_t tail_guard = 0;  // zeros after the packed series (>= kGuard + the longest series)
   bool uniform = true;
   DevBuf<double> d_samples;
   DevBuf<float> d_samples32;
@@ -199,9 +201,35 @@ struct dtwg_ctx {
 
   // k-medoids sweep statistics (dtwg_km_stats): device time and algorithmic bytes of the
   // assignment and candidate-sum kernels (8 bytes per distance read).
-  cudaEvent_t km0 = nullptr, km1 = nullptr;
+  cudaEvent_t km0 = nullptr, km1 = nullptr, km2 = nullptr, km3 = nullptr;
   double km_assign_ms = 0, km_update_ms = 0, km_assign_bytes = 0, km_update_bytes = 0;
+  double km_prep_ms = 0;
   int64_t km_sweeps = 0;
+
+  // Cluster-ordered copy of the square (km_host.cu ensure_layout): psq[u][v] =
+  // square[perm[u]][perm[v]] with series grouped by their nearest farthest-point anchor, so
+  // a cluster's members occupy runs of consecutive positions and the candidate sums read
+  // whole sectors. Built once per resident matrix when two squares fit in HBM.
+  DevBuf<double> d_psq;
+  DevBuf<int32_t> d_perm, d_pinv;
+  bool layout_valid = false;  // d_psq/d_perm/d_pinv match the square
+  bool layout_tried = false;  // decided for this square (built, or skipped: p small / no room)
+  DevBuf<int64_t> d_anchors, d_fpt_i;
+  DevBuf<double> d_fpt_v;
+
+  // Device-side bucketing (kmedoids.hpp:86-92): slot per series, radix-sort keys, iota,
+  // members in layout order, cub temporary storage.
+  DevBuf<int32_t> d_lab, d_keys_a, d_keys_b, d_iota, d_members_p;
+  DevBuf<uint8_t> d_cub;
+  size_t cub_bytes = 0;
+  int64_t iota_n = 0;
+  // Pinned host staging for the per-sweep and per-seed-step copies.
+  double* h_km_dist[2] = {nullptr, nullptr};
+  double* h_km_nearest = nullptr;
+  int64_t* h_km_best = nullptr;
+  int64_t* h_km_cb = nullptr;
+  int64_t* h_km_med = nullptr;
+  int64_t h_km_p = 0, h_km_k = 0;
 
   // k-medoids scratch
   DevBuf<int64_t> d_medoids, d_assign, d_best_member, d_cb;

@@ -5,6 +5,8 @@
 // on restart-worker contexts and, for multi-device contexts, on several GPUs.
 #include "host_ctx.cuh"
 
+#include <chrono>
+
 namespace dtwgpu {
 namespace host {
 
@@ -34,6 +36,7 @@ int ensure_square(dtwg_ctx* ctx) {
     return DTWG_OK;
   }
   CU(ctx->d_square.reserve((size_t)(p * p)), "cudaMalloc square");
+  const auto t0 = std::chrono::steady_clock::now();
   if (p >= 2) {
     CU(dtwgpu::launch_expand_square(ctx->d_cond.ptr, p, ctx->d_square.ptr, ctx->stream),
        "expand");
@@ -42,114 +45,181 @@ int ensure_square(dtwg_ctx* ctx) {
     CU(cudaMemsetAsync(ctx->d_square.ptr, 0, sizeof(double), ctx->stream), "memset");
   }
   ctx->square_valid = true;
+  CU(cudaStreamSynchronize(ctx->stream), "sync");
+  ctx->km_prep_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return DTWG_OK;
+}
+
+int ensure_iota(dtwg_ctx* ctx, int64_t p);
+
+// ---- cluster-ordered layout --------------------------------------------------------
+// The medoid update reads, for every candidate, its row at its cluster's member columns
+// (sum over clusters of |C|^2 distances). Members of a cluster are scattered over the
+// row, so in the plain square every 8-byte read costs a whole 32-byte sector (round 1:
+// ~15x the algorithmic bytes). ensure_layout builds once per resident matrix a copy of
+// the square with the series grouped by their nearest farthest-point anchor (n_anchor
+// = k anchors, deterministic, all on the device): members of a cluster then occupy runs
+// of consecutive positions. It only moves data -- the candidate sums read the same
+// doubles, and the contenders' exact sums keep reading the plain square in ascending
+// member order -- so results are bit-identical with or without it. Skipped for small p
+// (nothing to gain), in condensed mode, and when a second square does not fit in HBM.
+int ensure_layout(dtwg_ctx* ctx, int64_t k) {
+  if (ctx->layout_tried) return DTWG_OK;
+  ctx->layout_tried = true;
+  ctx->layout_valid = false;
+  const int64_t p = ctx->mat_p;
+  const int64_t min_p = env_or("DTWGPU_KM_LAYOUT_MIN_P", 4096);
+  if (ctx->km_condensed || p < std::max<int64_t>(min_p, 2) || env_or("DTWGPU_KM_LAYOUT", 1) == 0)
+    return DTWG_OK;
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const double need = double(p) * double(p) * 8.0 - double(ctx->d_psq.cap) * 8.0;
+  if (need > 0.8 * double(free_b)) return DTWG_OK;
+  const int na = (int)std::min<int64_t>(std::max<int64_t>(k, 2), std::min<int64_t>(p, 256));
+  const int nblk = (int)std::min<int64_t>((p + 255) / 256, 1024);
+  CU(ctx->d_psq.reserve((size_t)(p * p)), "cudaMalloc layout square");
+  CU(ctx->d_perm.reserve(p), "malloc");
+  CU(ctx->d_pinv.reserve(p), "malloc");
+  CU(ctx->d_anchors.reserve(na), "malloc");
+  CU(ctx->d_fpt_v.reserve(nblk), "malloc");
+  CU(ctx->d_fpt_i.reserve(nblk), "malloc");
+  CU(ctx->d_nearest.reserve(p), "malloc");
+  CU(ctx->d_assign.reserve(p), "malloc");
+  CU(ctx->d_dist.reserve(p), "malloc");
+  CU(ctx->d_lab.reserve(p), "malloc");
+  CU(ctx->d_keys_a.reserve(p), "malloc");
+  int rc = ensure_iota(ctx, p);
+  if (rc) return rc;
+  const auto t0 = std::chrono::steady_clock::now();
+  CU(dtwgpu::launch_cluster_layout(ctx->d_square.ptr, p, na, ctx->d_anchors.ptr,
+                                   ctx->d_nearest.ptr, ctx->d_fpt_v.ptr, ctx->d_fpt_i.ptr,
+                                   ctx->d_assign.ptr, ctx->d_dist.ptr, ctx->d_lab.ptr,
+                                   ctx->d_keys_a.ptr, ctx->d_iota.ptr, ctx->d_perm.ptr,
+                                   ctx->d_pinv.ptr, ctx->d_psq.ptr, ctx->d_cub.ptr, ctx->cub_bytes,
+                                   ctx->stream),
+     "cluster layout");
+  ctx->launches += 2 * (na - 1) + 4;
+  CU(cudaStreamSynchronize(ctx->stream), "sync");
+  ctx->km_prep_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  ctx->layout_valid = true;
   return DTWG_OK;
 }
 
 // ---- k-medoids host loop ------------------------------------------------------------
+// One sweep is enqueued as: H2D medoids -> assign_slots (assignment, distance, cluster
+// slot) -> device bucketing (stable radix sort by slot; the cluster bounds) -> candidate
+// sums and per-cluster selection -> one D2H of the distances, bounds and winners into
+// pinned buffers. The host then waits once, repairs/dedupes (O(k log k); O(p) only for an
+// empty cluster) and launches the next sweep before it sums the previous assignment's cost
+// in ascending order, so that sequential sum overlaps the GPU.
 struct KmState {
-  dtwg_ctx* ctx;
+  dtwg_ctx* ctx;  // this worker's stream and sweep buffers
   int64_t p, k;
-  std::vector<int64_t> assignment;
-  std::vector<double> dist;
+  const double* sq;      // sweep view (square or condensed)
+  bool cond;             // sweep view is the condensed matrix
+  const double* psq;     // cluster-ordered copy (nullptr: none)
+  const int32_t* perm;   // its order
+  const int32_t* pinv;
+  int buf = 0;           // pinned distance buffer of the sweep in flight
 };
 
-int km_assign(KmState& S, const std::vector<int64_t>& medoids) {
+int km_enqueue_assign(KmState& S, const std::vector<int64_t>& medoids) {
   dtwg_ctx* ctx = S.ctx;
-  CU(cudaMemcpyAsync(ctx->d_medoids.ptr, medoids.data(), medoids.size() * 8,
+  std::copy(medoids.begin(), medoids.end(), ctx->h_km_med);
+  CU(cudaMemcpyAsync(ctx->d_medoids.ptr, ctx->h_km_med, medoids.size() * 8,
                      cudaMemcpyHostToDevice, ctx->stream),
      "H2D medoids");
   CU(cudaEventRecord(ctx->km0, ctx->stream), "event");
-  CU(dtwgpu::launch_assign(km_matrix(ctx), km_is_cond(ctx), S.p, ctx->d_medoids.ptr,
-                           (int64_t)medoids.size(),
-                           ctx->d_assign.ptr, ctx->d_dist.ptr, ctx->stream),
+  CU(dtwgpu::launch_assign_slots(S.sq, S.cond, S.p, ctx->d_medoids.ptr, (int64_t)medoids.size(),
+                                 ctx->d_assign.ptr, ctx->d_dist.ptr, ctx->d_lab.ptr, ctx->stream),
      "assign");
-  CU(cudaEventRecord(ctx->km1, ctx->stream), "event");
   ctx->launches++;
-  S.assignment.resize(S.p);
-  S.dist.resize(S.p);
-  CU(cudaMemcpyAsync(S.assignment.data(), ctx->d_assign.ptr, S.p * 8, cudaMemcpyDeviceToHost,
-                     ctx->stream),
-     "D2H assignment");
-  CU(cudaMemcpyAsync(S.dist.data(), ctx->d_dist.ptr, S.p * 8, cudaMemcpyDeviceToHost,
+  return DTWG_OK;
+}
+
+// assignment + update of one sweep, results to the pinned buffers (dist into buf)
+int km_enqueue_sweep(KmState& S, const std::vector<int64_t>& medoids, int buf) {
+  dtwg_ctx* ctx = S.ctx;
+  const int64_t p = S.p, k = (int64_t)medoids.size();
+  int rc = km_enqueue_assign(S, medoids);
+  if (rc) return rc;
+  CU(cudaEventRecord(ctx->km1, ctx->stream), "event");
+  CU(cudaEventRecord(ctx->km2, ctx->stream), "event");
+  CU(dtwgpu::launch_bucket(ctx->d_lab.ptr, S.psq ? S.perm : nullptr, ctx->d_iota.ptr, p, k,
+                           ctx->d_keys_a.ptr, ctx->d_keys_b.ptr, ctx->d_members.ptr,
+                           ctx->d_members_p.ptr, ctx->d_cb.ptr, ctx->d_cub.ptr, ctx->cub_bytes,
+                           ctx->stream),
+     "bucket");
+  CU(dtwgpu::launch_update2(S.sq, S.cond, S.psq, S.pinv, p, ctx->d_members.ptr,
+                            ctx->d_members_p.ptr, ctx->d_cb.ptr, k, ctx->d_best_member.ptr,
+                            ctx->d_best_sum.ptr, ctx->stream),
+     "update");
+  CU(cudaEventRecord(ctx->km3, ctx->stream), "event");
+  ctx->launches += S.psq ? 6 : 4;
+  CU(cudaMemcpyAsync(ctx->h_km_dist[buf], ctx->d_dist.ptr, p * 8, cudaMemcpyDeviceToHost,
                      ctx->stream),
      "D2H dist");
+  CU(cudaMemcpyAsync(ctx->h_km_cb, ctx->d_cb.ptr, (k + 1) * 8, cudaMemcpyDeviceToHost,
+                     ctx->stream),
+     "D2H cb");
+  CU(cudaMemcpyAsync(ctx->h_km_best, ctx->d_best_member.ptr, k * 8, cudaMemcpyDeviceToHost,
+                     ctx->stream),
+     "D2H best");
+  return DTWG_OK;
+}
+
+int km_wait_sweep(KmState& S) {
+  dtwg_ctx* ctx = S.ctx;
   CU(cudaStreamSynchronize(ctx->stream), "sync");
-  float ms = 0;
+  float ms = 0, ms2 = 0;
   CU(cudaEventElapsedTime(&ms, ctx->km0, ctx->km1), "elapsed");
+  CU(cudaEventElapsedTime(&ms2, ctx->km2, ctx->km3), "elapsed");
+  const int64_t k = S.k;
+  double sq = 0;
+  for (int64_t c = 0; c < k; ++c) {
+    const double n = double(ctx->h_km_cb[c + 1] - ctx->h_km_cb[c]);
+    sq += n * n;
+  }
   ctx->km_assign_ms += ms;
-  ctx->km_assign_bytes += 8.0 * (double)S.p * (double)medoids.size() + 16.0 * (double)S.p;
+  ctx->km_assign_bytes += 8.0 * (double)S.p * (double)k + 20.0 * (double)S.p;
+  ctx->km_update_ms += ms2;
+  ctx->km_update_bytes += 8.0 * sq + 12.0 * (double)S.p;
+  ctx->km_sweeps += 1;
   return DTWG_OK;
 }
 
 // cluster_result.hpp:65-72 -- ascending-j sequential sum on the host.
-double km_cost(const KmState& S) {
+double km_cost(const double* dist, int64_t p) {
   double total = 0.0;
-  for (int64_t j = 0; j < S.p; ++j) total += S.dist[j];
+  for (int64_t j = 0; j < p; ++j) total += dist[j];
   return total;
 }
 
-// kmedoids.hpp:84-139.
-int km_update(KmState& S, const std::vector<int64_t>& medoids, std::vector<int64_t>& updated) {
-  dtwg_ctx* ctx = S.ctx;
+// kmedoids.hpp:94-137 from the sweep's winners: empty clusters take the worst-served
+// non-medoid (strict >, from the assignment distances), then sort, unique and refill.
+void km_finish_update(const KmState& S, const std::vector<int64_t>& medoids, const double* dist,
+                      std::vector<int64_t>& updated) {
+  const dtwg_ctx* ctx = S.ctx;
   const int64_t p = S.p, k = (int64_t)medoids.size();
-  // Stable bucket by lower_bound slot (kmedoids.hpp:88-92).
-  std::vector<int64_t> cb(k + 1, 0);
-  std::vector<int64_t> slot_of(p);
-  for (int64_t j = 0; j < p; ++j) {
-    const int64_t c = std::lower_bound(medoids.begin(), medoids.end(), S.assignment[j]) -
-                      medoids.begin();
-    slot_of[j] = c;
-    cb[c + 1]++;
-  }
-  for (int64_t c = 0; c < k; ++c) cb[c + 1] += cb[c];
-  std::vector<int32_t> members(p);
-  {
-    std::vector<int64_t> fill(cb.begin(), cb.end() - 1);
-    for (int64_t j = 0; j < p; ++j) members[fill[slot_of[j]]++] = (int32_t)j;
-  }
-  CU(cudaMemcpyAsync(ctx->d_members.ptr, members.data(), p * 4, cudaMemcpyHostToDevice,
-                     ctx->stream),
-     "H2D members");
-  CU(cudaMemcpyAsync(ctx->d_cb.ptr, cb.data(), (k + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
-     "H2D cb");
-  CU(cudaEventRecord(ctx->km0, ctx->stream), "event");
-  CU(dtwgpu::launch_update(km_matrix(ctx), km_is_cond(ctx), p, ctx->d_members.ptr, ctx->d_cb.ptr, k,
-                           ctx->d_best_member.ptr, ctx->d_best_sum.ptr, ctx->stream),
-     "update");
-  CU(cudaEventRecord(ctx->km1, ctx->stream), "event");
-  ctx->launches += 2;
-  std::vector<int64_t> best(k);
-  CU(cudaMemcpyAsync(best.data(), ctx->d_best_member.ptr, k * 8, cudaMemcpyDeviceToHost,
-                     ctx->stream),
-     "D2H best");
-  CU(cudaStreamSynchronize(ctx->stream), "sync");
-  {
-    float ms = 0;
-    CU(cudaEventElapsedTime(&ms, ctx->km0, ctx->km1), "elapsed");
-    double sq = 0;
-    for (int64_t c = 0; c < k; ++c) sq += double(cb[c + 1] - cb[c]) * double(cb[c + 1] - cb[c]);
-    ctx->km_update_ms += ms;
-    ctx->km_update_bytes += 8.0 * sq + 12.0 * (double)p;
-    ctx->km_sweeps += 1;
-  }
-
   updated.assign(k, 0);
+  int64_t worst = -2;  // computed once: the same for every empty cluster
   for (int64_t c = 0; c < k; ++c) {
-    if (cb[c] == cb[c + 1]) {  // kmedoids.hpp:97-109: worst-served non-medoid, strict >
-      int64_t worst = medoids[c];
-      double worst_d = -1.0;
-      for (int64_t j = 0; j < p; ++j) {
-        if (std::find(medoids.begin(), medoids.end(), j) != medoids.end()) continue;
-        const double d = S.dist[j];  // == D(j, assignment[j])
-        if (d > worst_d) {
-          worst_d = d;
-          worst = j;
+    if (ctx->h_km_cb[c] == ctx->h_km_cb[c + 1]) {  // kmedoids.hpp:97-109
+      if (worst == -2) {
+        worst = medoids[c];
+        double worst_d = -1.0;
+        for (int64_t j = 0; j < p; ++j) {
+          if (std::binary_search(medoids.begin(), medoids.end(), j)) continue;
+          if (dist[j] > worst_d) {  // dist[j] == D(j, assignment[j])
+            worst_d = dist[j];
+            worst = j;
+          }
         }
       }
-      updated[c] = worst;
+      updated[c] = worst < 0 ? medoids[c] : worst;
       continue;
     }
-    updated[c] = best[c];
+    updated[c] = ctx->h_km_best[c];
   }
   std::sort(updated.begin(), updated.end());
   updated.erase(std::unique(updated.begin(), updated.end()), updated.end());
@@ -164,53 +234,43 @@ int km_update(KmState& S, const std::vector<int64_t>& medoids, std::vector<int64
     }
     std::sort(updated.begin(), updated.end());
   }
-  return DTWG_OK;
 }
 
-// kmedoids.hpp:33-79.
+// kmedoids.hpp:33-79. The device refreshes nearest[] (and marks the new seed chosen); the
+// host keeps the reference's sequential weight sum -- stored as running prefixes, since
+// the draw's accumulation repeats exactly the same additions, the draw is then the first
+// prefix above the target (prefixes of non-negative terms never decrease).
 int km_seeds(KmState& S, int64_t k, SplitMix64& rng, std::vector<int64_t>& medoids) {
   dtwg_ctx* ctx = S.ctx;
   const int64_t p = S.p;
   medoids.clear();
   std::vector<uint8_t> chosen(p, 0);
-  std::vector<double> nearest(p, kInf);
+  std::vector<double> pre(p);
   CU(cudaMemsetAsync(ctx->d_chosen.ptr, 0, p, ctx->stream), "memset chosen");
-  CU(cudaMemcpyAsync(ctx->d_nearest.ptr, nearest.data(), p * 8, cudaMemcpyHostToDevice,
-                     ctx->stream),
-     "H2D nearest");
+  CU(dtwgpu::launch_fill_inf(ctx->d_nearest.ptr, p, ctx->stream), "fill nearest");
   int64_t current = (int64_t)rng.next_below((uint64_t)p);
   while ((int64_t)medoids.size() < k) {
     medoids.push_back(current);
     chosen[current] = 1;
     if ((int64_t)medoids.size() == k) break;
-    CU(cudaMemcpyAsync(ctx->d_chosen.ptr + current, &chosen[current], 1, cudaMemcpyHostToDevice,
-                       ctx->stream),
-       "H2D chosen");
-    CU(dtwgpu::launch_nearest_update(km_matrix(ctx), km_is_cond(ctx), p, current, ctx->d_chosen.ptr,
-                                     ctx->d_nearest.ptr, ctx->stream),
+    CU(dtwgpu::launch_seed_step(S.sq, S.cond, p, current, ctx->d_chosen.ptr, ctx->d_nearest.ptr,
+                                ctx->stream),
        "nearest");
     ctx->launches++;
-    CU(cudaMemcpyAsync(nearest.data(), ctx->d_nearest.ptr, p * 8, cudaMemcpyDeviceToHost,
+    CU(cudaMemcpyAsync(ctx->h_km_nearest, ctx->d_nearest.ptr, p * 8, cudaMemcpyDeviceToHost,
                        ctx->stream),
        "D2H nearest");
     CU(cudaStreamSynchronize(ctx->stream), "sync");
+    const double* nearest = ctx->h_km_nearest;
     double total = 0.0;
     for (int64_t j = 0; j < p; ++j) {
-      if (chosen[j]) continue;
-      total += nearest[j];
+      if (!chosen[j]) total += nearest[j];
+      pre[j] = total;
     }
     int64_t next = p;
     if (total > 0.0) {
       const double target = rng.next_double() * total;
-      double acc = 0.0;
-      for (int64_t j = 0; j < p; ++j) {
-        if (chosen[j]) continue;
-        acc += nearest[j];
-        if (acc > target) {
-          next = j;
-          break;
-        }
-      }
+      next = std::upper_bound(pre.begin(), pre.end(), target) - pre.begin();
     }
     if (next == p) {
       for (int64_t j = 0; j < p; ++j) {
@@ -226,11 +286,52 @@ int km_seeds(KmState& S, int64_t k, SplitMix64& rng, std::vector<int64_t>& medoi
   return DTWG_OK;
 }
 
+int ensure_iota(dtwg_ctx* ctx, int64_t p) {
+  if (ctx->iota_n < p) {
+    CU(ctx->d_iota.reserve(p), "malloc");
+    CU(dtwgpu::launch_iota(ctx->d_iota.ptr, p, ctx->stream), "iota");
+    ctx->iota_n = p;
+  }
+  const size_t need = dtwgpu::bucket_temp_bytes(p);
+  if (ctx->cub_bytes < need) {
+    CU(ctx->d_cub.reserve(need), "malloc");
+    ctx->cub_bytes = need;
+  }
+  return DTWG_OK;
+}
+
 int km_reserve(dtwg_ctx* ctx, int64_t p, int64_t k) {
   if (!ctx->km0) {
     CU(cudaEventCreate(&ctx->km0), "event");
     CU(cudaEventCreate(&ctx->km1), "event");
+    CU(cudaEventCreate(&ctx->km2), "event");
+    CU(cudaEventCreate(&ctx->km3), "event");
   }
+  if (ctx->h_km_p < p) {
+    for (double*& h : ctx->h_km_dist) {
+      if (h) cudaFreeHost(h);
+      h = nullptr;
+      CU(cudaMallocHost(&h, std::max<int64_t>(p, 1) * 8), "pinned");
+    }
+    if (ctx->h_km_nearest) cudaFreeHost(ctx->h_km_nearest);
+    ctx->h_km_nearest = nullptr;
+    CU(cudaMallocHost(&ctx->h_km_nearest, std::max<int64_t>(p, 1) * 8), "pinned");
+    ctx->h_km_p = p;
+  }
+  if (ctx->h_km_k < k) {
+    for (int64_t** h : {&ctx->h_km_best, &ctx->h_km_cb, &ctx->h_km_med}) {
+      if (*h) cudaFreeHost(*h);
+      *h = nullptr;
+      CU(cudaMallocHost(h, (k + 1) * 8), "pinned");
+    }
+    ctx->h_km_k = k;
+  }
+  CU(ctx->d_lab.reserve(p), "malloc");
+  CU(ctx->d_keys_a.reserve(p), "malloc");
+  CU(ctx->d_keys_b.reserve(p), "malloc");
+  CU(ctx->d_members_p.reserve(p), "malloc");
+  int rc = ensure_iota(ctx, p);
+  if (rc) return rc;
   CU(ctx->d_medoids.reserve(k), "malloc");
   CU(ctx->d_assign.reserve(p), "malloc");
   CU(ctx->d_dist.reserve(p), "malloc");
@@ -316,7 +417,10 @@ int dtwg_km_stats(dtwg_ctx* ctx, double* out, int reset) {
   out[2] = ctx->km_assign_bytes;
   out[3] = ctx->km_update_ms;
   out[4] = ctx->km_update_bytes;
+  out[5] = ctx->km_prep_ms;
+  out[6] = ctx->layout_valid ? 1.0 : 0.0;
   if (reset) {
+    ctx->km_prep_ms = 0;
     ctx->km_sweeps = 0;
     ctx->km_assign_ms = ctx->km_update_ms = ctx->km_assign_bytes = ctx->km_update_bytes = 0;
   }
@@ -416,12 +520,17 @@ static int km_run(dtwg_ctx* ctx, int64_t k, int64_t restarts, int64_t max_iterat
     return ctx->fail(DTWG_INVALID_ARGUMENTS, "empty restart range");
   int rc = ensure_square(ctx);
   if (rc) return rc;
+  rc = km_reserve(ctx, p, k);
+  if (rc) return rc;
+  rc = ensure_layout(ctx, k);
+  if (rc) return rc;
   // Independent restarts run concurrently: contiguous restart blocks on restart workers
   // (same device, own streams), observer calls replayed and the best restart reduced in
   // restart order with strict < -- the sequential loop's result, bit for bit.
   const int64_t nr = restart_end - restart_begin;
   // (small matrices: a restart is a few tens of microseconds, less than a thread hand-off)
-  const int64_t cap = p >= 2048 ? 8 : 1;
+  const int64_t hw = (int64_t)std::max(1u, std::thread::hardware_concurrency());
+  const int64_t cap = p >= 2048 ? std::min<int64_t>(std::max<int64_t>(hw - 2, 1), 10) : 1;
   const int nw = (int)std::min<int64_t>(nr, std::max<int64_t>(1, env_or("DTWGPU_KM_WORKERS", cap)));
   if (nw <= 1)
     return km_loop(ctx, p, k, max_iterations, seed, restart_begin, restart_end, observer, user,
@@ -494,6 +603,18 @@ static int km_run(dtwg_ctx* ctx, int64_t k, int64_t restarts, int64_t max_iterat
   return DTWG_OK;
 }
 
+// The matrix views a context's sweeps read: its own, or (restart workers) the source's.
+static KmState km_state(dtwg_ctx* ctx, int64_t p, int64_t k) {
+  const dtwg_ctx* m = ctx->km_src ? ctx->km_src : ctx;
+  KmState S{ctx, p, k, km_matrix(ctx), km_is_cond(ctx), nullptr, nullptr, nullptr, 0};
+  if (m->layout_valid) {
+    S.psq = m->d_psq.ptr;
+    S.perm = m->d_perm.ptr;
+    S.pinv = m->d_pinv.ptr;
+  }
+  return S;
+}
+
 // The reference's restart loop (kmedoids.hpp:158-187) over restarts [restart_begin,
 // restart_end) on one context's stream and sweep buffers.
 static int km_loop(dtwg_ctx* ctx, int64_t p, int64_t k, int64_t max_iterations, uint64_t seed,
@@ -502,7 +623,7 @@ static int km_loop(dtwg_ctx* ctx, int64_t p, int64_t k, int64_t max_iterations, 
                    int64_t* best_restart_out) {
   int rc = km_reserve(ctx, p, k);
   if (rc) return rc;
-  KmState S{ctx, p, k, {}, {}};
+  KmState S = km_state(ctx, p, k);
   bool have_best = false;
   double best_cost = 0.0;
   std::vector<int64_t> medoids, updated;
@@ -512,26 +633,44 @@ static int km_loop(dtwg_ctx* ctx, int64_t p, int64_t k, int64_t max_iterations, 
     if (rc) return rc;
     double cost = 0.0;
     bool converged = false;
+    int buf = 0;
+    rc = km_enqueue_sweep(S, medoids, buf);
+    if (rc) return rc;
     for (int64_t it = 0; it < max_iterations && !converged; ++it) {
-      rc = km_assign(S, medoids);
+      rc = km_wait_sweep(S);  // assignment of `medoids` and its update are on the host now
       if (rc) return rc;
-      cost = km_cost(S);
+      const double* dist = ctx->h_km_dist[buf];
+      km_finish_update(S, medoids, dist, updated);
+      converged = updated == medoids;
+      // the next sweep runs while the host sums this assignment's cost
+      const bool more = !converged && it + 1 < max_iterations;
+      if (more) {
+        rc = km_enqueue_sweep(S, updated, buf ^ 1);
+        if (rc) return rc;
+      }
+      cost = km_cost(dist, p);  // cluster_result.hpp:65-72
       if (observer) observer(user, r, it, cost);
-      rc = km_update(S, medoids, updated);
-      if (rc) return rc;
-      if (updated == medoids) converged = true;
-      else medoids = updated;
+      if (!converged) {
+        medoids = updated;
+        buf ^= 1;
+      }
     }
-    if (!converged) {
-      rc = km_assign(S, medoids);
+    if (!converged) {  // iteration cap hit right after an update (kmedoids.hpp:177-180)
+      rc = km_enqueue_assign(S, medoids);
       if (rc) return rc;
-      cost = km_cost(S);
+      CU(cudaMemcpyAsync(ctx->h_km_dist[buf], ctx->d_dist.ptr, p * 8, cudaMemcpyDeviceToHost,
+                         ctx->stream),
+         "D2H dist");
+      CU(cudaStreamSynchronize(ctx->stream), "sync");
+      cost = km_cost(ctx->h_km_dist[buf], p);
     }
     if (!have_best || cost < best_cost) {
       best_cost = cost;
       have_best = true;
       if (medoids_out) std::copy(medoids.begin(), medoids.end(), medoids_out);
-      if (assignment_out) std::copy(S.assignment.begin(), S.assignment.end(), assignment_out);
+      if (assignment_out)
+        CU(cudaMemcpy(assignment_out, ctx->d_assign.ptr, p * 8, cudaMemcpyDeviceToHost),
+           "D2H assignment");
       if (best_restart_out) *best_restart_out = r;
     }
   }
@@ -576,12 +715,18 @@ int dtwg_km_assign(dtwg_ctx* ctx, const int64_t* medoids, int64_t k, int64_t* as
   if (k < 1 || k > p) return ctx->fail(DTWG_K_OUT_OF_RANGE, "k=%lld is outside [1, p]", (long long)k);
   rc = km_reserve(ctx, p, k);
   if (rc) return rc;
-  KmState S{ctx, p, k, {}, {}};
+  KmState S = km_state(ctx, p, k);
   std::vector<int64_t> med(medoids, medoids + k);
-  rc = km_assign(S, med);
+  rc = km_enqueue_assign(S, med);
   if (rc) return rc;
-  if (assignment_out) std::copy(S.assignment.begin(), S.assignment.end(), assignment_out);
-  if (dist_out) std::copy(S.dist.begin(), S.dist.end(), dist_out);
+  if (assignment_out)
+    CU(cudaMemcpyAsync(assignment_out, ctx->d_assign.ptr, p * 8, cudaMemcpyDeviceToHost,
+                       ctx->stream),
+       "D2H assignment");
+  if (dist_out)
+    CU(cudaMemcpyAsync(dist_out, ctx->d_dist.ptr, p * 8, cudaMemcpyDeviceToHost, ctx->stream),
+       "D2H dist");
+  CU(cudaStreamSynchronize(ctx->stream), "sync");
   return DTWG_OK;
 }
 
@@ -595,28 +740,44 @@ int dtwg_km_update(dtwg_ctx* ctx, const int64_t* medoids, int64_t k, const int64
   if (k < 1 || k > p) return ctx->fail(DTWG_K_OUT_OF_RANGE, "k=%lld is outside [1, p]", (long long)k);
   rc = km_reserve(ctx, p, k);
   if (rc) return rc;
-  KmState S{ctx, p, k, {}, {}};
+  for (int64_t j = 0; j < p; ++j)
+    if (assignment[j] < 0 || assignment[j] >= p)
+      return ctx->fail(DTWG_INDEX_OUT_OF_RANGE, "assignment out of range");
+  KmState S = km_state(ctx, p, k);
   std::vector<int64_t> med(medoids, medoids + k);
-  // Needs D(j, assignment[j]) for the empty-cluster repair: one assign-side gather.
-  S.assignment.assign(assignment, assignment + p);
-  S.dist.resize(p);
-  {
-    // dist[j] = D(j, assignment[j]) from the dense matrix rows.
-    std::vector<double> row(p);
-    for (int64_t j = 0; j < p; ++j) {
-      const int64_t a = assignment[j];
-      if (a < 0 || a >= p) return ctx->fail(DTWG_INDEX_OUT_OF_RANGE, "assignment out of range");
-      if (a == j) {
-        S.dist[j] = 0.0;
-        continue;
-      }
-      CU(cudaMemcpy(&S.dist[j], ctx->d_square.ptr + a * p + j, 8, cudaMemcpyDeviceToHost),
-         "D2H entry");
-    }
-  }
+  // The caller's assignment (any, not necessarily nearest-medoid): cluster slots by
+  // lower_bound (kmedoids.hpp:88-90) and D(j, assignment[j]) for the empty-cluster repair.
+  CU(ctx->d_assign.reserve(p), "malloc");
+  std::copy(med.begin(), med.end(), ctx->h_km_med);
+  CU(cudaMemcpyAsync(ctx->d_medoids.ptr, ctx->h_km_med, k * 8, cudaMemcpyHostToDevice, ctx->stream),
+     "H2D medoids");
+  CU(cudaMemcpyAsync(ctx->d_assign.ptr, assignment, p * 8, cudaMemcpyHostToDevice, ctx->stream),
+     "H2D assignment");
+  CU(dtwgpu::launch_slots_of(S.sq, S.cond, p, ctx->d_medoids.ptr, k, ctx->d_assign.ptr,
+                             ctx->d_dist.ptr, ctx->d_lab.ptr, ctx->stream),
+     "slots");
+  CU(cudaEventRecord(ctx->km2, ctx->stream), "event");
+  CU(dtwgpu::launch_bucket(ctx->d_lab.ptr, S.psq ? S.perm : nullptr, ctx->d_iota.ptr, p, k,
+                           ctx->d_keys_a.ptr, ctx->d_keys_b.ptr, ctx->d_members.ptr,
+                           ctx->d_members_p.ptr, ctx->d_cb.ptr, ctx->d_cub.ptr, ctx->cub_bytes,
+                           ctx->stream),
+     "bucket");
+  CU(dtwgpu::launch_update2(S.sq, S.cond, S.psq, S.pinv, p, ctx->d_members.ptr,
+                            ctx->d_members_p.ptr, ctx->d_cb.ptr, k, ctx->d_best_member.ptr,
+                            ctx->d_best_sum.ptr, ctx->stream),
+     "update");
+  CU(cudaEventRecord(ctx->km3, ctx->stream), "event");
+  ctx->launches += S.psq ? 7 : 5;
+  CU(cudaMemcpyAsync(ctx->h_km_dist[0], ctx->d_dist.ptr, p * 8, cudaMemcpyDeviceToHost, ctx->stream),
+     "D2H dist");
+  CU(cudaMemcpyAsync(ctx->h_km_cb, ctx->d_cb.ptr, (k + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream),
+     "D2H cb");
+  CU(cudaMemcpyAsync(ctx->h_km_best, ctx->d_best_member.ptr, k * 8, cudaMemcpyDeviceToHost,
+                     ctx->stream),
+     "D2H best");
+  CU(cudaStreamSynchronize(ctx->stream), "sync");
   std::vector<int64_t> upd;
-  rc = km_update(S, med, upd);
-  if (rc) return rc;
+  km_finish_update(S, med, ctx->h_km_dist[0], upd);
   std::copy(upd.begin(), upd.end(), updated_out);
   return DTWG_OK;
 }

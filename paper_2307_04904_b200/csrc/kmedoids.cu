@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cub/device/device_radix_sort.cuh>
 #include <math_constants.h>
 
 #include <cstdint>
@@ -339,6 +340,293 @@ __global__ void silhouette_kernel(const V D, int64_t p,
   }
 }
 
+
+// ---- sweep kernels, round 2 -----------------------------------------------------------
+// cluster_result.hpp:40-61, one block per 32 consecutive series j: warp w of the block's
+// 8 takes the medoids t = w, w+8, w+16, ... (4 independent row loads in flight per lane,
+// every load a coalesced 256-byte row segment D(m_t, j0..j0+31)); the 8 per-warp minima
+// are then merged in shared memory by (distance, t) -- the lowest t among equal
+// distances, which is exactly what the reference's ascending-t scan with strict < keeps.
+// A medoid owns itself. Besides the assignment and its distance, the kernel writes the
+// cluster slot t (medoids ascending: slot = lower_bound(medoids, assignment[j]),
+// kmedoids.hpp:88-90) for the device-side bucketing that follows.
+template <class V>
+__global__ void __launch_bounds__(256) assign_slots_kernel(
+    const V D, int64_t p, const int64_t* __restrict__ medoids, int64_t k,
+    int64_t* __restrict__ assignment, double* __restrict__ dist, int32_t* __restrict__ lab) {
+  __shared__ double sd[8][32];
+  __shared__ int st[8][32];
+  __shared__ int sm[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t j0 = (int64_t)blockIdx.x * 32; j0 < p; j0 += (int64_t)gridDim.x * 32) {
+    const int64_t j = j0 + lane;
+    const bool in = j < p;
+    double bd = CUDART_INF;
+    int bt = -1, med = -1;
+    for (int64_t t = w; t < k; t += 32) {
+      int64_t m[4];
+      double d[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t tt = t + 8 * u;
+        m[u] = tt < k ? __ldg(medoids + tt) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) d[u] = (m[u] >= 0 && in) ? D(m[u], j) : CUDART_INF;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (m[u] < 0) continue;
+        if (m[u] == j) med = (int)(t + 8 * u);
+        if (bt < 0 || d[u] < bd) {  // t ascending within the warp: strict < keeps the first
+          bd = d[u];
+          bt = (int)(t + 8 * u);
+        }
+      }
+    }
+    sd[w][lane] = bd;
+    st[w][lane] = bt;
+    sm[w][lane] = med;
+    __syncthreads();
+    if (w == 0 && in) {
+      double b = CUDART_INF;
+      int tb = -1, md = -1;
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {
+        if (sm[x][lane] >= 0) md = sm[x][lane];
+        const int tx = st[x][lane];
+        const double vx = sd[x][lane];
+        if (tx >= 0 && (tb < 0 || vx < b || (vx == b && tx < tb))) {
+          b = vx;
+          tb = tx;
+        }
+      }
+      if (md >= 0) {
+        assignment[j] = j;
+        dist[j] = 0.0;
+        lab[j] = md;
+      } else {
+        assignment[j] = __ldg(medoids + tb);
+        dist[j] = b;
+        lab[j] = tb;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// kmedoids.hpp:88-90 for a caller-given assignment (dtwg_km_update): the cluster slot
+// lower_bound(medoids, assignment[j]) and D(j, assignment[j]).
+template <class V>
+__global__ void slots_of_kernel(const V D, int64_t p, const int64_t* __restrict__ medoids,
+                                int64_t k, const int64_t* __restrict__ assignment,
+                                double* __restrict__ dist, int32_t* __restrict__ lab) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = assignment[j];
+    int64_t lo = 0, hi = k;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (medoids[mid] < a) lo = mid + 1;
+      else hi = mid;
+    }
+    lab[j] = (int32_t)lo;
+    dist[j] = a == j ? 0.0 : D(a, j);
+  }
+}
+
+// kmedoids.hpp:45-52 for one seeding step: `current` becomes chosen and every unchosen
+// nearest[j] = std::min(nearest[j], D(j, current)) (b < a ? b : a).
+template <class V>
+__global__ void seed_step_kernel(const V D, int64_t p, int64_t current,
+                                 uint8_t* __restrict__ chosen, double* __restrict__ nearest) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    if (j == current) {
+      chosen[j] = 1;
+      continue;
+    }
+    if (chosen[j]) continue;
+    const double a = nearest[j], b = D(current, j);
+    nearest[j] = b < a ? b : a;
+  }
+}
+
+// Cluster boundaries from the labels sorted ascending: cb[c] = first position with
+// label >= c, cb[k] = p (empty clusters get equal neighbours).
+__global__ void cluster_bounds_kernel(const int32_t* __restrict__ sorted, int64_t p, int64_t k,
+                                      int64_t* __restrict__ cb) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < p;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lo = q == 0 ? 0 : (int64_t)sorted[q - 1] + 1, hi = sorted[q];
+    for (int64_t c = lo; c <= hi; ++c) cb[c] = q;
+    if (q == p - 1)
+      for (int64_t c = hi + 1; c <= k; ++c) cb[c] = p;
+  }
+}
+
+__global__ void fill_inf_kernel(double* __restrict__ out, int64_t n) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = CUDART_INF;
+}
+
+__global__ void iota_kernel(int32_t* __restrict__ out, int64_t n) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = (int32_t)t;
+}
+
+// keys[u] = lab[perm[u]]: the cluster slot of the series stored at permuted position u.
+__global__ void permuted_labels_kernel(const int32_t* __restrict__ lab,
+                                       const int32_t* __restrict__ perm, int64_t p,
+                                       int32_t* __restrict__ keys) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < p;
+       u += (int64_t)gridDim.x * blockDim.x)
+    keys[u] = lab[perm[u]];
+}
+
+__global__ void inverse_perm_kernel(const int32_t* __restrict__ perm, int64_t p,
+                                    int32_t* __restrict__ pinv) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < p;
+       u += (int64_t)gridDim.x * blockDim.x)
+    pinv[perm[u]] = (int32_t)u;
+}
+
+// Candidate sums over the cluster-ordered copy of the square (see launch_update2): the
+// candidate's row is psq row pinv[a] and its cluster's members, as positions u of that
+// copy, are ascending -- runs of consecutive u, so the warp's loads are coalesced instead
+// of one 32-byte sector per member. Any summation order: these sums only rule candidates
+// out (cluster_select_kernel).
+__global__ void tree_sum_perm_kernel(const double* __restrict__ psq, int64_t p,
+                                     const int32_t* __restrict__ pinv,
+                                     const int32_t* __restrict__ members,
+                                     const int32_t* __restrict__ members_perm,
+                                     const int64_t* __restrict__ cb, int64_t k,
+                                     double* __restrict__ tsum) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < p; q += nw) {
+    int64_t lo = 0, hi = k - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) / 2;
+      if (__ldg(cb + mid) <= q) lo = mid;
+      else hi = mid - 1;
+    }
+    const int64_t b = __ldg(cb + lo), e = __ldg(cb + lo + 1);
+    const double* row = psq + (int64_t)__ldg(pinv + __ldg(members + q)) * p;
+    double acc0 = 0.0, acc1 = 0.0;
+    int64_t t = b + lane;
+    for (; t + 224 < e; t += 256) {  // 8 loads in flight per lane
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(row + __ldg(members_perm + t + 32 * u));
+      acc0 = __dadd_rn(acc0, __dadd_rn(__dadd_rn(v[0], v[1]), __dadd_rn(v[2], v[3])));
+      acc1 = __dadd_rn(acc1, __dadd_rn(__dadd_rn(v[4], v[5]), __dadd_rn(v[6], v[7])));
+    }
+    for (; t < e; t += 32) acc0 = __dadd_rn(acc0, __ldg(row + __ldg(members_perm + t)));
+    double acc = __dadd_rn(acc0, acc1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    if (lane == 0) tsum[q] = acc;
+  }
+}
+
+// Farthest-point anchors for the cluster-ordered layout (not part of the reference's
+// algorithm; it only decides where rows live): nearest[j] = min(nearest[j], D(a, j)) for
+// the newest anchor a, and each block's (max, lowest index) of nearest.
+__global__ void fpt_update_kernel(const double* __restrict__ sq, int64_t p,
+                                  const int64_t* __restrict__ anchors, int a,
+                                  double* __restrict__ nearest, double* __restrict__ part_v,
+                                  int64_t* __restrict__ part_i) {
+  __shared__ double sv[256];
+  __shared__ int64_t si[256];
+  const int64_t cur = anchors[a - 1];
+  double bv = -1.0;
+  int64_t bi = p;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const double d = sq[cur * p + j];
+    const double v = a == 1 ? d : (d < nearest[j] ? d : nearest[j]);
+    nearest[j] = v;
+    if (v > bv) {  // j ascending per thread: strict > keeps the first
+      bv = v;
+      bi = j;
+    }
+  }
+  sv[threadIdx.x] = bv;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      const double ov = sv[threadIdx.x + w];
+      const int64_t oi = si[threadIdx.x + w];
+      if (ov > sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+        sv[threadIdx.x] = ov;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part_v[blockIdx.x] = sv[0];
+    part_i[blockIdx.x] = si[0];
+  }
+}
+
+__global__ void fpt_pick_kernel(const double* __restrict__ part_v,
+                                const int64_t* __restrict__ part_i, int nblk,
+                                int64_t* __restrict__ anchors, int a) {
+  __shared__ double sv[256];
+  __shared__ int64_t si[256];
+  double bv = -2.0;
+  int64_t bi = 0;
+  for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
+    if (part_v[b] > bv || (part_v[b] == bv && part_i[b] < bi)) {
+      bv = part_v[b];
+      bi = part_i[b];
+    }
+  }
+  sv[threadIdx.x] = bv;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      const double ov = sv[threadIdx.x + w];
+      const int64_t oi = si[threadIdx.x + w];
+      if (ov > sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+        sv[threadIdx.x] = ov;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) anchors[a] = si[0];
+}
+
+// psq[u][v] = sq[perm[u]][perm[v]]: one block per output row; the source row (p doubles,
+// contiguous) is gathered through L1/L2 while the output row is written coalesced.
+__global__ void __launch_bounds__(512) permute_square_kernel(const double* __restrict__ sq,
+                                                             int64_t p,
+                                                             const int32_t* __restrict__ perm,
+                                                             double* __restrict__ psq) {
+  for (int64_t u = blockIdx.x; u < p; u += gridDim.x) {
+    const double* src = sq + (int64_t)__ldg(perm + u) * p;
+    double* dst = psq + u * p;
+    int64_t v = threadIdx.x;
+    for (; v + 3 * 512 < p; v += 4 * 512) {
+      const int32_t c0 = __ldg(perm + v), c1 = __ldg(perm + v + 512);
+      const int32_t c2 = __ldg(perm + v + 1024), c3 = __ldg(perm + v + 1536);
+      const double a0 = __ldg(src + c0), a1 = __ldg(src + c1);
+      const double a2 = __ldg(src + c2), a3 = __ldg(src + c3);
+      __stcs(dst + v, a0);
+      __stcs(dst + v + 512, a1);
+      __stcs(dst + v + 1024, a2);
+      __stcs(dst + v + 1536, a3);
+    }
+    for (; v < p; v += 512) __stcs(dst + v, __ldg(src + __ldg(perm + v)));
+  }
+}
+
 int grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   if (g > 148 * 32) g = 148 * 32;
@@ -430,6 +718,140 @@ cudaError_t launch_update(const double* matrix, bool condensed, int64_t p,
   else
     cluster_select_kernel<<<(unsigned)k, 256, 0, s>>>(SquareView{matrix, p}, p, members,
                                                       cluster_begin, sums, best_member, best_sum);
+  return cudaGetLastError();
+}
+
+
+// ---- round-2 sweep launchers ----------------------------------------------------------
+cudaError_t launch_assign_slots(const double* matrix, bool condensed, int64_t p,
+                                const int64_t* medoids, int64_t k, int64_t* assignment,
+                                double* dist, int32_t* lab, cudaStream_t s) {
+  const unsigned blocks = (unsigned)std::min<int64_t>((p + 31) / 32, 148 * 8);
+  if (condensed)
+    assign_slots_kernel<<<blocks, 256, 0, s>>>(CondView{matrix, p}, p, medoids, k, assignment,
+                                                dist, lab);
+  else
+    assign_slots_kernel<<<blocks, 256, 0, s>>>(SquareView{matrix, p}, p, medoids, k, assignment,
+                                                dist, lab);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_slots_of(const double* matrix, bool condensed, int64_t p,
+                            const int64_t* medoids, int64_t k, const int64_t* assignment,
+                            double* dist, int32_t* lab, cudaStream_t s) {
+  if (condensed)
+    slots_of_kernel<<<grid_for(p, 256), 256, 0, s>>>(CondView{matrix, p}, p, medoids, k,
+                                                     assignment, dist, lab);
+  else
+    slots_of_kernel<<<grid_for(p, 256), 256, 0, s>>>(SquareView{matrix, p}, p, medoids, k,
+                                                     assignment, dist, lab);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_seed_step(const double* matrix, bool condensed, int64_t p, int64_t current,
+                             uint8_t* chosen, double* nearest, cudaStream_t s) {
+  if (condensed)
+    seed_step_kernel<<<grid_for(p, 256), 256, 0, s>>>(CondView{matrix, p}, p, current, chosen,
+                                                      nearest);
+  else
+    seed_step_kernel<<<grid_for(p, 256), 256, 0, s>>>(SquareView{matrix, p}, p, current, chosen,
+                                                      nearest);
+  return cudaGetLastError();
+}
+
+static int key_bits(int64_t k) {
+  int b = 1;
+  while (b < 31 && (int64_t(1) << b) < k) ++b;
+  return b;
+}
+
+size_t bucket_temp_bytes(int64_t p) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int)p, 0, 31);
+  return bytes;
+}
+
+cudaError_t launch_fill_inf(double* out, int64_t n, cudaStream_t s) {
+  fill_inf_kernel<<<grid_for(n, 256), 256, 0, s>>>(out, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_iota(int32_t* out, int64_t n, cudaStream_t s) {
+  iota_kernel<<<grid_for(n, 256), 256, 0, s>>>(out, n);
+  return cudaGetLastError();
+}
+
+// kmedoids.hpp:86-92 on the device: members of each cluster in ascending series order (a
+// stable radix sort of the iota by cluster slot) and the cluster bounds; with a
+// cluster-ordered copy of the square (perm != nullptr) also each cluster's members as
+// ascending positions of that copy.
+cudaError_t launch_bucket(const int32_t* lab, const int32_t* perm, const int32_t* iota, int64_t p,
+                          int64_t k, int32_t* keys_a, int32_t* keys_b, int32_t* members,
+                          int32_t* members_perm, int64_t* cb, void* tmp, size_t tmp_bytes,
+                          cudaStream_t s) {
+  const int bits = key_bits(k);
+  size_t bytes = tmp_bytes;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, bytes, lab, keys_a, iota, members, (int)p,
+                                                  0, bits, s);
+  if (e != cudaSuccess) return e;
+  cluster_bounds_kernel<<<grid_for(p, 256), 256, 0, s>>>(keys_a, p, k, cb);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (!perm) return cudaSuccess;
+  permuted_labels_kernel<<<grid_for(p, 256), 256, 0, s>>>(lab, perm, p, keys_b);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  bytes = tmp_bytes;
+  return cub::DeviceRadixSort::SortPairs(tmp, bytes, keys_b, keys_a, iota, members_perm, (int)p,
+                                         0, bits, s);
+}
+
+// Candidate sums + per-cluster selection (kmedoids.hpp:111-121). With psq (the
+// cluster-ordered copy) the sums read contiguous runs; the contenders' exact sequential
+// sums always read the square in ascending member order (cluster_select_kernel).
+cudaError_t launch_update2(const double* matrix, bool condensed, const double* psq,
+                           const int32_t* pinv, int64_t p, const int32_t* members,
+                           const int32_t* members_perm, const int64_t* cluster_begin,
+                           int64_t k, int64_t* best_member, double* best_sum,
+                           cudaStream_t s) {
+  if (!psq)
+    return launch_update(matrix, condensed, p, members, cluster_begin, k, best_member, best_sum,
+                         s);
+  double* sums = best_sum + k;
+  const int64_t warps = std::min<int64_t>(p, 148 * 64);
+  const unsigned tb = (unsigned)((warps + 7) / 8);
+  tree_sum_perm_kernel<<<tb, 256, 0, s>>>(psq, p, pinv, members, members_perm, cluster_begin, k,
+                                          sums);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  cluster_select_kernel<<<(unsigned)k, 256, 0, s>>>(SquareView{matrix, p}, p, members,
+                                                    cluster_begin, sums, best_member, best_sum);
+  return cudaGetLastError();
+}
+
+// The cluster-ordered copy of the square: farthest-point anchors (deterministic, on the
+// device), each series' nearest anchor, a stable sort by anchor -> perm, and the copy.
+cudaError_t launch_cluster_layout(const double* sq, int64_t p, int n_anchor, int64_t* anchors,
+                                  double* nearest, double* part_v, int64_t* part_i,
+                                  int64_t* asg_tmp, double* dist_tmp, int32_t* lab,
+                                  int32_t* keys_tmp, const int32_t* iota, int32_t* perm,
+                                  int32_t* pinv, double* psq, void* tmp, size_t tmp_bytes,
+                                  cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(anchors, 0, sizeof(int64_t), s);  // first anchor: series 0
+  if (e != cudaSuccess) return e;
+  const int nblk = (int)std::min<int64_t>((p + 255) / 256, 1024);
+  for (int a = 1; a < n_anchor; ++a) {
+    fpt_update_kernel<<<nblk, 256, 0, s>>>(sq, p, anchors, a, nearest, part_v, part_i);
+    fpt_pick_kernel<<<1, 256, 0, s>>>(part_v, part_i, nblk, anchors, a);
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  e = launch_assign_slots(sq, false, p, anchors, n_anchor, asg_tmp, dist_tmp, lab, s);
+  if (e != cudaSuccess) return e;
+  size_t bytes = tmp_bytes;
+  e = cub::DeviceRadixSort::SortPairs(tmp, bytes, lab, keys_tmp, iota, perm, (int)p, 0,
+                                      key_bits(n_anchor), s);
+  if (e != cudaSuccess) return e;
+  inverse_perm_kernel<<<grid_for(p, 256), 256, 0, s>>>(perm, p, pinv);
+  permute_square_kernel<<<(unsigned)std::min<int64_t>(p, 148 * 8), 512, 0, s>>>(sq, p, perm, psq);
   return cudaGetLastError();
 }
 

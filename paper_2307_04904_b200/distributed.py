@@ -104,20 +104,40 @@ def reduce_best(results: Sequence[Optional[tuple]]) -> tuple:
     return best
 
 
-def kmedoids_restart_sharded(run: Callable[[int, int], Optional[tuple]], restarts: int,
-                             rank: int, world: int, group=None) -> tuple:
-    """Restarts split into contiguous blocks per rank; `run(rb, re)` returns
-    (cost, best_restart, medoids, assignment) for restarts [rb, re) or None if empty.
-    Results are exchanged with all_gather_object and reduced identically on all ranks."""
-    bounds = equal_bounds(restarts, world)
-    rb, re = bounds[rank]
-    mine = run(rb, re) if re > rb else None
+def restarts_of_rank(restarts: int, rank: int, world: int) -> List[int]:
+    """restart r runs on rank r mod world."""
+    return list(range(rank, restarts, max(world, 1)))
+
+
+def kmedoids_restart_round_robin(run: Callable[[List[int]], Optional[tuple]], restarts: int,
+                                 rank: int, world: int, group=None) -> tuple:
+    """Restart r on rank r mod world; `run(rs)` returns (cost, best_restart, medoids,
+    assignment) for the restarts `rs` (ascending) or None if empty. Results are exchanged
+    with all_gather_object and reduced in restart order with strict < on every rank
+    (kmedoids.hpp:182)."""
+    rs = restarts_of_rank(restarts, rank, world)
+    mine = run(rs) if rs else None
     if world > 1:
         gathered: list = [None] * world
         dist.all_gather_object(gathered, mine, group=group)
     else:
         gathered = [mine]
     return reduce_best(gathered)
+
+
+def kmedoids_restart_sharded(run: Callable[[int, int], Optional[tuple]], restarts: int,
+                             rank: int, world: int, group=None) -> tuple:
+    """Round-robin restart sharding over a per-restart-range callable `run(rb, re)`: each
+    of this rank's restarts r runs as [r, r+1), best kept in restart order."""
+    def run_list(rs):
+        best = None
+        for r in rs:
+            res = run(r, r + 1)
+            if res is not None and (best is None or res[0] < best[0]):
+                best = res
+        return best
+
+    return kmedoids_restart_round_robin(run_list, restarts, rank, world, group)
 
 
 # ----------------------------------------------------------------------------- CUDA path

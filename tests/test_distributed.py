@@ -118,3 +118,10 @@ def test_bounds_cover_all_slots():
 def test_reduce_best_ties_go_to_earliest_restart():
     res = [(5.0, 3, [1], [1]), (5.0, 1, [2], [2]), None, (6.0, 0, [3], [3])]
     assert dd.reduce_best(res)[1] == 1
+
+
+def test_restart_round_robin_balances_eight_ranks():
+    # restart r on rank r mod G -- 10 restarts over 8 ranks leave no rank idle
+    got = [dd.restarts_of_rank(10, r, 8) for r in range(8)]
+    assert got[0] == [0, 8] and got[1] == [1, 9] and all(len(g) == 1 for g in got[2:])
+    assert sorted(x for g in got for x in g) == list(range(10))

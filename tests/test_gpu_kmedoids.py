@@ -286,3 +286,45 @@ def test_acceptance_silhouette_fuzz():
         assert all(-1.0 <= v <= 1.0 for v in rep.silhouette)
         sil, mean = sref(D, p, res.medoids, res.assignment)
         assert np.array_equal(np.array(rep.silhouette), sil) and rep.mean_silhouette == mean
+
+
+# ---------------------------------------------------- cluster-ordered layout (round 2)
+@pytest.mark.parametrize("cfgno,q,k", [(3, 900, 24), (5, 300, 10), (1, 100, 4), (3, 700, 60)])
+def test_cluster_layout_identical(monkeypatch, cfgno, q, k):
+    """The candidate sums read a cluster-ordered copy of the square (km_host.cu
+    ensure_layout; normally only for p >= 4096, forced here): medoids, labels, cost and the
+    observer trace equal the plain-square path's and the reference's."""
+    ds = gen.make_config(cfgno).subset(q)
+    m = api.build_matrix_packed(ds.samples, ds.offsets,
+                                WarpWindow(None if ds.half_width < 0 else ds.half_width),
+                                ds.auto_widen)
+    cfg = KMedoidsConfig(k=k, restarts=4, seed=2)
+    runs = []
+    for layout in ("0", "1"):
+        monkeypatch.setenv("DTWGPU_KM_LAYOUT", layout)
+        monkeypatch.setenv("DTWGPU_KM_LAYOUT_MIN_P", "2")
+        mm = DistanceMatrix.from_condensed(ds.p, m.condensed())
+        trace = []
+        r = kmedoids(mm, cfg, lambda rr, it, c: trace.append((rr, it, c)))
+        runs.append((r.medoids, r.assignment, r.total_cost, trace))
+    assert runs[0] == runs[1]
+    ref_trace = []
+    med, asg, cost = kref(m.condensed(), ds.p, cfg, lambda rr, it, c: ref_trace.append((rr, it, c)))
+    assert runs[1][:3] == (list(med), list(asg), cost) and runs[1][3] == ref_trace
+
+
+@pytest.mark.parametrize("p,k", [(64, 9), (300, 40)])
+def test_cluster_layout_duplicates_and_empty_clusters(monkeypatch, p, k):
+    """Duplicated series (zero distances, collapsed medoids, refill) and many small clusters
+    with the layout forced: identical to the reference."""
+    monkeypatch.setenv("DTWGPU_KM_LAYOUT_MIN_P", "2")
+    rng = np.random.default_rng(p)
+    base = random_condensed(ScalarRng(p), p)
+    sq = np.zeros((p, p))
+    iu = np.triu_indices(p, 1)
+    sq[iu] = base
+    sq = sq + sq.T
+    dup = rng.integers(0, p // 4, size=p)  # series j is a copy of series dup[j]
+    sq = sq[np.ix_(dup, dup)]
+    D = np.ascontiguousarray(sq[iu])
+    check_same(D, p, KMedoidsConfig(k=k, restarts=5, seed=3))
