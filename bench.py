@@ -275,24 +275,57 @@ def all_configs_block(eng, dev, a):
 def kmedoids_run(eng, ds, cond, check):
     """The config's k-medoids (kmedoids.hpp:148-189) over the matrix resident in HBM."""
     p = ds.p
-    eng.adopt(None, p, on_device_ptr=cond.data_ptr())
-    eng._p_resident = p
-    eng.synchronize()
-    eng.km_stats(reset=True)
-    t0 = time.perf_counter()
-    med, asg, cost, br = eng.kmedoids(p, ds.k, ds.restarts, 100, 0)
-    km_s = time.perf_counter() - t0
+    # first call (untimed warm-up: restart-worker contexts, buffers, module loading), then
+    # the timed call over a freshly adopted matrix (square expansion and cluster-ordered
+    # copy rebuilt inside the timed region)
+    first = []
+    for rep in range(2):
+        eng.adopt(None, p, on_device_ptr=cond.data_ptr())
+        eng._p_resident = p
+        eng.synchronize()
+        eng.km_stats(reset=True)
+        t0 = time.perf_counter()
+        med, asg, cost, br = eng.kmedoids(p, ds.k, ds.restarts, 100, 0)
+        km_s = time.perf_counter() - t0
+        first.append(km_s)
     st = eng.km_stats()
     hbm = _hbm_peak()
     upd_gbs = st["update_bytes"] / max(st["update_ms"], 1e-9) / 1e6
     res = {"k": ds.k, "restarts": ds.restarts, "series": p, "seconds": km_s,
+           "first_call_seconds": first[0],
            "sweeps": st["sweeps"], "total_cost": cost, "best_restart": br,
-           "includes": "square expansion + every restart (seeding, sweeps, host sums)",
+           "includes": "square expansion, cluster-ordered copy, every restart (seeding, "
+                       "sweeps, host sums); restarts on concurrent restart workers",
+           "square_expand_ms": st["prep_ms"], "cluster_layout": st["cluster_layout"],
+           "layout_build_ms": st["layout_ms"],
            "update_kernels": {"ms": st["update_ms"], "algorithmic_bytes": st["update_bytes"],
                               "achieved_gbs": upd_gbs, "peak_gbs": hbm[0],
-                              "frac": upd_gbs / hbm[0], "peak_source": hbm[1]},
+                              "frac": upd_gbs / hbm[0], "peak_source": hbm[1],
+                              "note": "sum of per-sweep device intervals; with concurrent "
+                                      "restart workers they overlap, see sequential"},
            "assign_kernel": {"ms": st["assign_ms"], "algorithmic_bytes": st["assign_bytes"],
                              "achieved_gbs": st["assign_bytes"] / max(st["assign_ms"], 1e-9) / 1e6}}
+    # one restart worker: per-sweep kernel intervals not overlapped by other restarts
+    os.environ["DTWGPU_KM_WORKERS"] = "1"
+    try:
+        eng.adopt(None, p, on_device_ptr=cond.data_ptr())
+        eng.synchronize()
+        eng.km_stats(reset=True)
+        t0 = time.perf_counter()
+        m1, a1, c1, _ = eng.kmedoids(p, ds.k, ds.restarts, 100, 0)
+        s1 = time.perf_counter() - t0
+        st1 = eng.km_stats()
+    finally:
+        del os.environ["DTWGPU_KM_WORKERS"]
+    sw = max(st1["sweeps"], 1)
+    res["sequential"] = {
+        "seconds": s1, "identical": bool(list(m1) == list(med) and list(a1) == list(asg)
+                                         and c1 == cost),
+        "update_us_per_sweep": st1["update_ms"] / sw * 1e3,
+        "assign_us_per_sweep": st1["assign_ms"] / sw * 1e3,
+        "update_algorithmic_gbs": st1["update_bytes"] / max(st1["update_ms"], 1e-9) / 1e6,
+        "update_frac_of_hbm": st1["update_bytes"] / max(st1["update_ms"], 1e-9) / 1e6 / hbm[0],
+        "assign_algorithmic_gbs": st1["assign_bytes"] / max(st1["assign_ms"], 1e-9) / 1e6}
     if check:
         # Parity against the reference's own kmedoids (oracle/_ref; the C restatement when
         # it was not built), timed: its single-threaded restart loop over the same host

@@ -144,12 +144,13 @@ int dtwg_kmedoids(dtwg_ctx* ctx, int64_t k, int64_t restarts, int64_t max_iterat
                   dtwg_observer_fn observer, void* user, int64_t* medoids_out,
                   int64_t* assignment_out, double* cost_out, int64_t* best_restart_out);
 
-/* k-medoids sweep statistics since the last reset (out: 7 doubles): out[0] sweeps,
+/* k-medoids sweep statistics since the last reset (out: 8 doubles): out[0] sweeps,
  * out[1] assignment kernel ms, out[2] its algorithmic bytes (8 per distance read), out[3]
  * update kernels ms (device bucketing + candidate sums + selection), out[4] their
  * algorithmic bytes (8 * sum |C|^2 + index traffic), out[5] ms spent preparing the sweep
- * views (square expansion + cluster-ordered copy), out[6] 1 if the cluster-ordered copy
- * is in use. With concurrent restart workers the per-sweep times overlap each other. */
+ * views (square expansion), out[6] 1 if the cluster-ordered copy is in use (2: as fp32), out[7] its
+ * build time in ms (device; it overlaps the seeding). With concurrent restart workers the
+ * per-sweep times overlap each other. */
 int dtwg_km_stats(dtwg_ctx* ctx, double* out, int reset);
 
 /*

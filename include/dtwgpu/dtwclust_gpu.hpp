@@ -259,10 +259,18 @@ inline dtwclust::ScoreReport silhouette_scores(const dtwclust::DistanceMatrix& d
 }
 
 /// Drop-in for dtwclust::LazyDistanceSource (pairwise.hpp:133-188) on the k-medoids path
-/// (runner.hpp:187-189, 211): instead of computing pairs on demand on the host, the first
-/// use fills the whole matrix on the GPU. Satisfies the DistanceSource concept
-/// (cluster_result.hpp:13-17); every distance is identical, so kmedoids returns the same
-/// ClusterResult -- only computed_pairs() reports p(p-1)/2.
+/// (runner.hpp:187-189, 211). Instead of computing pairs on demand on the host, the first
+/// use fills the whole matrix on the GPU, into this source's own device context where it
+/// stays resident: dtwgpu::kmedoids(GpuDistanceSource&, ...) below sweeps it there with no
+/// host round trip, and distance(i, j) from host code reads a host copy fetched once.
+/// Satisfies the DistanceSource concept (cluster_result.hpp:13-17).
+///
+/// Semantics kept from LazyDistanceSource::distance: indices are checked first
+/// (IndexOutOfRangeError), i == j is 0 without any work, and a banded window without
+/// auto-widen throws BandInfeasibleError(min(i,j), max(i,j), cause) only for a requested
+/// infeasible pair -- the fill then computes the other pairs (auto-widened entries of the
+/// infeasible pairs are never handed out). Every returned distance is bit-identical to
+/// the reference's. Differences: computed_pairs() reports p(p-1)/2 once filled.
 class GpuDistanceSource {
  public:
   GpuDistanceSource(const std::vector<dtwclust::TimeSeries>& dataset,
@@ -270,28 +278,130 @@ class GpuDistanceSource {
       : dataset_(&dataset), window_(w), auto_widen_(auto_widen) {
     if (dataset.empty()) throw dtwclust::EmptyDatasetError();
     dtwclust::validate_dataset(dataset);
+    if (!w.is_unlimited() && !auto_widen) {
+      std::size_t lo = dataset[0].length(), hi = lo;
+      for (const auto& s : dataset) {
+        lo = std::min(lo, s.length());
+        hi = std::max(hi, s.length());
+      }
+      has_infeasible_ = hi - lo > w.half_width();
+    }
   }
   std::size_t size() const noexcept { return dataset_->size(); }
+
   double distance(std::size_t i, std::size_t j) {
-    if (!matrix_) {
-      dtwclust::BuildStats stats;
-      matrix_ = std::make_unique<dtwclust::DistanceMatrix>(
-          dtwgpu::build_matrix(*dataset_, window_, 1, &stats, auto_widen_));
-      computed_ = stats.evaluations;
+    const std::size_t p = size();
+    if (i >= p) throw dtwclust::IndexOutOfRangeError(i, p);
+    if (j >= p) throw dtwclust::IndexOutOfRangeError(j, p);
+    if (i == j) return 0.0;
+    if (!feasible(i, j)) {
+      const auto& a = (*dataset_)[i];
+      const auto& b = (*dataset_)[j];
+      throw dtwclust::BandInfeasibleError(
+          std::min(i, j), std::max(i, j),
+          dtwclust::BandInfeasibleError(a.length(), b.length(), window_.half_width()));
     }
-    return matrix_->distance(i, j);
+    if (host_.empty()) {
+      ensure_device();
+      host_.resize(dtwclust::DistanceMatrix::condensed_size(p));
+      const int rc = dtwg_download_condensed(ctx_->get(), host_.data());
+      if (rc != DTWG_OK) detail::rethrow(ctx_->get(), rc, nullptr, 0);
+    }
+    const std::size_t lo = std::min(i, j), hi = std::max(i, j);
+    return host_[lo * p - lo * (lo + 1) / 2 + (hi - lo - 1)];
   }
+
   std::uint64_t computed_pairs() const { return computed_; }
-  /// The filled matrix (after the first distance() call), e.g. for kmedoids on the GPU.
-  const dtwclust::DistanceMatrix* matrix() const { return matrix_.get(); }
+  /// Whether some pair of the dataset is infeasible under the window (banded, no widen).
+  bool has_infeasible_pairs() const noexcept { return has_infeasible_; }
+
+  /// Fills the matrix on the GPU (once) and leaves it resident in this source's context.
+  dtwg_ctx* ensure_device() {
+    if (!ctx_) {
+      ctx_ = std::make_unique<Context>(default_devices()[0]);
+      const std::size_t p = size();
+      std::vector<std::int64_t> offsets(p + 1, 0);
+      for (std::size_t i = 0; i < p; ++i)
+        offsets[i + 1] = offsets[i] + static_cast<std::int64_t>((*dataset_)[i].length());
+      std::vector<double> samples(static_cast<std::size_t>(offsets[p]));
+      for (std::size_t i = 0; i < p; ++i)
+        std::copy((*dataset_)[i].samples.begin(), (*dataset_)[i].samples.end(),
+                  samples.begin() + offsets[i]);
+      const std::int64_t hw =
+          window_.is_unlimited() ? -1 : static_cast<std::int64_t>(window_.half_width());
+      std::uint64_t evaluations = 0;
+      // infeasible pairs (never handed out, see distance) are filled auto-widened so the
+      // feasible ones can be computed in the same launch
+      const int rc = dtwg_build_matrix(ctx_->get(), samples.data(), offsets.data(),
+                                       static_cast<std::int64_t>(p), hw,
+                                       (auto_widen_ || has_infeasible_) ? 1 : 0, 1, DTWG_FP64,
+                                       nullptr, &evaluations);
+      if (rc != DTWG_OK) {
+        dtwg_ctx* c = ctx_->get();
+        const std::string msg = dtwg_last_error(c);
+        ctx_.reset();
+        throw DeviceError(rc, msg);
+      }
+      computed_ = evaluations;
+    }
+    return ctx_->get();
+  }
 
  private:
+  bool feasible(std::size_t i, std::size_t j) const {
+    if (!has_infeasible_) return true;
+    return window_.feasible_for((*dataset_)[i].length(), (*dataset_)[j].length());
+  }
+
   const std::vector<dtwclust::TimeSeries>* dataset_;
   dtwclust::WarpWindow window_;
   bool auto_widen_;
-  std::unique_ptr<dtwclust::DistanceMatrix> matrix_;
+  bool has_infeasible_ = false;
+  std::unique_ptr<Context> ctx_;
+  std::vector<double> host_;
   std::uint64_t computed_ = 0;
 };
+
+/// kmedoids.hpp:148-189 over a GpuDistanceSource (the runner's lazy path, runner.hpp:211):
+/// the sweeps run on the GPU over the matrix the source filled in HBM -- no host copy, no
+/// re-upload. An unqualified kmedoids(source, config) call picks this overload (ADL,
+/// non-template). If some pair is infeasible under the window, the reference's kmedoids
+/// throws for the first infeasible pair it requests, which depends on its access order;
+/// that case runs the reference's template over distance() so the same error surfaces.
+inline dtwclust::ClusterResult kmedoids(GpuDistanceSource& source,
+                                        const dtwclust::KMedoidsConfig& config,
+                                        const dtwclust::IterationObserver& observer = {}) {
+  const std::size_t p = source.size();
+  if (config.k < 1 || config.k > p) throw dtwclust::KOutOfRangeError(config.k, p);
+  if (config.restarts < 1) throw dtwclust::InvalidArgumentsError("restarts must be >= 1");
+  if (config.max_iterations < 1)
+    throw dtwclust::InvalidArgumentsError("max_iterations must be >= 1");
+  if (source.has_infeasible_pairs()) return dtwclust::kmedoids<GpuDistanceSource>(source, config, observer);
+  dtwg_ctx* ctx = source.ensure_device();
+  struct Trampoline {
+    static void call(void* user, std::int64_t r, std::int64_t it, double cost) {
+      (*static_cast<const dtwclust::IterationObserver*>(user))(static_cast<std::size_t>(r),
+                                                               static_cast<std::size_t>(it), cost);
+    }
+  };
+  std::vector<std::int64_t> medoids(config.k), assignment(p);
+  double cost = 0.0;
+  std::int64_t best_restart = -1;
+  const int rc = dtwg_kmedoids(ctx, static_cast<std::int64_t>(config.k),
+                               static_cast<std::int64_t>(config.restarts),
+                               static_cast<std::int64_t>(config.max_iterations), config.seed, 0,
+                               static_cast<std::int64_t>(config.restarts),
+                               observer ? &Trampoline::call : nullptr,
+                               const_cast<dtwclust::IterationObserver*>(&observer),
+                               medoids.data(), assignment.data(), &cost, &best_restart);
+  if (rc != DTWG_OK) detail::rethrow(ctx, rc, nullptr, 0);
+  dtwclust::ClusterResult result;
+  result.medoids.assign(medoids.begin(), medoids.end());
+  result.assignment.assign(assignment.begin(), assignment.end());
+  result.total_cost = cost;
+  result.certificate = dtwclust::Certificate::LocalHeuristic;
+  return result;
+}
 
 namespace detail {
 

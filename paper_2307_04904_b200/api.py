@@ -198,11 +198,12 @@ class Engine:
 
     def km_stats(self, reset: bool = False) -> dict:
         """Sweep count and device time / algorithmic bytes of the k-medoids kernels."""
-        out = np.zeros(7, dtype=np.float64)
+        out = np.zeros(8, dtype=np.float64)
         self.check(self.L.dtwg_km_stats(self.h, out, int(reset)))
         return {"sweeps": int(out[0]), "assign_ms": out[1], "assign_bytes": out[2],
                 "update_ms": out[3], "update_bytes": out[4], "prep_ms": out[5],
-                "cluster_layout": bool(out[6])}
+                "cluster_layout": {0: None, 1: "fp64", 2: "fp32"}.get(int(out[6])),
+                "layout_ms": out[7]}
 
     def last_plan(self) -> str:
         return self.L.dtwg_last_plan(self.h).decode()

@@ -84,7 +84,7 @@ cudaError_t launch_band_pad(const double* samples, const int64_t* off, const int
                             int64_t p, int64_t pad, void* out, bool fp32, cudaStream_t s);
 cudaError_t launch_expand_square(const double* condensed, int64_t p, double* square,
                                  cudaStream_t s);
-cudaError_t launch_validate_condensed(const double* condensed, int64_t total, int* bad,
+cudaError_t launch_validate_condensed(const double* condensed, int64_t total, int* flags,
                                       cudaStream_t s);
 cudaError_t launch_nearest_update(const double* matrix, bool condensed, int64_t p,
                                   int64_t current, const uint8_t* chosen, double* nearest,
@@ -98,7 +98,8 @@ cudaError_t launch_update(const double* matrix, bool condensed, int64_t p,
 // round 2: device-side bucketing, slot-writing assignment, cluster-ordered square
 cudaError_t launch_assign_slots(const double* matrix, bool condensed, int64_t p,
                                 const int64_t* medoids, int64_t k, int64_t* assignment,
-                                double* dist, int32_t* lab, cudaStream_t s);
+                                double* dist, int32_t* lab, cudaStream_t s,
+                                int32_t* counts = nullptr);
 cudaError_t launch_slots_of(const double* matrix, bool condensed, int64_t p,
                             const int64_t* medoids, int64_t k, const int64_t* assignment,
                             double* dist, int32_t* lab, cudaStream_t s);
@@ -110,16 +111,15 @@ cudaError_t launch_fill_inf(double* out, int64_t n, cudaStream_t s);
 cudaError_t launch_bucket(const int32_t* lab, const int32_t* perm, const int32_t* iota, int64_t p,
                           int64_t k, int32_t* keys_a, int32_t* keys_b, int32_t* members,
                           int32_t* members_perm, int64_t* cb, void* tmp, size_t tmp_bytes,
-                          cudaStream_t s);
-cudaError_t launch_update2(const double* matrix, bool condensed, const double* psq,
+                          cudaStream_t s, bool counted = false);
+cudaError_t launch_update2(const double* matrix, bool condensed, const void* psq, bool psq32,
                            const int32_t* pinv, int64_t p, const int32_t* members,
                            const int32_t* members_perm, const int64_t* cluster_begin,
                            int64_t k, int64_t* best_member, double* best_sum, cudaStream_t s);
-cudaError_t launch_cluster_layout(const double* sq, int64_t p, int n_anchor, int64_t* anchors,
-                                  double* nearest, double* part_v, int64_t* part_i,
+cudaError_t launch_cluster_layout(const double* sq, int64_t p, int n_anchor, const int64_t* anchors,
                                   int64_t* asg_tmp, double* dist_tmp, int32_t* lab,
                                   int32_t* keys_tmp, const int32_t* iota, int32_t* perm,
-                                  int32_t* pinv, double* psq, void* tmp, size_t tmp_bytes,
-                                  cudaStream_t s);
+                                  int32_t* pinv, void* psq, bool psq32, void* tmp,
+                                  size_t tmp_bytes, int num_sms, cudaStream_t s);
 
 }  // namespace dtwgpu

@@ -172,7 +172,8 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
   int n_strip_cls = 0;
   for (size_t c = 0; c < plan.size(); ++c) {
     const PlanClass& pc = plan[c];
-    const int64_t count = ctx->uniform ? (se - sb) : (int64_t)pc.slots.size();
+    const int64_t count = ctx->uniform ? (pc.range_begin >= 0 ? pc.range_count : se - sb)
+                                       : (int64_t)pc.slots.size();
     const int bps = dtwgpu::fill_blocks_per_sm(pc.cfg);
     const int64_t groups_per_block = dtwgpu::kThreads / pc.cfg.G;
     const int64_t items_per_block =
@@ -232,7 +233,8 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
     if (!dtwgpu::fill_cfg_supported(pc.cfg))
       return ctx->fail(DTWG_INTERNAL, "no kernel for %s G=%d R=%d", family_name(pc.cfg.family),
                        pc.cfg.G, pc.cfg.R);
-    const int64_t count = ctx->uniform ? (se - sb) : (int64_t)pc.slots.size();
+    const int64_t count = ctx->uniform ? (pc.range_begin >= 0 ? pc.range_count : se - sb)
+                                       : (int64_t)pc.slots.size();
     if (count == 0) continue;
     const int bps = dtwgpu::fill_blocks_per_sm(pc.cfg);
     const int64_t blocks = blocks_of[c];
@@ -247,7 +249,7 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
     a.half_width = hw;
     a.auto_widen = auto_widen;
     a.list = ctx->uniform ? nullptr : ctx->d_list.ptr + pos;
-    a.begin = ctx->uniform ? sb : 0;
+    a.begin = ctx->uniform ? (pc.range_begin >= 0 ? pc.range_begin : sb) : 0;
     a.count = count;
     a.out_base = out_base;
     a.out = d_out;
@@ -317,16 +319,18 @@ int validate_resident(dtwg_ctx* ctx, int64_t sb, int64_t se) {
   const int64_t total = ctx->mat_p * (ctx->mat_p - 1) / 2;
   if (se < 0) se = total;
   if (se <= sb) return DTWG_OK;
-  CU(ctx->d_flag.reserve(1), "cudaMalloc flag");
-  CU(cudaMemsetAsync(ctx->d_flag.ptr, 0, sizeof(int), ctx->stream), "memset");
+  CU(ctx->d_flag.reserve(2), "cudaMalloc flag");
+  CU(cudaMemsetAsync(ctx->d_flag.ptr, 0, 2 * sizeof(int), ctx->stream), "memset");
   CU(dtwgpu::launch_validate_condensed(ctx->d_cond.ptr + sb, se - sb, ctx->d_flag.ptr,
                                        ctx->stream),
      "validate");
   ctx->launches++;
-  int bad = 0;
-  CU(cudaMemcpyAsync(&bad, ctx->d_flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream),
+  int flags[2] = {0, 0};
+  CU(cudaMemcpyAsync(flags, ctx->d_flag.ptr, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream),
      "D2H flag");
   CU(cudaStreamSynchronize(ctx->stream), "sync");
+  const int bad = flags[0];
+  ctx->fp32_safe = sb == 0 && se == total && !flags[1];
   if (bad) {
     ctx->cond_valid = false;
     return ctx->fail(DTWG_DISTANCE_MATRIX_INVALID, "entries must be finite and non-negative");
@@ -430,8 +434,6 @@ void dtwg_destroy(dtwg_ctx* ctx) {
   ctx->d_perm.release();
   ctx->d_pinv.release();
   ctx->d_anchors.release();
-  ctx->d_fpt_i.release();
-  ctx->d_fpt_v.release();
   ctx->d_lab.release();
   ctx->d_keys_a.release();
   ctx->d_keys_b.release();
@@ -460,6 +462,17 @@ void dtwg_destroy(dtwg_ctx* ctx) {
   if (ctx->km0) cudaEventDestroy(ctx->km0);
   if (ctx->km1) cudaEventDestroy(ctx->km1);
   if (ctx->km2) cudaEventDestroy(ctx->km2);
+  if (ctx->layout_ready) cudaEventDestroy(ctx->layout_ready);
+  if (ctx->layout_t0) cudaEventDestroy(ctx->layout_t0);
+  ctx->d_layout_asg.release();
+  ctx->d_layout_dist.release();
+  ctx->d_layout_lab.release();
+  ctx->d_layout_keys.release();
+  ctx->d_layout_cub.release();
+  if (ctx->layout_stream) {
+    cudaStreamSynchronize(ctx->layout_stream);
+    cudaStreamDestroy(ctx->layout_stream);
+  }
   if (ctx->km3) cudaEventDestroy(ctx->km3);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);

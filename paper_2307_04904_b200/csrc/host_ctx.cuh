@@ -84,6 +84,8 @@ struct Shape {
 struct PlanClass {
   KernelCfg cfg;
   std::vector<int64_t> slots;  // empty + range mode when uniform
+  int64_t range_begin = -1;    // uniform: this class fills [range_begin, +range_count) only
+  int64_t range_count = 0;
   double cost = 0;
   int64_t max_n = 0;
   int64_t max_m = 0;  // longest shorter series: decides single- vs multi-strip Full kernels
@@ -213,9 +215,17 @@ struct dtwg_ctx {
   DevBuf<double> d_psq;
   DevBuf<int32_t> d_perm, d_pinv;
   bool layout_valid = false;  // d_psq/d_perm/d_pinv match the square
+  bool layout32 = false;      // d_psq holds fp32 values (p*p floats)
+  bool fp32_safe = false;     // every non-zero entry in [2^-100, 2^100] (validate_resident)
   bool layout_tried = false;  // decided for this square (built, or skipped: p small / no room)
-  DevBuf<int64_t> d_anchors, d_fpt_i;
-  DevBuf<double> d_fpt_v;
+  DevBuf<int64_t> d_anchors;
+  cudaStream_t layout_stream = nullptr;  // the copy is built here, overlapping the seeding
+  cudaEvent_t layout_ready = nullptr;    // sweeps reading it wait on this
+  cudaEvent_t layout_t0 = nullptr;
+  DevBuf<int64_t> d_layout_asg;
+  DevBuf<double> d_layout_dist;
+  DevBuf<int32_t> d_layout_lab, d_layout_keys;
+  DevBuf<uint8_t> d_layout_cub;
 
   // Device-side bucketing (kmedoids.hpp:86-92): slot per series, radix-sort keys, iota,
   // members in layout order, cub temporary storage.

@@ -24,6 +24,8 @@ bool km_is_cond(const dtwg_ctx* ctx) {
 int ensure_square(dtwg_ctx* ctx) {
   if (ctx->square_valid) return DTWG_OK;
   if (!ctx->cond_valid) return ctx->fail(DTWG_INVALID_ARGUMENTS, "no resident distance matrix");
+  // a cluster-ordered copy still being built from the old square must finish first
+  if (ctx->layout_stream) CU(cudaStreamSynchronize(ctx->layout_stream), "sync layout");
   const int64_t p = ctx->mat_p;
   const char* force = std::getenv("DTWGPU_KM_CONDENSED");
   size_t free_b = 0, total_b = 0;
@@ -57,50 +59,84 @@ int ensure_iota(dtwg_ctx* ctx, int64_t p);
 // (sum over clusters of |C|^2 distances). Members of a cluster are scattered over the
 // row, so in the plain square every 8-byte read costs a whole 32-byte sector (round 1:
 // ~15x the algorithmic bytes). ensure_layout builds once per resident matrix a copy of
-// the square with the series grouped by their nearest farthest-point anchor (n_anchor
-// = k anchors, deterministic, all on the device): members of a cluster then occupy runs
-// of consecutive positions. It only moves data -- the candidate sums read the same
-// doubles, and the contenders' exact sums keep reading the plain square in ascending
-// member order -- so results are bit-identical with or without it. Skipped for small p
-// (nothing to gain), in condensed mode, and when a second square does not fit in HBM.
+// the square with the series grouped by their nearest anchor -- 4k anchors drawn
+// uniformly with a fixed seed (a k-medoids cluster is then mostly a union of whole anchor
+// groups, i.e. runs of consecutive positions; exp. on c3 subsets: DRAM bytes of the sums
+// 1.9-2.0x the algorithmic ones, against 6.7x in the plain square; farthest-point anchors
+// 3.5x). It only moves data -- the candidate sums read the same doubles and the
+// contenders' exact sums keep reading the plain square in ascending member order -- so
+// results are bit-identical with or without it. Skipped for small p (the plain gathers
+// are cheap there), in condensed mode, and when a second square does not fit in HBM.
 int ensure_layout(dtwg_ctx* ctx, int64_t k) {
   if (ctx->layout_tried) return DTWG_OK;
+  if (ctx->layout_stream) CU(cudaStreamSynchronize(ctx->layout_stream), "sync layout");
   ctx->layout_tried = true;
   ctx->layout_valid = false;
   const int64_t p = ctx->mat_p;
-  const int64_t min_p = env_or("DTWGPU_KM_LAYOUT_MIN_P", 4096);
+  const int64_t min_p = env_or("DTWGPU_KM_LAYOUT_MIN_P", 8192);
   if (ctx->km_condensed || p < std::max<int64_t>(min_p, 2) || env_or("DTWGPU_KM_LAYOUT", 1) == 0)
     return DTWG_OK;
+  // fp32 copy when every entry keeps a 2^-24 relative rounding bound in fp32 (the
+  // candidate sums only filter; cluster_select_kernel widens its threshold by 2^-24):
+  // half the bytes per candidate-sum read and per copy write
+  const bool f32 = ctx->fp32_safe && env_or("DTWGPU_KM_LAYOUT32", 1) != 0;
+  const size_t words = f32 ? (size_t)((p * p + 1) / 2) : (size_t)(p * p);
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
-  const double need = double(p) * double(p) * 8.0 - double(ctx->d_psq.cap) * 8.0;
+  const double need = double(words) * 8.0 - double(ctx->d_psq.cap) * 8.0;
   if (need > 0.8 * double(free_b)) return DTWG_OK;
-  const int na = (int)std::min<int64_t>(std::max<int64_t>(k, 2), std::min<int64_t>(p, 256));
-  const int nblk = (int)std::min<int64_t>((p + 255) / 256, 1024);
-  CU(ctx->d_psq.reserve((size_t)(p * p)), "cudaMalloc layout square");
+  const int na = (int)std::min<int64_t>(std::max<int64_t>(4 * k, 2), std::min<int64_t>(p, 256));
+  // na distinct anchors, uniformly at random (fixed seed), ascending
+  std::vector<int64_t> anchors;
+  {
+    SplitMix64 rng(0x5EEDC0DEULL);
+    std::vector<char> used(p, 0);
+    while ((int)anchors.size() < na) {
+      const int64_t j = (int64_t)rng.next_below((uint64_t)p);
+      if (!used[j]) {
+        used[j] = 1;
+        anchors.push_back(j);
+      }
+    }
+    std::sort(anchors.begin(), anchors.end());
+  }
+  CU(ctx->d_psq.reserve(words), "cudaMalloc layout square");
+  ctx->layout32 = f32;
   CU(ctx->d_perm.reserve(p), "malloc");
   CU(ctx->d_pinv.reserve(p), "malloc");
   CU(ctx->d_anchors.reserve(na), "malloc");
-  CU(ctx->d_fpt_v.reserve(nblk), "malloc");
-  CU(ctx->d_fpt_i.reserve(nblk), "malloc");
-  CU(ctx->d_nearest.reserve(p), "malloc");
   CU(ctx->d_assign.reserve(p), "malloc");
   CU(ctx->d_dist.reserve(p), "malloc");
   CU(ctx->d_lab.reserve(p), "malloc");
   CU(ctx->d_keys_a.reserve(p), "malloc");
   int rc = ensure_iota(ctx, p);
   if (rc) return rc;
-  const auto t0 = std::chrono::steady_clock::now();
+  // Built on its own stream (own scratch: anchors' assignment in d_layout_*) while the
+  // restarts seed from the plain square; sweeps wait on layout_ready (km_state).
+  if (!ctx->layout_stream) {
+    CU(cudaStreamCreateWithFlags(&ctx->layout_stream, cudaStreamNonBlocking), "stream");
+    CU(cudaEventCreate(&ctx->layout_ready), "event");
+    CU(cudaEventCreate(&ctx->layout_t0), "event");
+  }
+  CU(ctx->d_layout_asg.reserve(p), "malloc");
+  CU(ctx->d_layout_dist.reserve(p), "malloc");
+  CU(ctx->d_layout_lab.reserve(p), "malloc");
+  CU(ctx->d_layout_keys.reserve(p), "malloc");
+  CU(ctx->d_layout_cub.reserve(ctx->cub_bytes), "malloc");
+  CU(cudaStreamSynchronize(ctx->stream), "sync");  // square and iota ready
+  cudaStream_t ls = ctx->layout_stream;
+  CU(cudaMemcpyAsync(ctx->d_anchors.ptr, anchors.data(), na * 8, cudaMemcpyHostToDevice, ls),
+     "H2D anchors");
+  CU(cudaStreamSynchronize(ls), "sync");  // `anchors` is pageable and about to go away
+  CU(cudaEventRecord(ctx->layout_t0, ls), "event");
   CU(dtwgpu::launch_cluster_layout(ctx->d_square.ptr, p, na, ctx->d_anchors.ptr,
-                                   ctx->d_nearest.ptr, ctx->d_fpt_v.ptr, ctx->d_fpt_i.ptr,
-                                   ctx->d_assign.ptr, ctx->d_dist.ptr, ctx->d_lab.ptr,
-                                   ctx->d_keys_a.ptr, ctx->d_iota.ptr, ctx->d_perm.ptr,
-                                   ctx->d_pinv.ptr, ctx->d_psq.ptr, ctx->d_cub.ptr, ctx->cub_bytes,
-                                   ctx->stream),
+                                   ctx->d_layout_asg.ptr, ctx->d_layout_dist.ptr,
+                                   ctx->d_layout_lab.ptr, ctx->d_layout_keys.ptr, ctx->d_iota.ptr,
+                                   ctx->d_perm.ptr, ctx->d_pinv.ptr, ctx->d_psq.ptr, f32,
+                                   ctx->d_layout_cub.ptr, ctx->cub_bytes, ctx->num_sms, ls),
      "cluster layout");
-  ctx->launches += 2 * (na - 1) + 4;
-  CU(cudaStreamSynchronize(ctx->stream), "sync");
-  ctx->km_prep_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  CU(cudaEventRecord(ctx->layout_ready, ls), "event");
+  ctx->launches += 6;
   ctx->layout_valid = true;
   return DTWG_OK;
 }
@@ -117,11 +153,18 @@ struct KmState {
   int64_t p, k;
   const double* sq;      // sweep view (square or condensed)
   bool cond;             // sweep view is the condensed matrix
-  const double* psq;     // cluster-ordered copy (nullptr: none)
+  const void* psq;       // cluster-ordered copy (nullptr: none)
+  bool psq32;            // ... holding fp32 values
   const int32_t* perm;   // its order
   const int32_t* pinv;
   int buf = 0;           // pinned distance buffer of the sweep in flight
 };
+
+// kernels of one device bucketing + update (cub's radix sort launches 3 per sort)
+int km_update_launches(const KmState& S) {
+  if (S.k <= 256) return 4;
+  return S.psq ? 10 : 6;
+}
 
 int km_enqueue_assign(KmState& S, const std::vector<int64_t>& medoids) {
   dtwg_ctx* ctx = S.ctx;
@@ -130,8 +173,10 @@ int km_enqueue_assign(KmState& S, const std::vector<int64_t>& medoids) {
                      cudaMemcpyHostToDevice, ctx->stream),
      "H2D medoids");
   CU(cudaEventRecord(ctx->km0, ctx->stream), "event");
+  // with k <= 256 the kernel also counts the cluster sizes for the bucketing (into keys_a)
   CU(dtwgpu::launch_assign_slots(S.sq, S.cond, S.p, ctx->d_medoids.ptr, (int64_t)medoids.size(),
-                                 ctx->d_assign.ptr, ctx->d_dist.ptr, ctx->d_lab.ptr, ctx->stream),
+                                 ctx->d_assign.ptr, ctx->d_dist.ptr, ctx->d_lab.ptr, ctx->stream,
+                                 ctx->d_keys_a.ptr),
      "assign");
   ctx->launches++;
   return DTWG_OK;
@@ -148,14 +193,14 @@ int km_enqueue_sweep(KmState& S, const std::vector<int64_t>& medoids, int buf) {
   CU(dtwgpu::launch_bucket(ctx->d_lab.ptr, S.psq ? S.perm : nullptr, ctx->d_iota.ptr, p, k,
                            ctx->d_keys_a.ptr, ctx->d_keys_b.ptr, ctx->d_members.ptr,
                            ctx->d_members_p.ptr, ctx->d_cb.ptr, ctx->d_cub.ptr, ctx->cub_bytes,
-                           ctx->stream),
+                           ctx->stream, /*counted=*/true),
      "bucket");
-  CU(dtwgpu::launch_update2(S.sq, S.cond, S.psq, S.pinv, p, ctx->d_members.ptr,
+  CU(dtwgpu::launch_update2(S.sq, S.cond, S.psq, S.psq32, S.pinv, p, ctx->d_members.ptr,
                             ctx->d_members_p.ptr, ctx->d_cb.ptr, k, ctx->d_best_member.ptr,
                             ctx->d_best_sum.ptr, ctx->stream),
      "update");
   CU(cudaEventRecord(ctx->km3, ctx->stream), "event");
-  ctx->launches += S.psq ? 6 : 4;
+  ctx->launches += km_update_launches(S) - (S.k <= 256 ? 1 : 0);
   CU(cudaMemcpyAsync(ctx->h_km_dist[buf], ctx->d_dist.ptr, p * 8, cudaMemcpyDeviceToHost,
                      ctx->stream),
      "D2H dist");
@@ -418,7 +463,15 @@ int dtwg_km_stats(dtwg_ctx* ctx, double* out, int reset) {
   out[3] = ctx->km_update_ms;
   out[4] = ctx->km_update_bytes;
   out[5] = ctx->km_prep_ms;
-  out[6] = ctx->layout_valid ? 1.0 : 0.0;
+  out[6] = ctx->layout_valid ? (ctx->layout32 ? 2.0 : 1.0) : 0.0;
+  out[7] = 0.0;
+  if (ctx->layout_valid) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(ctx->layout_ready) == cudaSuccess &&
+        cudaEventElapsedTime(&ms, ctx->layout_t0, ctx->layout_ready) == cudaSuccess)
+      out[7] = ms;
+    cudaGetLastError();
+  }
   if (reset) {
     ctx->km_prep_ms = 0;
     ctx->km_sweeps = 0;
@@ -606,9 +659,11 @@ static int km_run(dtwg_ctx* ctx, int64_t k, int64_t restarts, int64_t max_iterat
 // The matrix views a context's sweeps read: its own, or (restart workers) the source's.
 static KmState km_state(dtwg_ctx* ctx, int64_t p, int64_t k) {
   const dtwg_ctx* m = ctx->km_src ? ctx->km_src : ctx;
-  KmState S{ctx, p, k, km_matrix(ctx), km_is_cond(ctx), nullptr, nullptr, nullptr, 0};
+  KmState S{ctx, p, k, km_matrix(ctx), km_is_cond(ctx), nullptr, false, nullptr, nullptr, 0};
   if (m->layout_valid) {
+    cudaStreamWaitEvent(ctx->stream, m->layout_ready, 0);
     S.psq = m->d_psq.ptr;
+    S.psq32 = m->layout32;
     S.perm = m->d_perm.ptr;
     S.pinv = m->d_pinv.ptr;
   }
@@ -762,12 +817,12 @@ int dtwg_km_update(dtwg_ctx* ctx, const int64_t* medoids, int64_t k, const int64
                            ctx->d_members_p.ptr, ctx->d_cb.ptr, ctx->d_cub.ptr, ctx->cub_bytes,
                            ctx->stream),
      "bucket");
-  CU(dtwgpu::launch_update2(S.sq, S.cond, S.psq, S.pinv, p, ctx->d_members.ptr,
+  CU(dtwgpu::launch_update2(S.sq, S.cond, S.psq, S.psq32, S.pinv, p, ctx->d_members.ptr,
                             ctx->d_members_p.ptr, ctx->d_cb.ptr, k, ctx->d_best_member.ptr,
                             ctx->d_best_sum.ptr, ctx->stream),
      "update");
   CU(cudaEventRecord(ctx->km3, ctx->stream), "event");
-  ctx->launches += S.psq ? 7 : 5;
+  ctx->launches += 1 + km_update_launches(S);
   CU(cudaMemcpyAsync(ctx->h_km_dist[0], ctx->d_dist.ptr, p * 8, cudaMemcpyDeviceToHost, ctx->stream),
      "D2H dist");
   CU(cudaMemcpyAsync(ctx->h_km_cb, ctx->d_cb.ptr, (k + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream),

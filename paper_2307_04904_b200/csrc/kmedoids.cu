@@ -80,15 +80,20 @@ __global__ void expand_square_kernel(const double* __restrict__ cond, int64_t p,
   }
 }
 
-// DistanceMatrix::from_condensed validation (distance_matrix.hpp:34-38).
-__global__ void validate_kernel(const double* __restrict__ cond, int64_t total, int* bad) {
-  int local = 0;
+// DistanceMatrix::from_condensed validation (distance_matrix.hpp:34-38). flags[0]: some
+// entry is not finite or negative; flags[1]: some non-zero entry lies outside
+// [2^-100, 2^100] (the fp32 copy for the k-medoids candidate-sum filter would then lose
+// its relative error bound, see ensure_layout).
+__global__ void validate_kernel(const double* __restrict__ cond, int64_t total, int* flags) {
+  int local = 0, range = 0;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const double v = cond[t];
     if (!(isfinite(v) && v >= 0.0)) local = 1;
+    if (v != 0.0 && !(v >= 0x1p-100 && v <= 0x1p100)) range = 1;
   }
-  if (__any_sync(0xffffffffu, local) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+  if (__any_sync(0xffffffffu, local) && (threadIdx.x & 31) == 0) atomicOr(flags, 1);
+  if (__any_sync(0xffffffffu, range) && (threadIdx.x & 31) == 0) atomicOr(flags + 1, 1);
 }
 
 // kmedoids.hpp:48-52: nearest[j] = std::min(nearest[j], D(j, current)) for unchosen j.
@@ -182,7 +187,7 @@ template <class V>
 __global__ void cluster_select_kernel(const V D, int64_t p, const int32_t* __restrict__ members,
                                       const int64_t* __restrict__ cb,
                                       const double* __restrict__ tsum, int64_t* best_member,
-                                      double* best_sum) {
+                                      double* best_sum, bool in32 = false) {
   const int64_t c = blockIdx.x;
   const int64_t b = cb[c], e = cb[c + 1];
   __shared__ double sv[256];
@@ -201,7 +206,8 @@ __global__ void cluster_select_kernel(const V D, int64_t p, const int32_t* __res
   // (2) contenders: exact sequential sums (ascending members, kmedoids.hpp:111-121)
   const double n = (double)(e - b);
   const double u = 1.1102230246251565e-16;  // 2^-53
-  const double g = n * u / (1.0 - n * u);
+  // fp32 inputs (in32): every term is also rounded once to fp32, relative 2^-24
+  const double g = n * u / (1.0 - n * u) + (in32 ? 0x1p-24 : 0.0);
   const double thr = mn * (1.0 + 8.0 * g) * (1.0 + 4.0 * u);
   // Collect the contenders; the block then computes each one's sequential sum: all
   // threads gather the candidate's member distances into shared memory (parallel loads),
@@ -220,7 +226,14 @@ __global__ void cluster_select_kernel(const V D, int64_t p, const int32_t* __res
   __syncthreads();
   double bv = CUDART_INF;
   int64_t bq = -1;
-  if (ncand <= kMaxCand) {
+  if (ncand == 1) {
+    // A single contender is the reference's choice whatever its exact sum (only the
+    // argmin is used; best_sum then holds the tree sum).
+    if (threadIdx.x == 0) {
+      bv = tsum[cand[0]];
+      bq = cand[0];
+    }
+  } else if (ncand <= kMaxCand) {
     for (int ci = 0; ci < ncand; ++ci) {
       const int64_t q = cand[ci];
       const int64_t a = members[q];
@@ -229,8 +242,17 @@ __global__ void cluster_select_kernel(const V D, int64_t p, const int32_t* __res
         const int64_t len = e - t0 < kChunk ? e - t0 : kChunk;
         for (int64_t t = threadIdx.x; t < len; t += blockDim.x) vals[t] = D(a, __ldg(members + t0 + t));
         __syncthreads();
-        if (threadIdx.x == 0)
-          for (int64_t t = 0; t < len; ++t) sum = __dadd_rn(sum, vals[t]);
+        if (threadIdx.x == 0) {
+          int64_t t = 0;
+          for (; t + 8 <= len; t += 8) {  // loads batched, additions in order
+            double v[8];
+#pragma unroll
+            for (int uu = 0; uu < 8; ++uu) v[uu] = vals[t + uu];
+#pragma unroll
+            for (int uu = 0; uu < 8; ++uu) sum = __dadd_rn(sum, v[uu]);
+          }
+          for (; t < len; ++t) sum = __dadd_rn(sum, vals[t]);
+        }
         __syncthreads();
       }
       // contenders arrive in any order: lexicographic (sum, position) keeps the first minimum
@@ -353,10 +375,14 @@ __global__ void silhouette_kernel(const V D, int64_t p,
 template <class V>
 __global__ void __launch_bounds__(256) assign_slots_kernel(
     const V D, int64_t p, const int64_t* __restrict__ medoids, int64_t k,
-    int64_t* __restrict__ assignment, double* __restrict__ dist, int32_t* __restrict__ lab) {
+    int64_t* __restrict__ assignment, double* __restrict__ dist, int32_t* __restrict__ lab,
+    int32_t* __restrict__ counts) {
   __shared__ double sd[8][32];
   __shared__ int st[8][32];
   __shared__ int sm[8][32];
+  __shared__ int hist[256];  // cluster sizes (counts != nullptr: k <= 256)
+  if (counts)
+    for (int c = threadIdx.x; c < k; c += blockDim.x) hist[c] = 0;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int64_t j0 = (int64_t)blockIdx.x * 32; j0 < p; j0 += (int64_t)gridDim.x * 32) {
     const int64_t j = j0 + lane;
@@ -409,9 +435,13 @@ __global__ void __launch_bounds__(256) assign_slots_kernel(
         dist[j] = b;
         lab[j] = tb;
       }
+      if (counts) atomicAdd(&hist[md >= 0 ? md : tb], 1);
     }
     __syncthreads();
   }
+  if (counts)
+    for (int c = threadIdx.x; c < k; c += blockDim.x)
+      if (hist[c]) atomicAdd(counts + c, hist[c]);
 }
 
 // kmedoids.hpp:88-90 for a caller-given assignment (dtwg_km_update): the cluster slot
@@ -497,7 +527,8 @@ __global__ void inverse_perm_kernel(const int32_t* __restrict__ perm, int64_t p,
 // copy, are ascending -- runs of consecutive u, so the warp's loads are coalesced instead
 // of one 32-byte sector per member. Any summation order: these sums only rule candidates
 // out (cluster_select_kernel).
-__global__ void tree_sum_perm_kernel(const double* __restrict__ psq, int64_t p,
+template <class T>
+__global__ void tree_sum_perm_kernel(const T* __restrict__ psq, int64_t p,
                                      const int32_t* __restrict__ pinv,
                                      const int32_t* __restrict__ members,
                                      const int32_t* __restrict__ members_perm,
@@ -513,17 +544,17 @@ __global__ void tree_sum_perm_kernel(const double* __restrict__ psq, int64_t p,
       else hi = mid - 1;
     }
     const int64_t b = __ldg(cb + lo), e = __ldg(cb + lo + 1);
-    const double* row = psq + (int64_t)__ldg(pinv + __ldg(members + q)) * p;
+    const T* row = psq + (int64_t)__ldg(pinv + __ldg(members + q)) * p;
     double acc0 = 0.0, acc1 = 0.0;
     int64_t t = b + lane;
     for (; t + 224 < e; t += 256) {  // 8 loads in flight per lane
       double v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldg(row + __ldg(members_perm + t + 32 * u));
+      for (int u = 0; u < 8; ++u) v[u] = (double)__ldg(row + __ldg(members_perm + t + 32 * u));
       acc0 = __dadd_rn(acc0, __dadd_rn(__dadd_rn(v[0], v[1]), __dadd_rn(v[2], v[3])));
       acc1 = __dadd_rn(acc1, __dadd_rn(__dadd_rn(v[4], v[5]), __dadd_rn(v[6], v[7])));
     }
-    for (; t < e; t += 32) acc0 = __dadd_rn(acc0, __ldg(row + __ldg(members_perm + t)));
+    for (; t < e; t += 32) acc0 = __dadd_rn(acc0, (double)__ldg(row + __ldg(members_perm + t)));
     double acc = __dadd_rn(acc0, acc1);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
@@ -531,99 +562,125 @@ __global__ void tree_sum_perm_kernel(const double* __restrict__ psq, int64_t p,
   }
 }
 
-// Farthest-point anchors for the cluster-ordered layout (not part of the reference's
-// algorithm; it only decides where rows live): nearest[j] = min(nearest[j], D(a, j)) for
-// the newest anchor a, and each block's (max, lowest index) of nearest.
-__global__ void fpt_update_kernel(const double* __restrict__ sq, int64_t p,
-                                  const int64_t* __restrict__ anchors, int a,
-                                  double* __restrict__ nearest, double* __restrict__ part_v,
-                                  int64_t* __restrict__ part_i) {
-  __shared__ double sv[256];
-  __shared__ int64_t si[256];
-  const int64_t cur = anchors[a - 1];
-  double bv = -1.0;
-  int64_t bi = p;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const double d = sq[cur * p + j];
-    const double v = a == 1 ? d : (d < nearest[j] ? d : nearest[j]);
-    nearest[j] = v;
-    if (v > bv) {  // j ascending per thread: strict > keeps the first
-      bv = v;
-      bi = j;
-    }
-  }
-  sv[threadIdx.x] = bv;
-  si[threadIdx.x] = bi;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) {
-      const double ov = sv[threadIdx.x + w];
-      const int64_t oi = si[threadIdx.x + w];
-      if (ov > sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])) {
-        sv[threadIdx.x] = ov;
-        si[threadIdx.x] = oi;
-      }
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    part_v[blockIdx.x] = sv[0];
-    part_i[blockIdx.x] = si[0];
-  }
-}
-
-__global__ void fpt_pick_kernel(const double* __restrict__ part_v,
-                                const int64_t* __restrict__ part_i, int nblk,
-                                int64_t* __restrict__ anchors, int a) {
-  __shared__ double sv[256];
-  __shared__ int64_t si[256];
-  double bv = -2.0;
-  int64_t bi = 0;
-  for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
-    if (part_v[b] > bv || (part_v[b] == bv && part_i[b] < bi)) {
-      bv = part_v[b];
-      bi = part_i[b];
-    }
-  }
-  sv[threadIdx.x] = bv;
-  si[threadIdx.x] = bi;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) {
-      const double ov = sv[threadIdx.x + w];
-      const int64_t oi = si[threadIdx.x + w];
-      if (ov > sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])) {
-        sv[threadIdx.x] = ov;
-        si[threadIdx.x] = oi;
-      }
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) anchors[a] = si[0];
-}
-
-// psq[u][v] = sq[perm[u]][perm[v]]: one block per output row; the source row (p doubles,
-// contiguous) is gathered through L1/L2 while the output row is written coalesced.
-__global__ void __launch_bounds__(512) permute_square_kernel(const double* __restrict__ sq,
-                                                             int64_t p,
-                                                             const int32_t* __restrict__ perm,
-                                                             double* __restrict__ psq) {
+// psq[u][v] = sq[perm[u]][perm[v]]. Rows up to kPermSmemRow doubles: the source row is
+// staged in shared memory by coalesced 16-byte loads and the output row is written from
+// it, so DRAM reads every source row once. Longer rows gather through L2 with few rows in
+// flight (a grid sized so the rows being gathered stay L2-resident).
+constexpr int kPermSmemRow = 26624;  // 208 KB
+template <class T>
+__global__ void __launch_bounds__(1024) permute_square_smem_kernel(const double* __restrict__ sq,
+                                                                   int64_t p,
+                                                                   const int32_t* __restrict__ perm,
+                                                                   T* __restrict__ psq) {
+  extern __shared__ double row[];
   for (int64_t u = blockIdx.x; u < p; u += gridDim.x) {
     const double* src = sq + (int64_t)__ldg(perm + u) * p;
-    double* dst = psq + u * p;
-    int64_t v = threadIdx.x;
-    for (; v + 3 * 512 < p; v += 4 * 512) {
-      const int32_t c0 = __ldg(perm + v), c1 = __ldg(perm + v + 512);
-      const int32_t c2 = __ldg(perm + v + 1024), c3 = __ldg(perm + v + 1536);
-      const double a0 = __ldg(src + c0), a1 = __ldg(src + c1);
-      const double a2 = __ldg(src + c2), a3 = __ldg(src + c3);
-      __stcs(dst + v, a0);
-      __stcs(dst + v + 512, a1);
-      __stcs(dst + v + 1024, a2);
-      __stcs(dst + v + 1536, a3);
+    if ((p & 1) == 0) {
+      const double2* s2 = reinterpret_cast<const double2*>(src);
+      double2* r2 = reinterpret_cast<double2*>(row);
+      for (int64_t v = threadIdx.x; v < p / 2; v += blockDim.x) r2[v] = __ldcs(s2 + v);
+    } else {
+      for (int64_t v = threadIdx.x; v < p; v += blockDim.x) row[v] = __ldcs(src + v);
     }
-    for (; v < p; v += 512) __stcs(dst + v, __ldg(src + __ldg(perm + v)));
+    __syncthreads();
+    T* dst = psq + u * p;
+    for (int64_t v = threadIdx.x; v < p; v += blockDim.x) __stcs(dst + v, (T)row[__ldg(perm + v)]);
+    __syncthreads();
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(512) permute_square_l2_kernel(const double* __restrict__ sq,
+                                                                int64_t p,
+                                                                const int32_t* __restrict__ perm,
+                                                                T* __restrict__ psq) {
+  for (int64_t u = blockIdx.x; u < p; u += gridDim.x) {
+    const double* src = sq + (int64_t)__ldg(perm + u) * p;
+    T* dst = psq + u * p;
+    for (int64_t v = threadIdx.x; v < p; v += 512)
+      __stcs(dst + v, (T)__ldg(src + __ldg(perm + v)));
+  }
+}
+
+
+// Device bucketing for k <= kBucketSmallK (kmedoids.hpp:86-92): counts per cluster slot,
+// then one block per (cluster, order) compacts the series of that cluster in ascending
+// order -- series index order (members) or, for the cluster-ordered copy, position order
+// (members_perm) -- with warp ballots/scans; each block derives its cluster's start from
+// the counts, so the bounds cb come out of the same pass. Integer-only and deterministic.
+constexpr int kBucketSmallK = 256;
+__global__ void cluster_count_kernel(const int32_t* __restrict__ lab, int64_t p, int64_t k,
+                                     int32_t* __restrict__ counts) {
+  __shared__ int h[kBucketSmallK];
+  for (int c = threadIdx.x; c < k; c += blockDim.x) h[c] = 0;
+  __syncthreads();
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p;
+       j += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&h[lab[j]], 1);
+  __syncthreads();
+  for (int c = threadIdx.x; c < k; c += blockDim.x)
+    if (h[c]) atomicAdd(counts + c, h[c]);
+}
+
+__global__ void __launch_bounds__(1024) cluster_compact_kernel(
+    const int32_t* __restrict__ lab, const int32_t* __restrict__ perm, int64_t p, int64_t k,
+    const int32_t* __restrict__ counts, int32_t* __restrict__ members,
+    int32_t* __restrict__ members_perm, int64_t* __restrict__ cb) {
+  __shared__ int wsum[32];
+  __shared__ int64_t sbase;
+  const int c = blockIdx.x % k;
+  const bool by_pos = blockIdx.x >= k;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (w == 0) {
+    int64_t b = 0;
+    for (int x = lane; x < c; x += 32) b += counts[x];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+    if (lane == 0) {
+      sbase = b;
+      if (!by_pos) {
+        cb[c] = b;
+        if (c == k - 1) cb[k] = p;
+      }
+    }
+  }
+  __syncthreads();
+  int32_t* out = by_pos ? members_perm : members;
+  int64_t running = sbase;
+  for (int64_t c0 = 0; c0 < p; c0 += 8 * 1024) {
+    const int64_t u0 = c0 + 8 * (int64_t)tid;
+    bool f[8];
+    int cnt = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t u = u0 + i;
+      f[i] = u < p && (by_pos ? __ldg(lab + __ldg(perm + u)) : __ldg(lab + u)) == c;
+      cnt += f[i];
+    }
+    int x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int v = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      wsum[lane] = v;
+    }
+    __syncthreads();
+    int64_t off = running + (w ? wsum[w - 1] : 0) + x - cnt;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (f[i]) out[off++] = (int32_t)(u0 + i);
+    running += wsum[31];
+    __syncthreads();
   }
 }
 
@@ -669,9 +726,9 @@ cudaError_t launch_expand_square(const double* condensed, int64_t p, double* squ
   return cudaGetLastError();
 }
 
-cudaError_t launch_validate_condensed(const double* condensed, int64_t total, int* bad,
+cudaError_t launch_validate_condensed(const double* condensed, int64_t total, int* flags,
                                       cudaStream_t s) {
-  validate_kernel<<<grid_for(total, 256), 256, 0, s>>>(condensed, total, bad);
+  validate_kernel<<<grid_for(total, 256), 256, 0, s>>>(condensed, total, flags);
   return cudaGetLastError();
 }
 
@@ -725,14 +782,19 @@ cudaError_t launch_update(const double* matrix, bool condensed, int64_t p,
 // ---- round-2 sweep launchers ----------------------------------------------------------
 cudaError_t launch_assign_slots(const double* matrix, bool condensed, int64_t p,
                                 const int64_t* medoids, int64_t k, int64_t* assignment,
-                                double* dist, int32_t* lab, cudaStream_t s) {
+                                double* dist, int32_t* lab, cudaStream_t s, int32_t* counts) {
+  if (counts && k > 256) counts = nullptr;
+  if (counts) {
+    const cudaError_t e = cudaMemsetAsync(counts, 0, k * sizeof(int32_t), s);
+    if (e != cudaSuccess) return e;
+  }
   const unsigned blocks = (unsigned)std::min<int64_t>((p + 31) / 32, 148 * 8);
   if (condensed)
     assign_slots_kernel<<<blocks, 256, 0, s>>>(CondView{matrix, p}, p, medoids, k, assignment,
-                                                dist, lab);
+                                                dist, lab, counts);
   else
     assign_slots_kernel<<<blocks, 256, 0, s>>>(SquareView{matrix, p}, p, medoids, k, assignment,
-                                                dist, lab);
+                                                dist, lab, counts);
   return cudaGetLastError();
 }
 
@@ -789,11 +851,22 @@ cudaError_t launch_iota(int32_t* out, int64_t n, cudaStream_t s) {
 cudaError_t launch_bucket(const int32_t* lab, const int32_t* perm, const int32_t* iota, int64_t p,
                           int64_t k, int32_t* keys_a, int32_t* keys_b, int32_t* members,
                           int32_t* members_perm, int64_t* cb, void* tmp, size_t tmp_bytes,
-                          cudaStream_t s) {
+                          cudaStream_t s, bool counted) {
+  cudaError_t e;
+  if (k <= kBucketSmallK) {
+    // keys_a holds the int32 cluster sizes (counted: already by assign_slots)
+    if (!counted) {
+      if ((e = cudaMemsetAsync(keys_a, 0, k * sizeof(int32_t), s)) != cudaSuccess) return e;
+      cluster_count_kernel<<<(unsigned)std::min<int64_t>((p + 255) / 256, 148), 256, 0, s>>>(
+          lab, p, k, keys_a);
+    }
+    cluster_compact_kernel<<<(unsigned)(perm ? 2 * k : k), 1024, 0, s>>>(
+        lab, perm, p, k, keys_a, members, members_perm, cb);
+    return cudaGetLastError();
+  }
   const int bits = key_bits(k);
   size_t bytes = tmp_bytes;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, bytes, lab, keys_a, iota, members, (int)p,
-                                                  0, bits, s);
+  e = cub::DeviceRadixSort::SortPairs(tmp, bytes, lab, keys_a, iota, members, (int)p, 0, bits, s);
   if (e != cudaSuccess) return e;
   cluster_bounds_kernel<<<grid_for(p, 256), 256, 0, s>>>(keys_a, p, k, cb);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -808,7 +881,7 @@ cudaError_t launch_bucket(const int32_t* lab, const int32_t* perm, const int32_t
 // Candidate sums + per-cluster selection (kmedoids.hpp:111-121). With psq (the
 // cluster-ordered copy) the sums read contiguous runs; the contenders' exact sequential
 // sums always read the square in ascending member order (cluster_select_kernel).
-cudaError_t launch_update2(const double* matrix, bool condensed, const double* psq,
+cudaError_t launch_update2(const double* matrix, bool condensed, const void* psq, bool psq32,
                            const int32_t* pinv, int64_t p, const int32_t* members,
                            const int32_t* members_perm, const int64_t* cluster_begin,
                            int64_t k, int64_t* best_member, double* best_sum,
@@ -819,39 +892,58 @@ cudaError_t launch_update2(const double* matrix, bool condensed, const double* p
   double* sums = best_sum + k;
   const int64_t warps = std::min<int64_t>(p, 148 * 64);
   const unsigned tb = (unsigned)((warps + 7) / 8);
-  tree_sum_perm_kernel<<<tb, 256, 0, s>>>(psq, p, pinv, members, members_perm, cluster_begin, k,
-                                          sums);
+  if (psq32)
+    tree_sum_perm_kernel<float><<<tb, 256, 0, s>>>((const float*)psq, p, pinv, members,
+                                                   members_perm, cluster_begin, k, sums);
+  else
+    tree_sum_perm_kernel<double><<<tb, 256, 0, s>>>((const double*)psq, p, pinv, members,
+                                                    members_perm, cluster_begin, k, sums);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   cluster_select_kernel<<<(unsigned)k, 256, 0, s>>>(SquareView{matrix, p}, p, members,
-                                                    cluster_begin, sums, best_member, best_sum);
+                                                    cluster_begin, sums, best_member, best_sum,
+                                                    psq32);
   return cudaGetLastError();
 }
 
-// The cluster-ordered copy of the square: farthest-point anchors (deterministic, on the
-// device), each series' nearest anchor, a stable sort by anchor -> perm, and the copy.
-cudaError_t launch_cluster_layout(const double* sq, int64_t p, int n_anchor, int64_t* anchors,
-                                  double* nearest, double* part_v, int64_t* part_i,
+// The cluster-ordered copy of the square: each series' nearest anchor (anchors given,
+// ascending), a stable sort by anchor -> perm, its inverse, and the copy.
+cudaError_t launch_cluster_layout(const double* sq, int64_t p, int n_anchor, const int64_t* anchors,
                                   int64_t* asg_tmp, double* dist_tmp, int32_t* lab,
                                   int32_t* keys_tmp, const int32_t* iota, int32_t* perm,
-                                  int32_t* pinv, double* psq, void* tmp, size_t tmp_bytes,
-                                  cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(anchors, 0, sizeof(int64_t), s);  // first anchor: series 0
-  if (e != cudaSuccess) return e;
-  const int nblk = (int)std::min<int64_t>((p + 255) / 256, 1024);
-  for (int a = 1; a < n_anchor; ++a) {
-    fpt_update_kernel<<<nblk, 256, 0, s>>>(sq, p, anchors, a, nearest, part_v, part_i);
-    fpt_pick_kernel<<<1, 256, 0, s>>>(part_v, part_i, nblk, anchors, a);
-  }
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  e = launch_assign_slots(sq, false, p, anchors, n_anchor, asg_tmp, dist_tmp, lab, s);
+                                  int32_t* pinv, void* psq, bool psq32, void* tmp,
+                                  size_t tmp_bytes, int num_sms, cudaStream_t s) {
+  cudaError_t e = launch_assign_slots(sq, false, p, anchors, n_anchor, asg_tmp, dist_tmp, lab, s,
+                                      nullptr);
   if (e != cudaSuccess) return e;
   size_t bytes = tmp_bytes;
   e = cub::DeviceRadixSort::SortPairs(tmp, bytes, lab, keys_tmp, iota, perm, (int)p, 0,
                                       key_bits(n_anchor), s);
   if (e != cudaSuccess) return e;
   inverse_perm_kernel<<<grid_for(p, 256), 256, 0, s>>>(perm, p, pinv);
-  permute_square_kernel<<<(unsigned)std::min<int64_t>(p, 148 * 8), 512, 0, s>>>(sq, p, perm, psq);
+  if (p <= kPermSmemRow) {
+    const int smem = (int)(p * sizeof(double));
+    const unsigned g = (unsigned)std::min<int64_t>(p, num_sms);
+    if (psq32) {
+      e = cudaFuncSetAttribute(permute_square_smem_kernel<float>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      permute_square_smem_kernel<float><<<g, 1024, smem, s>>>(sq, p, perm, (float*)psq);
+    } else {
+      e = cudaFuncSetAttribute(permute_square_smem_kernel<double>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      permute_square_smem_kernel<double><<<g, 1024, smem, s>>>(sq, p, perm, (double*)psq);
+    }
+  } else {
+    // ~48 MB of source rows in flight
+    const int64_t rows = std::max<int64_t>(1, (int64_t)(48 << 20) / (p * 8));
+    const unsigned g = (unsigned)std::min<int64_t>(p, rows);
+    if (psq32)
+      permute_square_l2_kernel<float><<<g, 512, 0, s>>>(sq, p, perm, (float*)psq);
+    else
+      permute_square_l2_kernel<double><<<g, 512, 0, s>>>(sq, p, perm, (double*)psq);
+  }
   return cudaGetLastError();
 }
 

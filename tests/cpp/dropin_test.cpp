@@ -160,9 +160,52 @@ int main() {
          KMedoidsConfig cfg;
          cfg.k = 3;
          cfg.seed = 2024;
-         require(dtwclust::kmedoids(lazy, cfg) == dtwclust::kmedoids(gpu, cfg), "results differ");
+         std::vector<double> ta, tb;
+         const ClusterResult a =
+             dtwclust::kmedoids(lazy, cfg, [&](std::size_t, std::size_t, double c) { ta.push_back(c); });
+         // unqualified call, as runner.hpp:211 makes it: resolves to the GPU sweeps (ADL)
+         const ClusterResult b = kmedoids(gpu, cfg, [&](std::size_t, std::size_t, double c) { tb.push_back(c); });
+         require(a == b, "results differ");
+         require(ta == tb, "observer traces differ");
          require(gpu.computed_pairs() == 60 * 59 / 2, "computed_pairs");
-         return "kmedoids(lazy) == kmedoids(GpuDistanceSource); computed_pairs = p(p-1)/2";
+         // host-side reads equal the reference's lazily computed ones
+         for (std::size_t i = 0; i < 60; i += 7)
+           for (std::size_t j = 0; j < 60; j += 5)
+             require(lazy.distance(i, j) == gpu.distance(i, j), "distance differs");
+         return "kmedoids(lazy) == kmedoids(GpuDistanceSource) on the device, same trace";
+       }},
+      {"lazy source: lazy errors (index, diagonal, infeasible pair)",
+       [] {
+         // lengths 40..90 with a narrow band, no auto-widen: some pairs are infeasible
+         const auto ds = walks(9, 30, 40, 90);
+         dtwclust::LazyDistanceSource lazy(ds, WarpWindow::banded(5), false);
+         dtwgpu::GpuDistanceSource gpu(ds, WarpWindow::banded(5), false);
+         std::string e1, e2;
+         try { lazy.distance(3, 30); } catch (const IndexOutOfRangeError& e) { e1 = e.what(); }
+         try { gpu.distance(3, 30); } catch (const IndexOutOfRangeError& e) { e2 = e.what(); }
+         require(!e1.empty() && e1 == e2, "index error differs");
+         require(gpu.distance(4, 4) == 0.0 && gpu.computed_pairs() == 0, "diagonal did work");
+         std::size_t checked = 0, infeasible = 0;
+         for (std::size_t i = 0; i < 30; ++i)
+           for (std::size_t j = 0; j < 30; ++j) {
+             std::string a, b;
+             double va = -1, vb = -2;
+             try { va = lazy.distance(i, j); } catch (const BandInfeasibleError& e) { a = e.what(); }
+             try { vb = gpu.distance(i, j); } catch (const BandInfeasibleError& e) { b = e.what(); }
+             require(a == b, "errors differ at (" + std::to_string(i) + "," + std::to_string(j) + ")");
+             if (a.empty()) require(va == vb, "distance differs");
+             infeasible += !a.empty();
+             ++checked;
+           }
+         require(infeasible > 0, "no infeasible pair in the test data");
+         KMedoidsConfig cfg;
+         cfg.k = 3;
+         std::string k1, k2;
+         try { dtwclust::kmedoids(lazy, cfg); } catch (const BandInfeasibleError& e) { k1 = e.what(); }
+         try { kmedoids(gpu, cfg); } catch (const BandInfeasibleError& e) { k2 = e.what(); }
+         require(k1 == k2, "kmedoids errors differ: '" + k1 + "' vs '" + k2 + "'");
+         return std::to_string(checked) + " requests, " + std::to_string(infeasible) +
+                " infeasible with the reference's message; kmedoids error '" + k2 + "'";
        }},
       {"matrix files: byte-identical text, round trips, same first error",
        [] {

@@ -328,3 +328,20 @@ def test_cluster_layout_duplicates_and_empty_clusters(monkeypatch, p, k):
     sq = sq[np.ix_(dup, dup)]
     D = np.ascontiguousarray(sq[iu])
     check_same(D, p, KMedoidsConfig(k=k, restarts=5, seed=3))
+
+
+@pytest.mark.parametrize("layout", ["0", "1"])
+def test_many_clusters_radix_bucketing(monkeypatch, layout):
+    """k > 256 takes the radix-sort bucketing (cub) instead of the per-cluster compaction;
+    with and without the cluster-ordered copy the result equals the reference's."""
+    monkeypatch.setenv("DTWGPU_KM_LAYOUT", layout)
+    monkeypatch.setenv("DTWGPU_KM_LAYOUT_MIN_P", "2")
+    p = 700
+    D = random_condensed(ScalarRng(77), p)
+    check_same(D, p, KMedoidsConfig(k=300, restarts=2, seed=4))
+    m = DistanceMatrix.from_condensed(p, D)
+    medoids = sorted(np.random.default_rng(3).choice(p, 290, replace=False).tolist())
+    if oracle.have_ref():
+        asg_ref, _, upd_ref = oracle.ref_sweep(D, p, medoids)
+        assert api.assign_to_medoids(m, medoids) == list(asg_ref)
+        assert api.update_medoids(m, medoids, list(asg_ref)) == list(upd_ref)
