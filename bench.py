@@ -581,7 +581,15 @@ def run_gpu_arm(a, ds):
         kmed = {"headline_config": {"k": ds.k, "restarts": ds.restarts,
                                     "seconds": time.perf_counter() - t0,
                                     "total_cost": best[0], "best_restart": best[1],
-                                    "restarts_on_this_rank": list(range(rank, ds.restarts, world))}}
+                                    "restarts_on_rank0": dd.restarts_of_rank(ds.restarts, 0, world)}}
+        if rank == 0 and a.check and p <= 5000:
+            # the reduced result against the reference's own kmedoids on the same matrix
+            import oracle
+            D = eng.download(p)
+            fn = oracle.ref_kmedoids if oracle.have_ref() else oracle.kmedoids
+            rmed, rasg, rcost = fn(D, p, ds.k, ds.restarts, 100, 0)
+            kmed["headline_config"]["parity"] = bool(
+                list(rmed) == list(best[2]) and list(rasg) == list(best[3]) and rcost == best[0])
 
     cpu = None
     if rank == 0 and world == 1 and a.cpu_baseline:

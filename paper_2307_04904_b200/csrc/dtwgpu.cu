@@ -200,8 +200,18 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
     const bool multipass = pc.cfg.family == Family::Full && pc.cfg.mp &&
                            (ctx->uniform ? (ctx->h_len[0] > W) : true);
     if (multipass && count > 0) {
+      // One boundary column per resident lane group: with one lane per pair and very long
+      // series that is max_n * 8 B * 37,888 groups (30 GB at n = 1e5). Cap the class's
+      // scratch at a share of free HBM by running fewer (persistent, grid-stride) blocks.
+      const int64_t per_block = (pc.max_n + kScratchPad) * groups_per_block;
+      size_t free_b = 0, total_b = 0;
+      if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = size_t(8) << 30;
+      const int64_t budget = std::min<int64_t>((int64_t)(free_b / 4 / sizeof(double)),
+                                               env_or("DTWGPU_SCRATCH_MAX_MB", 16384) << 17);
+      const int64_t cap = std::max<int64_t>(1, budget / std::max<int64_t>(per_block, 1));
+      if (blocks_of[c] > cap) blocks_of[c] = cap;
       scratch_off[c] = scratch_total;
-      scratch_total += (pc.max_n + kScratchPad) * blocks_of[c] * groups_per_block;
+      scratch_total += per_block * blocks_of[c];
     }
   }
   if (scratch_total) CU(ctx->d_scratch.reserve((size_t)scratch_total), "cudaMalloc scratch");

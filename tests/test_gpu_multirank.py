@@ -22,7 +22,7 @@ def test_two_rank_bench_assembles_the_matrix(config, subset, exchange):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", "--master-port=29531", os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "2", "--warmup", "1", "--config", str(config),
-           "--subset", str(subset), "--dist-backend", "gloo", "--no-cpu-baseline", "--kmedoids",
+           "--subset", str(subset), "--dist-backend", "gloo", "--no-cpu-baseline", "--kmedoids-headline",
            "--exchange", exchange]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
@@ -31,4 +31,7 @@ def test_two_rank_bench_assembles_the_matrix(config, subset, exchange):
     assert d["n_gpus"] == 2 and d["value"] > 0
     assert d["config"]["exchange"] == exchange, d["config"]
     assert d["parity"].startswith("8/8"), d["parity"]
-    assert d["kmedoids"]["parity"] is True
+    assert d["kmedoids"]["headline_config"]["parity"] is True
+    # per-rank fill/exchange times and the e2e D2H of each rank's own slice
+    assert [r["rank"] for r in d["per_rank"]] == [0, 1]
+    assert d["e2e"]["d2h_bytes_per_step"] > 0 and d["e2e"]["value"] > 0
