@@ -454,6 +454,7 @@ def run_gpu_arm(a, ds):
             dist.barrier()
     step_ms = [s.elapsed_time(t) for s, t in evs]
     launches = eng.launch_count() - launches0
+    headline_plan = eng.last_plan()  # before e2e / all_configs replan other workloads
     my_ms = sum(step_ms)
     t = torch.tensor([my_ms], dtype=torch.float64, device="cpu" if gloo else dev)
     if world > 1:
@@ -623,7 +624,7 @@ def run_gpu_arm(a, ds):
                                        if world > 1 else "condensed-slot shards x1"),
                        "exchange": exchange,
                        "l2": "flushed (256 MB write) between timed steps",
-                       "plan": eng.last_plan()},
+                       "plan": headline_plan},
             "pairs_per_s": total * a.steps / (max_ms * 1e-3),
             "roofline": {"bound": "fp64" if prec == 0 else "fp32",
                          "achieved": achieved, "peak": peak,

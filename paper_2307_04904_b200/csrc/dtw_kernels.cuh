@@ -327,12 +327,14 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
           // lane 0 loads its boundary rows unconditionally: a predicated load, no branch.
           if constexpr (MP)
             if (use_bnd) bq[t] = bnd[r0 + TR + t];
-          L[t] = __shfl_up_sync(kFull, send[t], 1, G);
+          // G = 1: no left neighbour (lane 0 of its own group takes the boundary below)
+          if constexpr (G > 1) L[t] = __shfl_up_sync(kFull, send[t], 1, G);
+          else L[t] = INF;
         }
         if constexpr (kF32) {
           // Neighbour values are relative to its offset: add the (fp32-rounded) offset
           // difference once per row (inf stays inf). Lane 0 reads absolute fp64 values.
-          const double loff = __shfl_up_sync(kFull, send_off, 1, G);
+          const double loff = G > 1 ? __shfl_up_sync(kFull, send_off, 1, G) : 0.0;
           const T delta = (T)(loff - off);
 #pragma unroll
           for (int t = 0; t < TR; ++t) {
