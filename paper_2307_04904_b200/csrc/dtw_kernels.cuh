@@ -253,7 +253,10 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
   const int gw = lane / G;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  double* bnd = A.scratch ? A.scratch + (warp * GPW + gw) * A.scratch_stride : nullptr;
+  // The warp's GPW boundary columns interleaved by row (column of group gw at
+  // bnd[row * GPW]), so the boundary loads and stores of a warp's groups for one row are
+  // GPW consecutive doubles (one or a few sectors) instead of GPW scattered ones.
+  double* bnd = A.scratch ? A.scratch + warp * GPW * A.scratch_stride + gw : nullptr;
   const T INF = Ar::inf();
   const T* S = Ar::base(A);
 
@@ -290,7 +293,7 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
       T diag0 = INF;  // cell (r0-1, jl-1)
       if (gl == 0) {
         if (pass == 0) diag0 = (rs == 1) ? T(0) : INF;
-        else if (rs - 1 >= 1 && rs - 1 <= written_hi) diag0 = (T)bnd[rs - 1];
+        else if (rs - 1 >= 1 && rs - 1 <= written_hi) diag0 = (T)bnd[(rs - 1) * GPW];
       }
       double off = 0.0;  // fp32: this lane's offset
       T send[TR];
@@ -312,7 +315,7 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
         xq[t] = __ldg(X + (r0 + t - 1));
         bq[t] = (double)Ar::inf();
         if constexpr (MP)
-          if (use_bnd) bq[t] = bnd[r0 + t];
+          if (use_bnd) bq[t] = bnd[(r0 + t) * GPW];
       }
 
       for (int s = 0; s < nsteps; ++s, r0 += TR) {
@@ -326,7 +329,7 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
           // Rows past the previous pass's last row hold +inf (written at its end), so
           // lane 0 loads its boundary rows unconditionally: a predicated load, no branch.
           if constexpr (MP)
-            if (use_bnd) bq[t] = bnd[r0 + TR + t];
+            if (use_bnd) bq[t] = bnd[(r0 + TR + t) * GPW];
           // G = 1: no left neighbour (lane 0 of its own group takes the boundary below)
           if constexpr (G > 1) L[t] = __shfl_up_sync(kFull, send[t], 1, G);
           else L[t] = INF;
@@ -404,8 +407,8 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
           for (int t = 0; t < TR; ++t) {
             send[t] = out[t];
             if (wb && t < nr) {
-              if constexpr (kF32) bnd[r0 + t] = (double)out[t] + off;  // +inf + off = +inf
-              else bnd[r0 + t] = out[t];
+              if constexpr (kF32) bnd[(r0 + t) * GPW] = (double)out[t] + off;  // +inf + off = +inf
+              else bnd[(r0 + t) * GPW] = out[t];
             }
           }
           // pv now holds row r0 + nr - 1; row n is the last row of the last pass (re = n).
@@ -421,7 +424,7 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
         // The next pass ends at most W rows lower; its rows past this pass's last one
         // lie outside the band at this pass's last column (+inf).
         if (wb)
-          for (int r = re + 1; r <= min(n, re + W); ++r) bnd[r] = (double)INF;
+          for (int r = re + 1; r <= min(n, re + W); ++r) bnd[r * GPW] = (double)INF;
       }
       written_hi = re;
       __syncwarp();
@@ -518,133 +521,6 @@ __global__ void __launch_bounds__(kThreads) dtw_lane_kernel(const FillArgs A) {
         result = (double)rv;
       }
       diag0 = INF;  // column 0 below row 0
-    }
-    if (valid) store_result(A, P.slot, result);
-  }
-}
-
-// ===================================================================================
-// One lane per pair, multi-pass (fp64; dtw_lanemp_kernel). As dtw_lane_kernel, for
-// pairs wider than R. Measured slower than the wavefront kernels so far (c4 2110 against
-// 2192 GCUPS) and not planned; kept for forced runs. The Full family with G = 1, except that the strip's R y
-// samples live in shared memory (a lane's 2R row registers do not fit in fp64): each lane
-// stages its own strip's y and reads it with immediate-offset LDS, one per cell. No
-// neighbour shuffles and no wavefront fill/drain: a pair's rows run back to back (c3:
-// 1.0x the in-band cells computed instead of 1.09x for G = 2), and the lanes of a warp
-// run their own pairs in lockstep up to the warp's longest pass. MP: pairs wider than R
-// run in passes, the strip's last column handed to the next pass through the lane's own
-// boundary column in global memory (read and overwritten in place, row by row). Band
-// edges use the Full family's kill cells; rows outside the pass's band range are skipped.
-// ===================================================================================
-template <int R, int TR, bool MASK, class Ar, bool MP = true>
-__global__ void __launch_bounds__(kThreads) dtw_lanemp_kernel(const FillArgs A) {
-  using T = typename Ar::T;
-  constexpr int YS = (R % 2) ? R : R + 1;  // odd stride (doubles): conflict-free LDS.64
-  __shared__ T ysm[kThreads * YS];
-  // volatile: one LDS per cell, not hoisted into (2R more) registers
-  volatile T* ys = ysm + threadIdx.x * YS;
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  const T INF = Ar::inf();
-  const T* S = Ar::base(A);
-  const int64_t base0 = tid - (threadIdx.x & 31);  // the warp's first item
-  // The warp's 32 boundary columns interleaved by row (bnd[row * 32]), so a warp's
-  // boundary loads and stores of one row are one coalesced 256-byte access.
-  double* bnd = MP ? A.scratch + (tid >> 5) * 32 * A.scratch_stride + (tid & 31) : nullptr;
-
-  for (int64_t base = base0; base < A.count; base += nthreads) {
-    const int64_t item = base + (threadIdx.x & 31);
-    const bool valid = item < A.count;
-    const Pair P = load_pair(A, valid ? item : base);
-    const T* X = S + P.xoff;
-    const T* Y = S + P.yoff;
-    const int n = P.n, m = P.m, hw = P.hw;
-    const int npass_l = valid ? (MP ? (m + R - 1) / R : 1) : 0;
-    const int npass = MP ? __reduce_max_sync(kFull, npass_l) : 1;
-    double result = 0.0;
-    for (int pass = 0; pass < npass; ++pass) {
-      const int c0 = pass * R;
-      int rs = 1, re = n;
-      if (MASK) {
-        rs = max(1, c0 + 1 - hw);
-        re = min(n, c0 + R + hw);
-      }
-      if (pass >= npass_l) re = rs - 1;  // this lane is done
-      const bool last = pass == npass_l - 1;
-      const bool wb = MP && !last && re >= rs;
-#pragma unroll
-      for (int r = 0; r < R; ++r) ys[r] = (c0 + r < m) ? __ldg(Y + c0 + r) : T(0);
-      T pv[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) pv[r] = INF;
-      // cell (rs - 1, c0): row 0 -> (0, 0) = 0 or +inf; else the previous pass's column
-      T diag0 = (rs == 1) ? (pass == 0 ? T(0) : INF) : (MP ? (T)bnd[(rs - 1) * 32] : INF);
-      const int steps = __reduce_max_sync(kFull, re >= rs ? (re - rs + TR) / TR : 0);
-      int r0 = rs;
-      T xq[TR];
-      double bq[TR];
-#pragma unroll
-      for (int t = 0; t < TR; ++t) {
-        xq[t] = __ldg(X + (min(r0 + t, n) - 1));
-        bq[t] = (MP && pass > 0) ? bnd[(r0 + t) * 32] : (double)INF;
-      }
-      for (int s = 0; s < steps; ++s, r0 += TR) {
-        T x[TR], L[TR];
-#pragma unroll
-        for (int t = 0; t < TR; ++t) {
-          x[t] = xq[t];
-          L[t] = (T)bq[t];
-          xq[t] = __ldg(X + (min(r0 + TR + t, n) - 1));
-          if (MP && pass > 0) bq[t] = bnd[(r0 + TR + t) * 32];
-        }
-        const int klo = r0 - hw - 2 - c0, khi = r0 + hw - c0;  // kill columns of row r0
-        int need = 0;
-        if (MASK) {
-          const int mine = (r0 <= re) ? kill_need<R, TR>(klo, khi) : 0;
-          need = (__any_sync(kFull, mine & 1) ? 1 : 0) | (__any_sync(kFull, mine & 2) ? 2 : 0);
-        }
-        T out[TR];
-        int done = 0;  // rows of this step computed (pv then holds row r0 + done - 1)
-        if (r0 + TR - 1 <= re) {
-          if (need == 0) FullRows<R, TR, 0, Ar>::run(pv, ys, x, diag0, L, klo, khi, out);
-          else if (need == 1) FullRows<R, TR, 1, Ar>::run(pv, ys, x, diag0, L, klo, khi, out);
-          else if (need == 2) FullRows<R, TR, 2, Ar>::run(pv, ys, x, diag0, L, klo, khi, out);
-          else FullRows<R, TR, 3, Ar>::run(pv, ys, x, diag0, L, klo, khi, out);
-          diag0 = L[TR - 1];
-          done = TR;
-        } else if (r0 <= re) {
-          // The pass's last re - r0 + 1 < TR rows, one at a time.
-#pragma unroll
-          for (int t = 0; t < TR - 1; ++t) {
-            if (r0 + t <= re) {
-              const T xt[1] = {x[t]};
-              const T Lt[1] = {L[t]};
-              T ot[1];
-              FullRows<R, 1, MASK ? 3 : 0, Ar>::run(pv, ys, xt, diag0, Lt, klo + t, khi + t, ot);
-              out[t] = ot[0];
-              diag0 = L[t];
-              done = t + 1;
-            }
-          }
-        }
-        if (wb) {
-#pragma unroll
-          for (int t = 0; t < TR; ++t)
-            if (t < done) bnd[(r0 + t) * 32] = (double)out[t];
-        }
-        if (last && done > 0 && r0 + done - 1 == n) {
-          T rv = pv[0];
-#pragma unroll
-          for (int r = 1; r < R; ++r) rv = (r == m - 1 - c0) ? pv[r] : rv;
-          result = (double)rv;
-        }
-      }
-      if constexpr (MP && MASK) {
-        // Rows the next pass may read past this pass's last one lie outside the band at
-        // this pass's last column (+inf).
-        if (wb)
-          for (int r = re + 1; r <= min(n, re + R); ++r) bnd[r * 32] = (double)INF;
-      }
     }
     if (valid) store_result(A, P.slot, result);
   }

@@ -20,12 +20,7 @@ struct BandTable {
 const void* band32_kernel_ptr(int R, int kr, int P, bool fp32) {
 #define DTWG_B(g, r)                                                              \
   if (g == 32 && R == r) {                                                        \
-    if (P == 2) {                                                                 \
-      if constexpr (r > 7) return nullptr; /* P = 2 only where the code is small */ \
-      if (fp32) return (const void*)dtw_band_kernel<g, r, -1, 2, F32>;           \
-      if (kr < 0) return (const void*)dtw_band_kernel<g, r, -1, 2, F64>;         \
-      return BandTable<g, r, r - 1, 2>::get(kr);                                  \
-    }                                                                             \
+    if (P != 1) return nullptr; /* P = 2 measured slower everywhere; not built */  \
     if (fp32) return (const void*)dtw_band_kernel<g, r, -1, 1, F32>;             \
     if (kr < 0) return (const void*)dtw_band_kernel<g, r, -1, 1, F64>;           \
     return BandTable<g, r, r - 1, 1>::get(kr);                                    \

@@ -32,8 +32,7 @@ const void* full_kernel_ptr(int G, int R, int TR, bool mask, bool fp32, bool mp)
 #undef DTWG_F32
 #define DTWG_L64(r, tr)                                                                     \
   if (!fp32 && G == 1 && R == r && TR == tr) {                                              \
-    if (mp) return mask ? (const void*)dtw_lanemp_kernel<r, tr, true, F64>                  \
-                        : (const void*)dtw_lanemp_kernel<r, tr, false, F64>;                \
+    if (mp) return nullptr; /* multi-pass one-lane fp64: dtw_full_kernel<1, R, 4> */    \
     return mask ? (const void*)dtw_lane_kernel<r, tr, true, F64>                            \
                 : (const void*)dtw_lane_kernel<r, tr, false, F64>;                          \
   }

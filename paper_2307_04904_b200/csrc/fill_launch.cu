@@ -7,7 +7,10 @@
 namespace dtwgpu {
 
 static const void* kernel_ptr(const KernelCfg& c) {
-  if (c.family == Family::Full) return full_kernel_ptr(c.G, c.R, c.TR, c.mask, c.fp32, c.mp);
+  if (c.family == Family::Full) {
+    const void* f = full_kernel_ptr(c.G, c.R, c.TR, c.mask, c.fp32, c.mp);
+    return (f || c.fp32) ? f : full64_kernel_ptr(c.G, c.R, c.TR, c.mask, c.mp);
+  }
   if (c.family == Family::Strip) return c.G == 32 ? strip_kernel_ptr(c.R, c.TR, c.mask, c.fp32) : nullptr;
   if (c.ring && c.U > 1) return c.P == 1 ? unit_kernel_ptr(c.G, c.R, c.U, c.kr, c.fp32) : nullptr;
   if (c.ring) return c.P == 1 ? ring_kernel_ptr(c.G, c.R, c.kr, c.fp32) : nullptr;

@@ -61,7 +61,7 @@ const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026}
                       {1, 46, 2270, 1, 2, false, 1, false, false, true}};
 const Cand kBand[] = {{16, 7, 1500},    {16, 9, 1600},    {16, 11, 1700},  {16, 13, 1800},
                       {32, 3, 1000},    {32, 5, 1250},    {32, 7, 1490},   {32, 9, 1500},
-                      {32, 13, 1450},   {32, 3, 600, 2},  {32, 5, 600, 2},  {32, 7, 700, 2},
+                      {32, 13, 1450},
                       {8, 16, 1900, 1, 2, true},  {8, 26, 2221, 1, 2, true},
                       {16, 8, 1500, 1, 2, true},  {16, 14, 2105, 1, 2, true},
                       {32, 6, 1300, 1, 2, true},
@@ -188,7 +188,7 @@ KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cos
                      int64_t count) {
   const bool mask = s.hw < s.n - 1;
   if (ctx->force_family >= 0) {
-    // 0: full (2 rows/step), 1: band P=1, 2: band P=2, 3: full (4 rows/step), 4: band ring,
+    // 0: full (2 rows/step), 1: band, 3: full (4 rows/step), 4: band ring,
     // 10 + U: band ring with U units per lane
     const int ff = ctx->force_family;
     if (ff == 5) {  // strip family (long pairs spread over warps), G = 32, 4 rows per step
@@ -277,7 +277,10 @@ void maybe_strip(dtwg_ctx* ctx, PlanClass& pc, int64_t count, int64_t m_uniform)
 // Full classes whose every pair fits one strip (m <= G*R) use the single-strip kernels:
 // no boundary column, fewer registers (c1's G=32 R=16: 126 instead of 168, 4 CTAs/SM).
 void set_single_strip(PlanClass& pc) {
-  if (pc.cfg.family == Family::Full && pc.max_m <= (int64_t)pc.cfg.G * pc.cfg.R) pc.cfg.mp = false;
+  if (pc.cfg.family != Family::Full || pc.max_m > (int64_t)pc.cfg.G * pc.cfg.R) return;
+  KernelCfg one = pc.cfg;
+  one.mp = false;
+  if (dtwgpu::fill_cfg_supported(one)) pc.cfg = one;  // multi-pass-only instantiations keep mp
 }
 
 // Same-length pairs all cost the same, so a class of few lanes per pair (one lane per

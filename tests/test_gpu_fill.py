@@ -174,6 +174,27 @@ def test_full_family_fp32_only_instantiations(eng, G, R, maxlen):
         assert_bitwise(got64, want, f"fp64 fallback hw={hw}")
 
 
+@pytest.mark.parametrize("G,R", [(2, 30), (4, 30), (8, 30)])
+def test_full_family_fp64_multipass_instantiations(eng, G, R):
+    """fp64-only multi-pass Full instantiations (fill_table.h DTWG_FULL_CFGS_F64): bitwise
+    with unlimited, auto-widened and narrow bands over several passes; fp32 requests (and
+    single-strip classes) fall back to the planner."""
+    rng = np.random.default_rng(1730 + G)
+    lengths = rng.integers(1, 4 * G * R, size=12)
+    lengths[:4] = [1, G * R, G * R + 1, 3 * G * R + 7]
+    samples, offsets = _walks(1730 + G, lengths)
+    for hw, aw in ((-1, False), (40, True), (3, True), (G * R + 5, False)):
+        eng.force_kernel(3, G, R)
+        got = eng.build_condensed(samples, offsets, hw, aw, precision=0)
+        assert f"full[G={G},R={R},T=4" in eng.last_plan(), eng.last_plan()
+        want = oracle.build_condensed(samples, offsets, hw, aw)
+        assert_bitwise(got, want, f"full64 G={G} R={R} hw={hw}")
+        eng.force_kernel(3, G, R)
+        got32 = eng.build_condensed(samples, offsets, hw, aw, precision=1)
+        assert f"full[G={G},R={R},fp32" not in eng.last_plan(), eng.last_plan()
+        np.testing.assert_allclose(got32, want, rtol=1e-5, atol=0)
+
+
 @pytest.mark.parametrize("G,R,fam", [(4, 12, 0), (4, 12, 3), (2, 23, 3), (8, 8, 0), (32, 4, 0),
                                      (32, 15, 3), (1, 20, 3), (2, 16, 3), (1, 28, 3)])
 def test_full_family_band_edge_kill_cells(eng, G, R, fam):
@@ -197,8 +218,8 @@ UNIT = [(8, 26, 3), (8, 26, 5), (16, 14, 3), (16, 13, 2), (16, 20, 3), (16, 26, 
         (32, 26, 3)]  # ring with U units per lane
 
 
-@pytest.mark.parametrize("G,R,family", [(g, r, f) for g, r in BAND for f in (1, 2)] +
-                         [(g, r, 4) for g, r in RING] +  # 2: two pairs/group, 4: smem ring
+@pytest.mark.parametrize("G,R,family", [(g, r, 1) for g, r in BAND] +
+                         [(g, r, 4) for g, r in RING] +  # 4: smem ring
                          [(g, r, 10 + u) for g, r, u in UNIT])
 @pytest.mark.parametrize("fp32", [False, True])
 def test_band_family_every_instantiation(eng, G, R, fp32, family):
