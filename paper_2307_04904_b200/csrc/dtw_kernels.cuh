@@ -195,19 +195,20 @@ struct FullRows {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       T up = pv[r];
+      const T yr = yv[r];  // one read per column (one LDS when y lives in shared memory)
 #pragma unroll
       for (int t = 0; t < NR; ++t) {
         T v;
         if constexpr (KILL == 0) {
-          v = Ar::cell(x[t], yv[r], Ar::mn(Ar::mn(d[t], up), l[t]));
+          v = Ar::cell(x[t], yr, Ar::mn(Ar::mn(d[t], up), l[t]));
         } else if constexpr (Ar::kFp32) {
-          v = Ar::cell(x[t], yv[r], Ar::mn(Ar::mn(d[t], up), l[t]));
+          v = Ar::cell(x[t], yr, Ar::mn(Ar::mn(d[t], up), l[t]));
           const bool k = ((KILL & 1) && r - t == klo) || ((KILL & 2) && r - t == khi);
           v = k ? INF : v;
         } else {
           const T m1 = (KILL & 1) ? min_unless(d[t], up, klo, r - t) : Ar::mn(d[t], up);
           const T m = (KILL & 2) ? min_unless(m1, l[t], khi, r - t) : Ar::mn(m1, l[t]);
-          v = Ar::cell(x[t], yv[r], m);
+          v = Ar::cell(x[t], yr, m);
         }
         d[t] = up;  // (t-1, r) is the diagonal of (t, r+1)
         l[t] = v;
@@ -242,9 +243,19 @@ __device__ __forceinline__ int kill_need(int klo, int khi) {
 // strips of width G*R with a per-group boundary column between passes. MP = false: every
 // pair of the launch fits one strip (m <= G*R), so the boundary-column machinery and its
 // registers are compiled out (c3: 198 -> fewer registers per thread).
-template <int G, int R, int TR, bool MASK, class Ar, bool MP = true>
-__global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
+template <bool YSM, class P, class Arr>
+__device__ __forceinline__ auto& pick_y(P& p, Arr& a) {
+  if constexpr (YSM) return p;
+  else return a;
+}
+
+// YSM (G = 1 only): the lane's R y samples live in shared memory (ys, odd stride) instead
+// of R registers, read once per column per step -- fewer registers, so more warps per SM
+// (dtw_full1s_kernel below).
+template <int G, int R, int TR, bool MASK, class Ar, bool MP, bool YSM>
+__device__ __forceinline__ void full_body(const FillArgs& A, volatile typename Ar::T* ys) {
   using T = typename Ar::T;
+  static_assert(!YSM || G == 1, "y in shared memory: one lane per pair only");
   constexpr bool kF32 = sizeof(T) == 4;
   constexpr int GPW = 32 / G;
   constexpr int W = G * R;
@@ -284,12 +295,16 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
       const int my_steps = pvalid ? ((re - rs + TR) / TR) + G - 1 : 0;
       const int nsteps = __reduce_max_sync(kFull, my_steps);
       const int jl = c0 + gl * R + 1;  // 1-based first column of this lane
-      T yv[R], pv[R];
+      T yreg[YSM ? 1 : R], pv[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        yv[r] = (jl + r <= m) ? __ldg(Y + jl + r - 1) : T(0);
+        const T yj = (jl + r <= m) ? __ldg(Y + jl + r - 1) : T(0);
+        if constexpr (YSM) ys[r] = yj;
+        else yreg[r] = yj;
         pv[r] = INF;
       }
+      // the strip's y: registers, or this lane's own shared-memory row (no sync needed)
+      auto& yv = pick_y<YSM>(ys, yreg);
       T diag0 = INF;  // cell (r0-1, jl-1)
       if (gl == 0) {
         if (pass == 0) diag0 = (rs == 1) ? T(0) : INF;
@@ -432,6 +447,21 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
     const int last_c0 = (npass_g - 1) * W;
     if (valid && ((m - 1 - last_c0) / R) == gl) store_result(A, P.slot, result);
   }
+}
+
+template <int G, int R, int TR, bool MASK, class Ar, bool MP = true>
+__global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
+  full_body<G, R, TR, MASK, Ar, MP, false>(A, nullptr);
+}
+
+// One lane per pair with y in shared memory: <= 168 registers, 3 CTAs (12 warps) per SM
+// instead of 2, for 32 extra LDS per 4 x 32-cell step.
+template <int R, int TR, bool MASK, class Ar, bool MP = true>
+__global__ void __launch_bounds__(kThreads, 3) dtw_full1s_kernel(const FillArgs A) {
+  using T = typename Ar::T;
+  constexpr int YS = (sizeof(T) == 8) ? ((R % 2) ? R : R + 1) : ((R % 2) ? R : R + 1);
+  __shared__ T ysm[kThreads * YS];
+  full_body<1, R, TR, MASK, Ar, MP, true>(A, ysm + threadIdx.x * YS);
 }
 
 // ===================================================================================

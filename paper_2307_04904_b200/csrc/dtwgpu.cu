@@ -291,8 +291,9 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
                pc.cfg.ring ? ",ring" : "",
                pc.cfg.U > 1 ? (",U=" + std::to_string(pc.cfg.U)).c_str() : "");
     if (pc.cfg.family != Family::Band)
-      snprintf(krs, sizeof(krs), ",T=%d%s", pc.cfg.TR,
-               pc.cfg.family == Family::Full && !pc.cfg.mp ? ",1strip" : "");
+      snprintf(krs, sizeof(krs), ",T=%d%s%s", pc.cfg.TR,
+               pc.cfg.family == Family::Full && !pc.cfg.mp ? ",1strip" : "",
+               pc.cfg.ysm ? ",ysm" : "");
     char cellsb[32] = "";
     if (pc.cells > 0) snprintf(cellsb, sizeof(cellsb), " cells=%.4g", pc.cells);
     snprintf(buf, sizeof(buf), "%s%s[G=%d,R=%d%s%s%s] pairs=%lld%s blocks=%lld(%d/SM)",

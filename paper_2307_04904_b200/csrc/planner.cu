@@ -22,6 +22,8 @@ struct Cand {
   bool mp_rate = false;   // full family: rate measured on multi-pass shapes (no penalty)
   bool f64_only = false;  // full family: planned for fp64 only
   bool unmasked = false;  // full family: planned for unlimited windows only
+  bool ysm = false;       // full family, G = 1: y in shared memory (dtw_full1s_kernel)
+  bool masked_only = false;  // full family: planned for banded shapes only
 };
 const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026},
                       {4, 12, 1956, 1, 4},   {8, 8, 1804},         {8, 8, 1700, 1, 4},
@@ -58,7 +60,14 @@ const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026}
                       {1, 64, 2888, 1, 4, false, 1, true, true, false, true},
                       // fp64: one lane per pair, y in shared memory (dtw_lane_kernel),
                       // single strip only: c3 2041 -> 2278 GCUPS
-                      {1, 46, 2270, 1, 2, false, 1, false, false, true}};
+                      {1, 46, 2270, 1, 2, false, 1, false, false, true},
+                      // fp64, banded multi-pass: one lane per pair with y in shared memory
+                      // (dtw_full1s_kernel, 3 CTAs/SM). Forced over all of c5: R=24 2066,
+                      // R=20 2026 GCUPS against 1863 for the register-y R=28 strips (rates
+                      // scaled from that ratio and the lane-cells each computes); unlimited
+                      // windows keep the register kernel (c4: 2363 against 2456)
+                      {1, 24, 2470, 1, 4, false, 1, false, true, true, false, true, true},
+                      {1, 20, 2400, 1, 4, false, 1, false, true, true, false, true, true}};
 const Cand kBand[] = {{16, 7, 1500},    {16, 9, 1600},    {16, 11, 1700},  {16, 13, 1800},
                       {32, 3, 1000},    {32, 5, 1250},    {32, 7, 1490},   {32, 9, 1500},
                       {32, 13, 1450},
@@ -153,12 +162,15 @@ KernelCfg choose_cfg_model(const Shape& s, bool fp32, double* cost_out, int64_t 
   double bc = 1e300;
   const bool mask = s.hw < s.n - 1;  // a band that excludes some cell
   for (const Cand& c : kFull) {
-    if ((c.f32_only && !fp32) || (c.f64_only && fp32) || (c.unmasked && mask)) continue;
+    if ((c.f32_only && !fp32) || (c.f64_only && fp32) || (c.unmasked && mask) ||
+        (c.masked_only && !mask))
+      continue;
     if (c.G == 1 && s.m > c.R && !c.mp_rate) continue;  // single strip unless measured multi-pass
     const double cst = full_cost(s, c, mask, fp32) / fill_factor(count, c.G, sms);
     if (cst < bc) {
       bc = cst;
       best = KernelCfg{Family::Full, c.G, c.R, mask, fp32, -1, 1, c.TR};
+      best.ysm = c.ysm;
     }
   }
   if (mask) {
@@ -193,6 +205,14 @@ KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cos
     const int ff = ctx->force_family;
     if (ff == 5) {  // strip family (long pairs spread over warps), G = 32, 4 rows per step
       KernelCfg f{Family::Strip, 32, ctx->force_R, mask, fp32, -1, 1, 4};
+      if (dtwgpu::fill_cfg_supported(f)) {
+        if (cost_out) *cost_out = 1.0;
+        return f;
+      }
+    }
+    if (ff == 6) {  // one lane per pair, y in shared memory, 4 rows per step
+      KernelCfg f{Family::Full, 1, ctx->force_R, mask, fp32, -1, 1, 4};
+      f.ysm = true;
       if (dtwgpu::fill_cfg_supported(f)) {
         if (cost_out) *cost_out = 1.0;
         return f;
@@ -352,7 +372,7 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
     double cst = 0;
     const KernelCfg cfg = choose_cfg(ctx, s, fp32, &cst);
     const auto key = std::make_tuple((int)cfg.family * 2 + (int)cfg.ring + 4 * cfg.U, cfg.G, cfg.R, cfg.mask,
-                                     cfg.kr, cfg.P, cfg.TR);
+                                     cfg.kr, cfg.P, cfg.TR + 100 * (int)cfg.ysm);
     int cls;
     auto ic = cls_of_cfg.find(key);
     if (ic == cls_of_cfg.end()) {

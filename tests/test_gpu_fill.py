@@ -183,7 +183,7 @@ def test_full_family_fp64_multipass_instantiations(eng, G, R):
     lengths = rng.integers(1, 4 * G * R, size=12)
     lengths[:4] = [1, G * R, G * R + 1, 3 * G * R + 7]
     samples, offsets = _walks(1730 + G, lengths)
-    for hw, aw in ((-1, False), (40, True), (3, True), (G * R + 5, False)):
+    for hw, aw in ((-1, False), (40, True), (3, True), (G * R + 5, True)):
         eng.force_kernel(3, G, R)
         got = eng.build_condensed(samples, offsets, hw, aw, precision=0)
         assert f"full[G={G},R={R},T=4" in eng.last_plan(), eng.last_plan()
@@ -192,6 +192,27 @@ def test_full_family_fp64_multipass_instantiations(eng, G, R):
         eng.force_kernel(3, G, R)
         got32 = eng.build_condensed(samples, offsets, hw, aw, precision=1)
         assert f"full[G={G},R={R},fp32" not in eng.last_plan(), eng.last_plan()
+        np.testing.assert_allclose(got32, want, rtol=1e-5, atol=0)
+
+
+@pytest.mark.parametrize("R", [28, 24, 20, 16])
+def test_full_one_lane_shared_y_instantiations(eng, R):
+    """One lane per pair with y in shared memory (dtw_full1s_kernel, fill_table.h
+    DTWG_FULL1S_CFGS; forced as family 6): bitwise over several passes with unlimited,
+    auto-widened and narrow bands, ragged lengths in one warp; fp32 falls back."""
+    rng = np.random.default_rng(1830 + R)
+    lengths = rng.integers(1, 12 * R, size=40)
+    lengths[:4] = [1, R, R + 1, 9 * R + 7]
+    samples, offsets = _walks(1830 + R, lengths)
+    for hw, aw in ((-1, False), (40, True), (3, True), (2 * R + 5, True)):
+        eng.force_kernel(6, 1, R)
+        got = eng.build_condensed(samples, offsets, hw, aw, precision=0)
+        assert f"full[G=1,R={R}" in eng.last_plan() and "ysm" in eng.last_plan(), eng.last_plan()
+        want = oracle.build_condensed(samples, offsets, hw, aw)
+        assert_bitwise(got, want, f"full1s R={R} hw={hw}")
+        eng.force_kernel(6, 1, R)
+        got32 = eng.build_condensed(samples, offsets, hw, aw, precision=1)
+        assert "ysm" not in eng.last_plan(), eng.last_plan()
         np.testing.assert_allclose(got32, want, rtol=1e-5, atol=0)
 
 
