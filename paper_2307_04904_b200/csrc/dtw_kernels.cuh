@@ -454,8 +454,9 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
   full_body<G, R, TR, MASK, Ar, MP, false>(A, nullptr);
 }
 
-// One lane per pair with y in shared memory: <= 168 registers, 3 CTAs (12 warps) per SM
-// instead of 2, for 32 extra LDS per 4 x 32-cell step.
+// One lane per pair with y in shared memory, one LDS per column per 4-row step: <= 168
+// registers, 3 CTAs (12 warps) per SM instead of 2. (8 rows per step at 2 CTAs/SM measured
+// slower: c4 2340, c5 1274 GCUPS.)
 template <int R, int TR, bool MASK, class Ar, bool MP = true>
 __global__ void __launch_bounds__(kThreads, 3) dtw_full1s_kernel(const FillArgs A) {
   using T = typename Ar::T;

@@ -195,8 +195,8 @@ def test_full_family_fp64_multipass_instantiations(eng, G, R):
         np.testing.assert_allclose(got32, want, rtol=1e-5, atol=0)
 
 
-@pytest.mark.parametrize("R", [28, 24, 20, 16])
-def test_full_one_lane_shared_y_instantiations(eng, R):
+@pytest.mark.parametrize("R,fam", [(28, 6), (24, 6), (20, 6), (16, 6)])
+def test_full_one_lane_shared_y_instantiations(eng, R, fam):
     """One lane per pair with y in shared memory (dtw_full1s_kernel, fill_table.h
     DTWG_FULL1S_CFGS; forced as family 6): bitwise over several passes with unlimited,
     auto-widened and narrow bands, ragged lengths in one warp; fp32 falls back."""
@@ -205,12 +205,13 @@ def test_full_one_lane_shared_y_instantiations(eng, R):
     lengths[:4] = [1, R, R + 1, 9 * R + 7]
     samples, offsets = _walks(1830 + R, lengths)
     for hw, aw in ((-1, False), (40, True), (3, True), (2 * R + 5, True)):
-        eng.force_kernel(6, 1, R)
+        eng.force_kernel(fam, 1, R)
         got = eng.build_condensed(samples, offsets, hw, aw, precision=0)
-        assert f"full[G=1,R={R}" in eng.last_plan() and "ysm" in eng.last_plan(), eng.last_plan()
+        plan = eng.last_plan()
+        assert f"full[G=1,R={R}" in plan and "ysm" in plan and f"T={4 if fam == 6 else 8}" in plan, plan
         want = oracle.build_condensed(samples, offsets, hw, aw)
         assert_bitwise(got, want, f"full1s R={R} hw={hw}")
-        eng.force_kernel(6, 1, R)
+        eng.force_kernel(fam, 1, R)
         got32 = eng.build_condensed(samples, offsets, hw, aw, precision=1)
         assert "ysm" not in eng.last_plan(), eng.last_plan()
         np.testing.assert_allclose(got32, want, rtol=1e-5, atol=0)
