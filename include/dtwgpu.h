@@ -109,8 +109,8 @@ uint64_t dtwg_launch_count(const dtwg_ctx* ctx);
 int dtwg_measure_cell_peak(dtwg_ctx* ctx, int precision, double* cells_per_s);
 /* Diagnostics/tests: force kernel family (0 = full with 2 rows per step, 1 = band, 3 = full
  * with 4 rows per step, 4 = band with a shared-memory y ring, 10 + U = ring band with U units
- * per lane, 5 = strip pipeline for long pairs, G = 32, 6 / 7 = one lane per pair with y in
- * shared memory, 4 rows per step) and (G, R) for every pair shape it can legally run;
+ * per lane, 5 = strip pipeline for long pairs, G = 32, 6 = Full strips with y in shared
+ * memory, 4 rows per step) and (G, R) for every pair shape it can legally run;
  * family < 0 restores the cost-model planner. */
 int dtwg_force_kernel(dtwg_ctx* ctx, int family, int G, int R);
 /* Human-readable plan of the last fill (kernel family, group lanes, cells per lane). */

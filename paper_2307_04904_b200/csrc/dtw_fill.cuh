@@ -59,7 +59,7 @@ struct KernelCfg {
   bool ring = false;  // Band family: y window in a shared-memory ring instead of registers
   int U = 1;          // ring variant: units per lane (independent cell chains per lane)
   bool mp = true;     // Full family: some pair needs several strips (boundary column)
-  bool ysm = false;   // Full family, G = 1: y in shared memory (dtw_full1s_kernel)
+  bool ysm = false;   // Full family: y in shared memory (dtw_full1s_kernel)
 };
 
 // Launches cfg over args on stream with `blocks` CTAs of kThreads threads.

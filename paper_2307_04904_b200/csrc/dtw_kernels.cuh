@@ -249,13 +249,12 @@ __device__ __forceinline__ auto& pick_y(P& p, Arr& a) {
   else return a;
 }
 
-// YSM (G = 1 only): the lane's R y samples live in shared memory (ys, odd stride) instead
+// YSM: the lane's R y samples live in shared memory (ys, odd stride) instead
 // of R registers, read once per column per step -- fewer registers, so more warps per SM
 // (dtw_full1s_kernel below).
 template <int G, int R, int TR, bool MASK, class Ar, bool MP, bool YSM>
 __device__ __forceinline__ void full_body(const FillArgs& A, volatile typename Ar::T* ys) {
   using T = typename Ar::T;
-  static_assert(!YSM || G == 1, "y in shared memory: one lane per pair only");
   constexpr bool kF32 = sizeof(T) == 4;
   constexpr int GPW = 32 / G;
   constexpr int W = G * R;
@@ -454,15 +453,18 @@ __global__ void DTWG_FULL_BOUNDS dtw_full_kernel(const FillArgs A) {
   full_body<G, R, TR, MASK, Ar, MP, false>(A, nullptr);
 }
 
-// One lane per pair with y in shared memory, one LDS per column per 4-row step: <= 168
-// registers, 3 CTAs (12 warps) per SM instead of 2. (8 rows per step at 2 CTAs/SM measured
-// slower: c4 2340, c5 1274 GCUPS.)
-template <int R, int TR, bool MASK, class Ar, bool MP = true>
+// Full strips with y in shared memory (every lane its own R samples, odd stride), one LDS
+// per column per 4-row step: <= 168 registers, 3 CTAs (12 warps) per SM instead of 2.
+// Planned with G = 1 (one lane per pair) for banded multi-pass shapes (c5). The register
+// file is split per SM sub-partition, so 3 warps per scheduler cap a thread at 168
+// registers whatever the CTA shape (R = 32 spills). (8 rows per step at 2 CTAs/SM
+// measured slower: c4 2340, c5 1274 GCUPS.)
+template <int G, int R, int TR, bool MASK, class Ar, bool MP = true>
 __global__ void __launch_bounds__(kThreads, 3) dtw_full1s_kernel(const FillArgs A) {
   using T = typename Ar::T;
-  constexpr int YS = (sizeof(T) == 8) ? ((R % 2) ? R : R + 1) : ((R % 2) ? R : R + 1);
+  constexpr int YS = (R % 2) ? R : R + 1;
   __shared__ T ysm[kThreads * YS];
-  full_body<1, R, TR, MASK, Ar, MP, true>(A, ysm + threadIdx.x * YS);
+  full_body<G, R, TR, MASK, Ar, MP, true>(A, ysm + threadIdx.x * YS);
 }
 
 // ===================================================================================

@@ -17,13 +17,13 @@ const void* full64_kernel_ptr(int G, int R, int TR, bool mask, bool mp) {
   return nullptr;
 }
 
-const void* full1s_kernel_ptr(int R, int TR, bool mask, bool fp32, bool mp) {
+const void* full1s_kernel_ptr(int G, int R, int TR, bool mask, bool fp32, bool mp) {
   using namespace kern;
   if (fp32 || !mp) return nullptr;
-#define DTWG_F1S(r, tr)                                                                     \
-  if (R == r && TR == tr)                                                                   \
-    return mask ? (const void*)dtw_full1s_kernel<r, tr, true, F64, true>                    \
-                : (const void*)dtw_full1s_kernel<r, tr, false, F64, true>;
+#define DTWG_F1S(g, r, tr)                                                                  \
+  if (G == g && R == r && TR == tr)                                                         \
+    return mask ? (const void*)dtw_full1s_kernel<g, r, tr, true, F64, true>                 \
+                : (const void*)dtw_full1s_kernel<g, r, tr, false, F64, true>;
   DTWG_FULL1S_CFGS(DTWG_F1S)
 #undef DTWG_F1S
   return nullptr;

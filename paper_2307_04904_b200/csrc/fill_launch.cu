@@ -8,7 +8,7 @@ namespace dtwgpu {
 
 static const void* kernel_ptr(const KernelCfg& c) {
   if (c.family == Family::Full && c.ysm)
-    return c.G == 1 ? full1s_kernel_ptr(c.R, c.TR, c.mask, c.fp32, c.mp) : nullptr;
+    return full1s_kernel_ptr(c.G, c.R, c.TR, c.mask, c.fp32, c.mp);
   if (c.family == Family::Full) {
     const void* f = full_kernel_ptr(c.G, c.R, c.TR, c.mask, c.fp32, c.mp);
     return (f || c.fp32) ? f : full64_kernel_ptr(c.G, c.R, c.TR, c.mask, c.mp);

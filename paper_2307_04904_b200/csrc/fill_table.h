@@ -8,8 +8,8 @@
   X(32, 15, 4) X(32, 16, 4) X(2, 16, 4) X(1, 20, 4) X(1, 24, 4) X(1, 28, 4) X(1, 32, 4)
 // Full family, fp32 only (wide strips: half the per-row overhead per cell; the fp64
 // instantiation would need > 255 registers)
-// One lane per pair with y in shared memory (dtw_full1s_kernel, 3 CTAs/SM): (R, rows per step)
-#define DTWG_FULL1S_CFGS(X) X(28, 4) X(24, 4) X(20, 4) X(16, 4)
+// Full strips with y in shared memory (dtw_full1s_kernel, 3 CTAs/SM): (G, R, rows per step)
+#define DTWG_FULL1S_CFGS(X) X(1, 28, 4) X(1, 24, 4) X(1, 20, 4) X(1, 16, 4)
 // Full family, fp64 only, multi-pass (long series: wider passes, fewer boundary columns)
 #define DTWG_FULL_CFGS_F64(X) X(2, 30, 4) X(4, 30, 4) X(8, 30, 4)
 #define DTWG_FULL_CFGS_F32(X) X(16, 30, 4) X(1, 46, 4) X(16, 32, 4) X(1, 56, 4) X(1, 64, 4)
@@ -31,7 +31,7 @@
 namespace dtwgpu {
 const void* full_kernel_ptr(int G, int R, int TR, bool mask, bool fp32, bool mp);
 const void* full64_kernel_ptr(int G, int R, int TR, bool mask, bool mp);
-const void* full1s_kernel_ptr(int R, int TR, bool mask, bool fp32, bool mp);
+const void* full1s_kernel_ptr(int G, int R, int TR, bool mask, bool fp32, bool mp);
 const void* band16_kernel_ptr(int R, int kr, int P, bool fp32);
 const void* band32_kernel_ptr(int R, int kr, int P, bool fp32);
 const void* ring_kernel_ptr(int G, int R, int kr, bool fp32);

@@ -22,7 +22,7 @@ struct Cand {
   bool mp_rate = false;   // full family: rate measured on multi-pass shapes (no penalty)
   bool f64_only = false;  // full family: planned for fp64 only
   bool unmasked = false;  // full family: planned for unlimited windows only
-  bool ysm = false;       // full family, G = 1: y in shared memory (dtw_full1s_kernel)
+  bool ysm = false;       // full family: y in shared memory (dtw_full1s_kernel)
   bool masked_only = false;  // full family: planned for banded shapes only
 };
 const Cand kFull[] = {{2, 23, 1913},         {2, 23, 2141, 1, 4},  {4, 12, 2026},
@@ -210,8 +210,8 @@ KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cos
         return f;
       }
     }
-    if (ff == 6) {  // one lane per pair, y in shared memory, 4 rows per step
-      KernelCfg f{Family::Full, 1, ctx->force_R, mask, fp32, -1, 1, 4};
+    if (ff == 6) {  // Full strips with y in shared memory, 4 rows per step
+      KernelCfg f{Family::Full, ctx->force_G, ctx->force_R, mask, fp32, -1, 1, 4};
       f.ysm = true;
       if (dtwgpu::fill_cfg_supported(f)) {
         if (cost_out) *cost_out = 1.0;
