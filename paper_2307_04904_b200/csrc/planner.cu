@@ -361,6 +361,22 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
   if (use_tab) cls_tab.assign((size_t)(L1 * L1), -1);
   std::map<Shape, int> cls_of_shape;
   std::map<std::tuple<int, int, int, bool, int, int, int>, int> cls_of_cfg;
+  // Second classification round (below): shapes whose first-round class was too small to
+  // fill the GPU with its lanes per pair are re-costed with that class's pair count.
+  std::vector<int> old_tab;
+  std::map<Shape, int> old_shape;
+  std::vector<int64_t> old_hint;  // per first-round class: pair count if underfilled, else 0
+  auto count_hint = [&](const Shape& s) -> int64_t {
+    if (old_hint.empty()) return 0;
+    int oc = -1;
+    if (use_tab) {
+      oc = old_tab[(size_t)(s.n * L1 + s.m)];
+    } else {
+      auto it = old_shape.find(s);
+      if (it != old_shape.end()) oc = it->second;
+    }
+    return oc >= 0 ? old_hint[oc] : 0;
+  };
   auto class_of = [&](int64_t a, int64_t b, Shape& s) -> int {
     s = shape_of(ctx, a, b, hw, auto_widen);
     int* slotp = use_tab ? &cls_tab[(size_t)(s.n * L1 + s.m)] : nullptr;
@@ -370,7 +386,7 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
       if (it != cls_of_shape.end()) return it->second;
     }
     double cst = 0;
-    const KernelCfg cfg = choose_cfg(ctx, s, fp32, &cst);
+    const KernelCfg cfg = choose_cfg(ctx, s, fp32, &cst, count_hint(s));
     const auto key = std::make_tuple((int)cfg.family * 2 + (int)cfg.ring + 4 * cfg.U, cfg.G, cfg.R, cfg.mask,
                                      cfg.kr, cfg.P, cfg.TR + 100 * (int)cfg.ysm);
     int cls;
@@ -407,7 +423,7 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
   const int64_t j0 = i0 + 1 + (sb - row_off(i0, p));
   // pass 1: classes, bucket counts
   std::vector<std::vector<int64_t>> counts;
-  {
+  auto pass1 = [&]() {
     int64_t i = i0, j = j0;
     Shape s;
     for (int64_t slot = sb; slot < se; ++slot) {
@@ -424,6 +440,32 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
         ++i;
         j = i + 1;
       }
+    }
+  };
+  pass1();
+  // Shapes are first costed without a pair count (fill factor 1), which favours few lanes
+  // per pair. A Full class that cannot keep ~half the GPU's warp slots busy with its
+  // lanes per pair is re-costed with its real pair count (fill_factor), and the pass runs
+  // again with those shapes re-classified (small ragged classes).
+  if (ctx->force_family < 0 && env_or("DTWGPU_UNDERFILL_REPLAN", 1) != 0) {
+    std::vector<int64_t> hint(plan.size(), 0);
+    bool any = false;
+    for (size_t c = 0; c < plan.size(); ++c) {
+      int64_t n = 0;
+      for (int64_t v : counts[c]) n += v;
+      if (plan[c].cfg.family == Family::Full && fill_factor(n, plan[c].cfg.G, ctx->num_sms) < 0.5) {
+        hint[c] = n;
+        any = true;
+      }
+    }
+    if (any) {
+      old_hint = std::move(hint);
+      if (use_tab) old_tab.swap(cls_tab), cls_tab.assign((size_t)(L1 * L1), -1);
+      else old_shape.swap(cls_of_shape);
+      plan.clear();
+      cls_of_cfg.clear();
+      counts.clear();
+      pass1();
     }
   }
   // descending bucket order -> start offsets

@@ -476,14 +476,13 @@ def test_full_size_matrix_bitwise_vs_reference(eng, cfg, q):
 
 @pytest.mark.parametrize("fp32", [False, True])
 def test_one_lane_per_pair_kernels(eng, fp32):
-    """One lane per pair (fp64: dtw_lane_kernel, y in shared memory, single strip and
-    multi-pass; fp32: the Full family with G = 1): ragged lengths, unlimited, banded (kill
-    cells) and auto-widened windows, pairs shorter than a row step; bit-exact in fp64."""
+    """One lane per pair, single strip (fp64: dtw_lane_kernel, y in shared memory; fp32:
+    the Full family with G = 1): ragged lengths, unlimited, banded (kill cells) and
+    auto-widened windows, pairs shorter than a row step; bit-exact in fp64. (Multi-pass
+    one-lane fp64 strips are the G = 1 Full instantiations, tested above.)"""
     rng = np.random.default_rng(46)
     lengths = rng.integers(1, 47, size=40)
     lengths[:6] = [1, 2, 3, 45, 46, 46]
-    if not fp32:  # fp64 lanes also run multi-pass: pairs up to 4 strips wide
-        lengths[6:12] = [47, 92, 93, 150, 184, 185]
     samples, offsets = _walks(4646, lengths)
     for hw, aw in ((-1, False), (0, True), (1, True), (5, True), (20, True), (45, True)):
         eng.force_kernel(3 if fp32 else 0, 1, 46)
