@@ -22,6 +22,9 @@ struct FillArgs {
   double* out;
   double* scratch;         // boundary columns for multi-pass fills (one per group)
   int64_t scratch_stride;  // doubles per group
+  // Readable sample indices relative to samples/samples32 (the zero guards included);
+  // checked by DTWG_CHECK_BOUNDS builds (tools/bounds_check.sh).
+  int64_t guard_lo, guard_hi;
   // Band family: the same series, each surrounded by kBandPad +inf samples, so band
   // columns outside [1, m] (and rows outside [1, n]) load +inf without a range check.
   const double* bsamples;

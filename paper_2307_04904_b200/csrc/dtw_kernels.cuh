@@ -42,6 +42,7 @@
 #include <math_constants.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "dtw_fill.cuh"
 
@@ -73,6 +74,33 @@ __device__ __forceinline__ void decode_slot(int64_t s, int64_t p, int64_t& i, in
   while (r + 1 <= p - 2 && row_off(r + 1, p) <= s) ++r;
   i = r;
   j = r + 1 + (s - row_off(r, p));
+}
+
+// ---- bounds checks (DTWG_CHECK_BOUNDS builds only; tools/bounds_check.sh) -----------
+// Every sample load of the Full/lane/strip kernels stays inside the guarded series buffer
+// (lanes of a warp run to the warp's longest pair and prefetch past their own ends) and
+// every boundary-column row inside the group's scratch column.
+#ifdef DTWG_CHECK_BOUNDS
+#define DTWG_CHK(cond, what, v)                                                              \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("DTWG_CHECK_BOUNDS %s out of range: %lld (block %d thread %d)\n", what,      \
+             (long long)(v), (int)blockIdx.x, (int)threadIdx.x);                           \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define DTWG_CHK(cond, what, v) \
+  do {                          \
+  } while (0)
+#endif
+template <class T>
+__device__ __forceinline__ void chk_sample(const FillArgs& A, const T* S, const T* P, int64_t i) {
+  const int64_t at = (int64_t)(P - S) + i;
+  DTWG_CHK(at >= A.guard_lo && at < A.guard_hi, "sample", at);
+}
+__device__ __forceinline__ void chk_row(const FillArgs& A, int64_t row) {
+  DTWG_CHK(row >= 0 && row < A.scratch_stride, "boundary row", row);
 }
 
 // ---- arithmetic policies ----------------------------------------------------------
@@ -297,6 +325,7 @@ __device__ __forceinline__ void full_body(const FillArgs& A, volatile typename A
       T yreg[YSM ? 1 : R], pv[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
+        if (jl + r <= m) chk_sample(A, S, Y, jl + r - 1);
         const T yj = (jl + r <= m) ? __ldg(Y + jl + r - 1) : T(0);
         if constexpr (YSM) ys[r] = yj;
         else yreg[r] = yj;
@@ -307,7 +336,10 @@ __device__ __forceinline__ void full_body(const FillArgs& A, volatile typename A
       T diag0 = INF;  // cell (r0-1, jl-1)
       if (gl == 0) {
         if (pass == 0) diag0 = (rs == 1) ? T(0) : INF;
-        else if (rs - 1 >= 1 && rs - 1 <= written_hi) diag0 = (T)bnd[(rs - 1) * GPW];
+        else if (rs - 1 >= 1 && rs - 1 <= written_hi) {
+          chk_row(A, rs - 1);
+          diag0 = (T)bnd[(rs - 1) * GPW];
+        }
       }
       double off = 0.0;  // fp32: this lane's offset
       T send[TR];
@@ -326,10 +358,14 @@ __device__ __forceinline__ void full_body(const FillArgs& A, volatile typename A
       double bq[TR];
 #pragma unroll
       for (int t = 0; t < TR; ++t) {
+        chk_sample(A, S, X, r0 + t - 1);
         xq[t] = __ldg(X + (r0 + t - 1));
         bq[t] = (double)Ar::inf();
         if constexpr (MP)
-          if (use_bnd) bq[t] = bnd[(r0 + t) * GPW];
+          if (use_bnd) {
+            chk_row(A, r0 + t);
+            bq[t] = bnd[(r0 + t) * GPW];
+          }
       }
 
       for (int s = 0; s < nsteps; ++s, r0 += TR) {
@@ -339,11 +375,15 @@ __device__ __forceinline__ void full_body(const FillArgs& A, volatile typename A
         for (int t = 0; t < TR; ++t) {
           x[t] = xq[t];
           b[t] = MP ? bq[t] : (double)Ar::inf();  // single strip: column 0 is +inf
+          chk_sample(A, S, X, r0 + TR + t - 1);
           xq[t] = __ldg(X + (r0 + TR + t - 1));
           // Rows past the previous pass's last row hold +inf (written at its end), so
           // lane 0 loads its boundary rows unconditionally: a predicated load, no branch.
           if constexpr (MP)
-            if (use_bnd) bq[t] = bnd[(r0 + TR + t) * GPW];
+            if (use_bnd) {
+              chk_row(A, r0 + TR + t);
+              bq[t] = bnd[(r0 + TR + t) * GPW];
+            }
           // G = 1: no left neighbour (lane 0 of its own group takes the boundary below)
           if constexpr (G > 1) L[t] = __shfl_up_sync(kFull, send[t], 1, G);
           else L[t] = INF;
@@ -421,6 +461,7 @@ __device__ __forceinline__ void full_body(const FillArgs& A, volatile typename A
           for (int t = 0; t < TR; ++t) {
             send[t] = out[t];
             if (wb && t < nr) {
+              chk_row(A, r0 + t);
               if constexpr (kF32) bnd[(r0 + t) * GPW] = (double)out[t] + off;  // +inf + off = +inf
               else bnd[(r0 + t) * GPW] = out[t];
             }
@@ -438,7 +479,10 @@ __device__ __forceinline__ void full_body(const FillArgs& A, volatile typename A
         // The next pass ends at most W rows lower; its rows past this pass's last one
         // lie outside the band at this pass's last column (+inf).
         if (wb)
-          for (int r = re + 1; r <= min(n, re + W); ++r) bnd[r * GPW] = (double)INF;
+          for (int r = re + 1; r <= min(n, re + W); ++r) {
+            chk_row(A, r);
+            bnd[r * GPW] = (double)INF;
+          }
       }
       written_hi = re;
       __syncwarp();
@@ -497,7 +541,10 @@ __global__ void __launch_bounds__(kThreads) dtw_lane_kernel(const FillArgs A) {
     const T* Y = S + P.yoff;
     const int n = valid ? P.n : 0, m = P.m, hw = P.hw;
 #pragma unroll
-    for (int r = 0; r < R; ++r) ys[r] = (r < m) ? __ldg(Y + r) : T(0);  // this lane's own
+    for (int r = 0; r < R; ++r) {
+      if (r < m) chk_sample(A, S, Y, r);
+      ys[r] = (r < m) ? __ldg(Y + r) : T(0);  // this lane's own
+    }
     T pv[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) pv[r] = INF;
@@ -509,12 +556,16 @@ __global__ void __launch_bounds__(kThreads) dtw_lane_kernel(const FillArgs A) {
     double result = 0.0;
     T xq[TR];
 #pragma unroll
-    for (int t = 0; t < TR; ++t) xq[t] = __ldg(X + t);
+    for (int t = 0; t < TR; ++t) {
+      chk_sample(A, S, X, t);
+      xq[t] = __ldg(X + t);
+    }
     for (int r0 = 1; r0 <= rows; r0 += TR) {
       T x[TR];
 #pragma unroll
       for (int t = 0; t < TR; ++t) {
         x[t] = xq[t];
+        chk_sample(A, S, X, r0 + TR + t - 1);
         xq[t] = __ldg(X + (r0 + TR + t - 1));  // rows past n read the zero guard (unused)
       }
       const int klo = r0 - hw - 2, khi = r0 + hw;  // kill columns of row r0, 0-based

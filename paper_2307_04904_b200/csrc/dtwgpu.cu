@@ -123,7 +123,7 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
     if (rc) return rc;
   }
   const dtwg_ctx::PlanKey key{hw, sb, se, auto_widen, fp32, ctx->force_family, ctx->force_G,
-                              ctx->force_R};
+                              ctx->force_R, env_or("DTWGPU_UNDERFILL_REPLAN", 1)};
   if (!(ctx->plan_valid && ctx->plan_key == key)) {
     ctx->plan_cache = make_plan(ctx, hw, auto_widen, fp32, sb, se);
     ctx->plan_key = key;
@@ -251,6 +251,8 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
     FillArgs a{};
     a.samples = ctx->d_samples.ptr + kGuard;
     a.samples32 = fp32 ? ctx->d_samples32.ptr + kGuard : nullptr;
+    a.guard_lo = -kGuard;
+    a.guard_hi = ctx->h_offsets[ctx->p] + ctx->tail_guard;
     a.bsamples = ctx->have_band64 ? ctx->d_bsamples.ptr : nullptr;
     a.bsamples32 = ctx->have_band32 ? ctx->d_bsamples32.ptr : nullptr;
     a.boffsets = (ctx->have_band64 || ctx->have_band32) ? ctx->d_boffsets.ptr : nullptr;

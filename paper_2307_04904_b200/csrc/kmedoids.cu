@@ -572,19 +572,25 @@ __global__ void __launch_bounds__(1024) permute_square_smem_kernel(const double*
                                                                    int64_t p,
                                                                    const int32_t* __restrict__ perm,
                                                                    T* __restrict__ psq) {
-  extern __shared__ double row[];
+  // the row is staged already converted to T: an fp32 copy stages half the bytes, so two
+  // blocks (two rows in flight) fit per SM
+  extern __shared__ __align__(16) unsigned char row_raw[];
+  T* row = reinterpret_cast<T*>(row_raw);
   for (int64_t u = blockIdx.x; u < p; u += gridDim.x) {
     const double* src = sq + (int64_t)__ldg(perm + u) * p;
     if ((p & 1) == 0) {
       const double2* s2 = reinterpret_cast<const double2*>(src);
-      double2* r2 = reinterpret_cast<double2*>(row);
-      for (int64_t v = threadIdx.x; v < p / 2; v += blockDim.x) r2[v] = __ldcs(s2 + v);
+      for (int64_t v = threadIdx.x; v < p / 2; v += blockDim.x) {
+        const double2 d = __ldcs(s2 + v);
+        row[2 * v] = (T)d.x;
+        row[2 * v + 1] = (T)d.y;
+      }
     } else {
-      for (int64_t v = threadIdx.x; v < p; v += blockDim.x) row[v] = __ldcs(src + v);
+      for (int64_t v = threadIdx.x; v < p; v += blockDim.x) row[v] = (T)__ldcs(src + v);
     }
     __syncthreads();
     T* dst = psq + u * p;
-    for (int64_t v = threadIdx.x; v < p; v += blockDim.x) __stcs(dst + v, (T)row[__ldg(perm + v)]);
+    for (int64_t v = threadIdx.x; v < p; v += blockDim.x) __stcs(dst + v, row[__ldg(perm + v)]);
     __syncthreads();
   }
 }
@@ -922,8 +928,10 @@ cudaError_t launch_cluster_layout(const double* sq, int64_t p, int n_anchor, con
   if (e != cudaSuccess) return e;
   inverse_perm_kernel<<<grid_for(p, 256), 256, 0, s>>>(perm, p, pinv);
   if (p <= kPermSmemRow) {
-    const int smem = (int)(p * sizeof(double));
-    const unsigned g = (unsigned)std::min<int64_t>(p, num_sms);
+    const int smem = (int)(p * (psq32 ? sizeof(float) : sizeof(double)));
+    // fp32 rows: 2 blocks per SM (<= 104 KB of staging each)
+    const int per_sm = (psq32 && 2 * smem <= (int)(220 << 10)) ? 2 : 1;
+    const unsigned g = (unsigned)std::min<int64_t>(p, (int64_t)num_sms * per_sm);
     if (psq32) {
       e = cudaFuncSetAttribute(permute_square_smem_kernel<float>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

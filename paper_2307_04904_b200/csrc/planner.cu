@@ -224,7 +224,11 @@ KernelCfg choose_cfg(const dtwg_ctx* ctx, const Shape& s, bool fp32, double* cos
                 (band && (!fp32 || ff > 10) && ctx->force_R > 0) ? (int)((2 * s.hw + 1) % ctx->force_R)
                                                                   : -1,
                 ff == 2 ? 2 : 1, ff == 3 ? 4 : 2, ff == 4 || ff > 10, ff > 10 ? ff - 10 : 1};
-    const bool ok = dtwgpu::fill_cfg_supported(f) &&
+    KernelCfg one = f;  // single-strip-only instantiations (dtw_lane_kernel) for m <= G*R
+    one.mp = false;
+    const bool ok = (dtwgpu::fill_cfg_supported(f) ||
+                     (f.family == Family::Full && s.m <= (int64_t)f.G * f.R &&
+                      dtwgpu::fill_cfg_supported(one))) &&
                     (f.family == Family::Full ||
                      (mask && f.R >= 2 && (int64_t)f.G * f.R >= 2 * s.hw + 1));
     if (ok) {

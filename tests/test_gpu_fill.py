@@ -495,10 +495,14 @@ def test_one_lane_per_pair_kernels(eng, fp32):
             assert_bitwise(got, want, f"lane kernel hw={hw}")
 
 
+@pytest.mark.parametrize("replan", ["0", "1"])
 @pytest.mark.parametrize("prec", [0, 1])
-def test_planner_mixed_classes_short_and_long(eng, prec):
+def test_planner_mixed_classes_short_and_long(eng, prec, replan, monkeypatch):
     """Default planner over a ragged set whose short pairs (m <= 46) take the one-lane
-    kernels and the rest the wavefront/band families, several classes in one fill."""
+    kernels and the rest the wavefront/band families, several classes in one fill. With
+    the underfill re-plan (default) such tiny classes (435 one-lane pairs: 14 warps) are
+    re-costed with their pair count and move to wider lane groups."""
+    monkeypatch.setenv("DTWGPU_UNDERFILL_REPLAN", replan)
     rng = np.random.default_rng(4647)
     lengths = np.concatenate([rng.integers(2, 47, size=30), rng.integers(47, 400, size=20)])
     samples, offsets = _walks(4647, lengths)
@@ -509,8 +513,10 @@ def test_planner_mixed_classes_short_and_long(eng, prec):
             np.testing.assert_allclose(got, want, rtol=1e-5, atol=0)
         else:
             assert_bitwise(got, want, f"mixed hw={hw} plan={eng.last_plan()[:300]}")
-        if hw < 0:
+        if hw < 0 and replan == "0":
             assert "G=1,R=46" in eng.last_plan(), eng.last_plan()
+        if hw < 0 and replan == "1":
+            assert "G=1,R=46" not in eng.last_plan(), eng.last_plan()
 
 
 @pytest.mark.parametrize("fam,G,R,prec", [(0, 1, 46, 0), (3, 1, 46, 1), (3, 16, 30, 1),

@@ -3,7 +3,9 @@ masked multi-pass Full strips (lane 0's unconditional boundary-column prefetch r
 TR*(G+1)+4 rows past the pair's last row, inside the kScratchPad rows of its group's
 column), single-strip Full, the band/ring/unit kernels, the strip pipeline and the
 k-medoids sweeps. Meant for `compute-sanitizer --tool memcheck python tools/sanitize_run.py`
--- closed on this GPU pool (round 1), so it runs as a plain smoke of every family."""
+-- plus the ADVICE r1 case: one lane per pair with one long series among many short ones
+(every lane of a warp runs to the warp's longest pair; its prefetches past its own pair's
+last row must stay inside the tail guard and its own scratch column)."""
 import os
 import sys
 
@@ -42,6 +44,17 @@ def main():
         for hw, aw in ((-1, False), (20, True), (2, True)):
             eng.force_kernel(fam, G, R)
             check(eng, samples, offsets, hw, aw, f"forced fam={fam} G={G} R={R} hw={hw}")
+    # one lane per pair (G = 1, register and shared-memory y), one long series among short
+    # ones: lanes run to the warp's longest pair, prefetching far past their own ends
+    lens = np.concatenate([[6000], rng.integers(2, 120, size=90)])
+    rows = [np.cumsum(rng.standard_normal(int(L))) for L in lens]
+    samples = np.concatenate(rows)
+    offsets = np.zeros(len(rows) + 1, dtype=np.int64)
+    np.cumsum(lens, out=offsets[1:])
+    for fam, G, R in ((3, 1, 32), (3, 1, 28), (6, 1, 24), (6, 1, 20), (0, 1, 46)):
+        for hw, aw in ((-1, False), (50, True)):
+            eng.force_kernel(fam, G, R)
+            check(eng, samples, offsets, hw, aw, f"long+short fam={fam} G={G} R={R} hw={hw}")
     eng.force_kernel(-1, 0, 0)
     # k-medoids sweeps over the resident matrix
     ds = gen.config1(n=24)
