@@ -581,9 +581,12 @@ static int km_run(dtwg_ctx* ctx, int64_t k, int64_t restarts, int64_t max_iterat
   // (same device, own streams), observer calls replayed and the best restart reduced in
   // restart order with strict < -- the sequential loop's result, bit for bit.
   const int64_t nr = restart_end - restart_begin;
-  // (small matrices: a restart is a few tens of microseconds, less than a thread hand-off)
+  // (small matrices: a restart is a few tens of microseconds, less than a thread hand-off).
+  // Each worker's host thread spin-waits on its stream and runs the ordered host sums: on
+  // the 16-thread GPU host, 8-10 workers made whole c3 runs swing 11 -> 22 ms (and up to
+  // 260 ms), 4 workers held 11.1-11.7 ms (tools/km_bench.py --workers, profiles/round2).
   const int64_t hw = (int64_t)std::max(1u, std::thread::hardware_concurrency());
-  const int64_t cap = p >= 2048 ? std::min<int64_t>(std::max<int64_t>(hw - 2, 1), 10) : 1;
+  const int64_t cap = p >= 2048 ? std::min<int64_t>(std::max<int64_t>(hw / 4, 1), 4) : 1;
   const int nw = (int)std::min<int64_t>(nr, std::max<int64_t>(1, env_or("DTWGPU_KM_WORKERS", cap)));
   if (nw <= 1)
     return km_loop(ctx, p, k, max_iterations, seed, restart_begin, restart_end, observer, user,

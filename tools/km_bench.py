@@ -27,6 +27,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", type=int, nargs="+", default=[3, 5])
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--workers", type=int, nargs="*", default=[],
+                    help="extra modes: DTWGPU_KM_WORKERS=w for each w")
+    ap.add_argument("--only-workers", action="store_true",
+                    help="run only the --workers modes")
     a = ap.parse_args()
     eng = api.engine(0)
     dev = torch.device("cuda", 0)
@@ -38,9 +42,12 @@ def main():
         eng.fill_slots(ds.half_width, ds.auto_widen, 0, 0, total, buf.data_ptr())
         eng.synchronize()
         ref = None
-        for mode, env in (("default", {}), ("workers1", {"DTWGPU_KM_WORKERS": "1"}),
-                          ("workers1_nolayout", {"DTWGPU_KM_WORKERS": "1", "DTWGPU_KM_LAYOUT": "0"}),
-                          ("default_nolayout", {"DTWGPU_KM_LAYOUT": "0"})):
+        modes = [] if a.only_workers else [
+            ("default", {}), ("workers1", {"DTWGPU_KM_WORKERS": "1"}),
+            ("workers1_nolayout", {"DTWGPU_KM_WORKERS": "1", "DTWGPU_KM_LAYOUT": "0"}),
+            ("default_nolayout", {"DTWGPU_KM_LAYOUT": "0"})]
+        modes += [(f"workers{w}", {"DTWGPU_KM_WORKERS": str(w)}) for w in a.workers]
+        for mode, env in modes:
             for k_, v_ in env.items():
                 os.environ[k_] = v_
             for rep in range(a.reps):
