@@ -7,6 +7,8 @@
 // bit-identical result. V selects where each of the cell's two compares runs:
 //   V0: both DSETP (the fill kernels' body)     V1: min(diag, up) integer, min(., left) DSETP
 //   V2: min(diag, up) DSETP, min(., left) int   V3: both integer
+//   V4: min(diag, up) as DSETP + 2 predicated IMADs (FMA pipe), min(., left) DSETP + 2 FSEL
+//   V5: both as DSETP + predicated IMADs
 // Throughput: CH independent chains per thread, W warps per SM; latency: one dependent
 // chain. Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mix mix_microbench.cu
 #include <cuda_runtime.h>
@@ -20,16 +22,42 @@ __device__ __forceinline__ double imin(double a, double b) {  // b < a ? b : a, 
 }
 __device__ __forceinline__ double fmin_(double a, double b) { return b < a ? b : a; }
 
+// b < a ? b : a as DSETP + two predicated IMADs by a run-time 1 (FMA pipe instead of the
+// ALU's two FSEL; ptxas cannot fold a multiply by an unknown value into a select)
+__device__ __forceinline__ double pmin(double a, double b, unsigned one) {
+  unsigned alo, ahi;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(alo), "=r"(ahi) : "d"(a));
+  unsigned blo, bhi;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(blo), "=r"(bhi) : "d"(b));
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.lt.f64 p, %4, %5;\n\t"
+      "@p mul.lo.u32 %0, %2, %6;\n\t"
+      "@p mul.lo.u32 %1, %3, %6;\n\t}"
+      : "+r"(alo), "+r"(ahi)
+      : "r"(blo), "r"(bhi), "d"(b), "d"(a), "r"(one));
+  double r;
+  asm("mov.b64 %0, {%1, %2};" : "=d"(r) : "r"(alo), "r"(ahi));
+  return r;
+}
+
 template <int V>
-__device__ __forceinline__ double cell(double x, double y, double diag, double up, double left) {
+__device__ __forceinline__ double cell(double x, double y, double diag, double up, double left,
+                                       unsigned one = 1) {
   const double d = __dsub_rn(x, y);
-  const double m1 = (V == 1 || V == 3) ? imin(diag, up) : fmin_(diag, up);
-  const double m2 = (V == 2 || V == 3) ? imin(m1, left) : fmin_(m1, left);
+  double m1, m2;
+  if constexpr (V >= 4) {
+    m1 = pmin(diag, up, one);
+    m2 = V == 5 ? pmin(m1, left, one) : fmin_(m1, left);
+  } else {
+    m1 = (V == 1 || V == 3) ? imin(diag, up) : fmin_(diag, up);
+    m2 = (V == 2 || V == 3) ? imin(m1, left) : fmin_(m1, left);
+  }
   return __dadd_rn(__dmul_rn(d, d), m2);
 }
 
 template <int V, int CH>
 __global__ void tput(const double* in, double* out, int iters) {
+  const unsigned one = iters > 0 ? 1u : 0u;  // a run-time 1
   double x = in[threadIdx.x & 7], y[CH], a[CH], b[CH];
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
@@ -40,7 +68,7 @@ __global__ void tput(const double* in, double* out, int iters) {
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
-      const double v = cell<V>(x, y[c], a[c], b[c], y[c]);
+      const double v = cell<V>(x, y[c], a[c], b[c], y[c], one);
       a[c] = b[c];
       b[c] = v;
       y[c] = v;
@@ -114,14 +142,16 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
   run_tput<0, 8>(sms, clk_khz, in, out);
-  run_tput<1, 8>(sms, clk_khz, in, out);
-  run_tput<2, 8>(sms, clk_khz, in, out);
-  run_tput<3, 8>(sms, clk_khz, in, out);
   run_tput<0, 4>(sms, clk_khz, in, out);
-  run_tput<1, 4>(sms, clk_khz, in, out);
+  run_tput<4, 4>(sms, clk_khz, in, out);
+  run_tput<5, 4>(sms, clk_khz, in, out);
+  run_tput<4, 8>(sms, clk_khz, in, out);
+  run_tput<5, 8>(sms, clk_khz, in, out);
   run_lat<0>(in, out, clk);
   run_lat<1>(in, out, clk);
   run_lat<2>(in, out, clk);
   run_lat<3>(in, out, clk);
+  run_lat<4>(in, out, clk);
+  run_lat<5>(in, out, clk);
   return 0;
 }
