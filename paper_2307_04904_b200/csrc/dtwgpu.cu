@@ -477,6 +477,8 @@ void dtwg_destroy(dtwg_ctx* ctx) {
   if (ctx->km2) cudaEventDestroy(ctx->km2);
   if (ctx->layout_ready) cudaEventDestroy(ctx->layout_ready);
   if (ctx->layout_t0) cudaEventDestroy(ctx->layout_t0);
+  if (ctx->square_t0) cudaEventDestroy(ctx->square_t0);
+  if (ctx->square_ready) cudaEventDestroy(ctx->square_ready);
   ctx->d_layout_asg.release();
   ctx->d_layout_dist.release();
   ctx->d_layout_lab.release();

@@ -223,6 +223,10 @@ struct dtwg_ctx {
   cudaStream_t layout_stream = nullptr;  // the copy is built here, overlapping the seeding
   cudaEvent_t layout_ready = nullptr;    // sweeps reading it wait on this
   cudaEvent_t layout_t0 = nullptr;
+  // the square expansion runs on `stream` without a host wait: the seeding reads the
+  // condensed matrix meanwhile, sweeps and the layout wait on square_ready
+  cudaEvent_t square_t0 = nullptr, square_ready = nullptr;
+  bool square_timed = false;  // square_t0/square_ready bracket an expansion not yet counted
   DevBuf<int64_t> d_layout_asg;
   DevBuf<double> d_layout_dist;
   DevBuf<int32_t> d_layout_lab, d_layout_keys;

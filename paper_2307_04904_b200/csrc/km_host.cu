@@ -38,7 +38,11 @@ int ensure_square(dtwg_ctx* ctx) {
     return DTWG_OK;
   }
   CU(ctx->d_square.reserve((size_t)(p * p)), "cudaMalloc square");
-  const auto t0 = std::chrono::steady_clock::now();
+  if (!ctx->square_ready) {
+    CU(cudaEventCreate(&ctx->square_t0), "event");
+    CU(cudaEventCreate(&ctx->square_ready), "event");
+  }
+  CU(cudaEventRecord(ctx->square_t0, ctx->stream), "event");
   if (p >= 2) {
     CU(dtwgpu::launch_expand_square(ctx->d_cond.ptr, p, ctx->d_square.ptr, ctx->stream),
        "expand");
@@ -46,9 +50,11 @@ int ensure_square(dtwg_ctx* ctx) {
   } else {
     CU(cudaMemsetAsync(ctx->d_square.ptr, 0, sizeof(double), ctx->stream), "memset");
   }
+  // no host wait: the seeding reads the condensed matrix while the square is written;
+  // the layout build and the sweeps wait on square_ready (km_wait_ready)
+  CU(cudaEventRecord(ctx->square_ready, ctx->stream), "event");
+  ctx->square_timed = true;
   ctx->square_valid = true;
-  CU(cudaStreamSynchronize(ctx->stream), "sync");
-  ctx->km_prep_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return DTWG_OK;
 }
 
@@ -112,7 +118,7 @@ int ensure_layout(dtwg_ctx* ctx, int64_t k) {
   int rc = ensure_iota(ctx, p);
   if (rc) return rc;
   // Built on its own stream (own scratch: anchors' assignment in d_layout_*) while the
-  // restarts seed from the plain square; sweeps wait on layout_ready (km_state).
+  // restarts seed from the condensed matrix; sweeps wait on layout_ready (km_wait_ready).
   if (!ctx->layout_stream) {
     CU(cudaStreamCreateWithFlags(&ctx->layout_stream, cudaStreamNonBlocking), "stream");
     CU(cudaEventCreate(&ctx->layout_ready), "event");
@@ -123,11 +129,13 @@ int ensure_layout(dtwg_ctx* ctx, int64_t k) {
   CU(ctx->d_layout_lab.reserve(p), "malloc");
   CU(ctx->d_layout_keys.reserve(p), "malloc");
   CU(ctx->d_layout_cub.reserve(ctx->cub_bytes), "malloc");
-  CU(cudaStreamSynchronize(ctx->stream), "sync");  // square and iota ready
   cudaStream_t ls = ctx->layout_stream;
   CU(cudaMemcpyAsync(ctx->d_anchors.ptr, anchors.data(), na * 8, cudaMemcpyHostToDevice, ls),
      "H2D anchors");
   CU(cudaStreamSynchronize(ls), "sync");  // `anchors` is pageable and about to go away
+  // the square (and iota) are enqueued on ctx->stream: wait for them on the device
+  CU(cudaEventRecord(ctx->km3, ctx->stream), "event");
+  CU(cudaStreamWaitEvent(ls, ctx->km3, 0), "wait square");
   CU(cudaEventRecord(ctx->layout_t0, ls), "event");
   CU(dtwgpu::launch_cluster_layout(ctx->d_square.ptr, p, na, ctx->d_anchors.ptr,
                                    ctx->d_layout_asg.ptr, ctx->d_layout_dist.ptr,
@@ -153,6 +161,9 @@ struct KmState {
   int64_t p, k;
   const double* sq;      // sweep view (square or condensed)
   bool cond;             // sweep view is the condensed matrix
+  const double* cmat;    // the condensed matrix (seeding reads it while the square is built)
+  const dtwg_ctx* src;   // the context owning the matrix (square_ready / layout_ready)
+  bool ready = false;    // this stream already waits for the square and the layout
   const void* psq;       // cluster-ordered copy (nullptr: none)
   bool psq32;            // ... holding fp32 values
   const int32_t* perm;   // its order
@@ -166,8 +177,17 @@ int km_update_launches(const KmState& S) {
   return S.psq ? 10 : 6;
 }
 
+// Before the first sweep on a stream: the square and the cluster-ordered copy are ready.
+void km_wait_ready(KmState& S) {
+  if (S.ready) return;
+  if (S.src->square_ready) cudaStreamWaitEvent(S.ctx->stream, S.src->square_ready, 0);
+  if (S.psq) cudaStreamWaitEvent(S.ctx->stream, S.src->layout_ready, 0);
+  S.ready = true;
+}
+
 int km_enqueue_assign(KmState& S, const std::vector<int64_t>& medoids) {
   dtwg_ctx* ctx = S.ctx;
+  km_wait_ready(S);
   std::copy(medoids.begin(), medoids.end(), ctx->h_km_med);
   CU(cudaMemcpyAsync(ctx->d_medoids.ptr, ctx->h_km_med, medoids.size() * 8,
                      cudaMemcpyHostToDevice, ctx->stream),
@@ -298,7 +318,8 @@ int km_seeds(KmState& S, int64_t k, SplitMix64& rng, std::vector<int64_t>& medoi
     medoids.push_back(current);
     chosen[current] = 1;
     if ((int64_t)medoids.size() == k) break;
-    CU(dtwgpu::launch_seed_step(S.sq, S.cond, p, current, ctx->d_chosen.ptr, ctx->d_nearest.ptr,
+    // the condensed matrix: ready now, while the square expansion may still be running
+    CU(dtwgpu::launch_seed_step(S.cmat, true, p, current, ctx->d_chosen.ptr, ctx->d_nearest.ptr,
                                 ctx->stream),
        "nearest");
     ctx->launches++;
@@ -462,6 +483,14 @@ int dtwg_km_stats(dtwg_ctx* ctx, double* out, int reset) {
   out[2] = ctx->km_assign_bytes;
   out[3] = ctx->km_update_ms;
   out[4] = ctx->km_update_bytes;
+  if (ctx->square_timed) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(ctx->square_ready) == cudaSuccess &&
+        cudaEventElapsedTime(&ms, ctx->square_t0, ctx->square_ready) == cudaSuccess)
+      ctx->km_prep_ms += ms;
+    cudaGetLastError();
+    ctx->square_timed = false;
+  }
   out[5] = ctx->km_prep_ms;
   out[6] = ctx->layout_valid ? (ctx->layout32 ? 2.0 : 1.0) : 0.0;
   out[7] = 0.0;
@@ -586,7 +615,10 @@ static int km_run(dtwg_ctx* ctx, int64_t k, int64_t restarts, int64_t max_iterat
   // the 16-thread GPU host, 8-10 workers made whole c3 runs swing 11 -> 22 ms (and up to
   // 260 ms), 4 workers held 11.1-11.7 ms (tools/km_bench.py --workers, profiles/round2).
   const int64_t hw = (int64_t)std::max(1u, std::thread::hardware_concurrency());
-  const int64_t cap = p >= 2048 ? std::min<int64_t>(std::max<int64_t>(hw / 4, 1), 4) : 1;
+  // Small matrices (c5, p = 5000: latency-bound restarts) keep up to 10 workers.
+  const int64_t cap = p < 2048 ? 1
+                      : p >= 16384 ? std::min<int64_t>(std::max<int64_t>(hw / 4, 1), 4)
+                                   : std::min<int64_t>(std::max<int64_t>(hw - 2, 1), 10);
   const int nw = (int)std::min<int64_t>(nr, std::max<int64_t>(1, env_or("DTWGPU_KM_WORKERS", cap)));
   if (nw <= 1)
     return km_loop(ctx, p, k, max_iterations, seed, restart_begin, restart_end, observer, user,
@@ -662,9 +694,8 @@ static int km_run(dtwg_ctx* ctx, int64_t k, int64_t restarts, int64_t max_iterat
 // The matrix views a context's sweeps read: its own, or (restart workers) the source's.
 static KmState km_state(dtwg_ctx* ctx, int64_t p, int64_t k) {
   const dtwg_ctx* m = ctx->km_src ? ctx->km_src : ctx;
-  KmState S{ctx, p, k, km_matrix(ctx), km_is_cond(ctx), nullptr, false, nullptr, nullptr, 0};
-  if (m->layout_valid) {
-    cudaStreamWaitEvent(ctx->stream, m->layout_ready, 0);
+  KmState S{ctx, p, k, km_matrix(ctx), km_is_cond(ctx), m->d_cond.ptr, m};
+  if (m->layout_valid) {  // the sweeps wait for it (km_wait_ready), the seeding does not
     S.psq = m->d_psq.ptr;
     S.psq32 = m->layout32;
     S.perm = m->d_perm.ptr;
@@ -802,6 +833,7 @@ int dtwg_km_update(dtwg_ctx* ctx, const int64_t* medoids, int64_t k, const int64
     if (assignment[j] < 0 || assignment[j] >= p)
       return ctx->fail(DTWG_INDEX_OUT_OF_RANGE, "assignment out of range");
   KmState S = km_state(ctx, p, k);
+  km_wait_ready(S);
   std::vector<int64_t> med(medoids, medoids + k);
   // The caller's assignment (any, not necessarily nearest-medoid): cluster slots by
   // lower_bound (kmedoids.hpp:88-90) and D(j, assignment[j]) for the empty-cluster repair.
