@@ -16,6 +16,9 @@
 // k-medoids host loop in km_host.cu (shared internals: host_ctx.cuh).
 #include "host_ctx.cuh"
 
+#include <chrono>
+#include <cstdio>
+
 namespace dtwgpu {
 namespace host {
 
@@ -125,10 +128,16 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
   const dtwg_ctx::PlanKey key{hw, sb, se, auto_widen, fp32, ctx->force_family, ctx->force_G,
                               ctx->force_R, env_or("DTWGPU_UNDERFILL_REPLAN", 1)};
   if (!(ctx->plan_valid && ctx->plan_key == key)) {
+    const auto t0 = std::chrono::steady_clock::now();
     ctx->plan_cache = make_plan(ctx, hw, auto_widen, fp32, sb, se);
     ctx->plan_key = key;
     ctx->plan_valid = true;
     ctx->list_uploaded = false;
+    if (env_or("DTWGPU_VERBOSE", 0))
+      fprintf(stderr, "dtwgpu: planned %lld pairs into %zu classes in %.1f ms\n",
+              (long long)(se - sb), ctx->plan_cache.size(),
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                  .count());
   }
   std::vector<PlanClass>& plan = ctx->plan_cache;
   ctx->last_plan.clear();

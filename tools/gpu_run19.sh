@@ -1,0 +1,5 @@
+set -x
+mkdir -p gpurun_out
+./tools/build/block > gpurun_out/r2v_block.log 2>&1
+DTWGPU_VERBOSE=1 timeout 300 python tools/prof_fill.py --config 5 --reps 2 > gpurun_out/r2v_plan.log 2>&1
+echo done
