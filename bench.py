@@ -367,6 +367,8 @@ def run_gpu_arm(a, ds):
             # NCCL init lines (rank count, transport) in the log so the ranks can be checked
             os.environ.setdefault("NCCL_DEBUG", "INFO")
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            # keep stdout to the one JSON line (NCCL logs to stdout by default)
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)

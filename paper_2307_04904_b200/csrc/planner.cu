@@ -381,6 +381,21 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
     }
     return oc >= 0 ? old_hint[oc] : 0;
   };
+  // precost (below): per distinct shape its configuration, computed on all host threads
+  std::vector<int32_t> pre_idx;
+  std::vector<KernelCfg> pre_cfgs;
+  auto class_of_cfg = [&](const KernelCfg& cfg) -> int {
+    const auto key = std::make_tuple((int)cfg.family * 2 + (int)cfg.ring + 4 * cfg.U, cfg.G, cfg.R, cfg.mask,
+                                     cfg.kr, cfg.P, cfg.TR + 100 * (int)cfg.ysm);
+    auto ic = cls_of_cfg.find(key);
+    if (ic != cls_of_cfg.end()) return ic->second;
+    PlanClass pc;
+    pc.cfg = cfg;
+    plan.push_back(pc);
+    const int cls = (int)plan.size() - 1;
+    cls_of_cfg[key] = cls;
+    return cls;
+  };
   auto class_of = [&](int64_t a, int64_t b, Shape& s) -> int {
     s = shape_of(ctx, a, b, hw, auto_widen);
     int* slotp = use_tab ? &cls_tab[(size_t)(s.n * L1 + s.m)] : nullptr;
@@ -390,20 +405,9 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
       if (it != cls_of_shape.end()) return it->second;
     }
     double cst = 0;
-    const KernelCfg cfg = choose_cfg(ctx, s, fp32, &cst, count_hint(s));
-    const auto key = std::make_tuple((int)cfg.family * 2 + (int)cfg.ring + 4 * cfg.U, cfg.G, cfg.R, cfg.mask,
-                                     cfg.kr, cfg.P, cfg.TR + 100 * (int)cfg.ysm);
-    int cls;
-    auto ic = cls_of_cfg.find(key);
-    if (ic == cls_of_cfg.end()) {
-      PlanClass pc;
-      pc.cfg = cfg;
-      plan.push_back(pc);
-      cls = (int)plan.size() - 1;
-      cls_of_cfg[key] = cls;
-    } else {
-      cls = ic->second;
-    }
+    const int32_t pre = slotp ? pre_idx[(size_t)(s.n * L1 + s.m)] : -1;
+    const int cls = class_of_cfg(pre >= 0 ? pre_cfgs[(size_t)pre]
+                                          : choose_cfg(ctx, s, fp32, &cst, count_hint(s)));
     if (slotp) *slotp = cls;
     else cls_of_shape[s] = cls;
     return cls;
@@ -425,6 +429,63 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
     i0 = lo;
   }
   const int64_t j0 = i0 + 1 + (sb - row_off(i0, p));
+  // Shapes are costed in parallel before the passes (c5: ~1.1M distinct (n, m) shapes x
+  // ~35 candidates, ~3.4 s serially): the distinct shapes of the slot range and their
+  // configurations on all host threads; pass 1 then only looks them up.
+  std::vector<std::pair<int32_t, int32_t>> shapes;  // distinct (n, m) of the slot range
+  auto precost = [&]() {
+    if (!use_tab) return;
+    if (shapes.empty()) {
+      std::vector<uint8_t> seen((size_t)(L1 * L1), 0);
+      int64_t i = i0, j = j0;
+      for (int64_t slot = sb; slot < se; ++slot) {
+        const int64_t la = ctx->h_len[i], lb = ctx->h_len[j];
+        const int64_t n = std::max(la, lb), m = std::min(la, lb);
+        uint8_t& f = seen[(size_t)(n * L1 + m)];
+        if (!f) {
+          f = 1;
+          shapes.emplace_back((int32_t)n, (int32_t)m);
+        }
+        if (++j == p) {
+          ++i;
+          j = i + 1;
+        }
+      }
+      std::sort(shapes.begin(), shapes.end());
+    }
+    const size_t ns = shapes.size();
+    std::vector<KernelCfg>& cfgs = pre_cfgs;
+    cfgs.assign(ns, KernelCfg{});
+    std::vector<Shape> sh(ns);
+    for (size_t q = 0; q < ns; ++q) {
+      // shape_of from the lengths alone (the pair's indices only pick the lengths)
+      Shape t;
+      t.n = shapes[q].first;
+      t.m = shapes[q].second;
+      if (hw < 0) {
+        t.hw = t.n;
+      } else {
+        const int64_t gap = t.n - t.m;
+        t.hw = (auto_widen && gap > hw) ? gap : hw;
+      }
+      if (t.hw > t.n) t.hw = t.n;
+      sh[q] = t;
+    }
+    const int nt = (int)std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)std::thread::hardware_concurrency(), (int64_t)(ns / 4096) + 1));
+    std::vector<std::thread> th;
+    for (int w = 0; w < nt; ++w)
+      th.emplace_back([&, w] {
+        for (size_t q = (size_t)w; q < ns; q += (size_t)nt) {
+          double cst = 0;
+          cfgs[q] = choose_cfg(ctx, sh[q], fp32, &cst, count_hint(sh[q]));
+        }
+      });
+    for (auto& t : th) t.join();
+    // class ids are assigned in pass 1, in order of first appearance (as before)
+    pre_idx.assign((size_t)(L1 * L1), -1);
+    for (size_t q = 0; q < ns; ++q) pre_idx[(size_t)(sh[q].n * L1 + sh[q].m)] = (int32_t)q;
+  };
   // pass 1: classes, bucket counts
   std::vector<std::vector<int64_t>> counts;
   auto pass1 = [&]() {
@@ -446,6 +507,7 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
       }
     }
   };
+  precost();
   pass1();
   // Shapes are first costed without a pair count (fill factor 1), which favours few lanes
   // per pair. A Full class that cannot keep ~half the GPU's warp slots busy with its
@@ -469,6 +531,7 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
       plan.clear();
       cls_of_cfg.clear();
       counts.clear();
+      precost();
       pass1();
     }
   }
