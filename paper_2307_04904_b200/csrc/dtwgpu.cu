@@ -126,7 +126,8 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
     if (rc) return rc;
   }
   const dtwg_ctx::PlanKey key{hw, sb, se, auto_widen, fp32, ctx->force_family, ctx->force_G,
-                              ctx->force_R, env_or("DTWGPU_UNDERFILL_REPLAN", 1)};
+                              ctx->force_R,
+                              env_or("DTWGPU_UNDERFILL_REPLAN", 1) * 2 + env_or("DTWGPU_PLAN_TABLE", 1)};
   if (!(ctx->plan_valid && ctx->plan_key == key)) {
     const auto t0 = std::chrono::steady_clock::now();
     ctx->plan_cache = make_plan(ctx, hw, auto_widen, fp32, sb, se);

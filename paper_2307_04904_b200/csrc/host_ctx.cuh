@@ -141,7 +141,7 @@ struct dtwg_ctx {
     int auto_widen;
     bool fp32;
     int force_family, force_G, force_R;
-    int64_t replan;  // DTWGPU_UNDERFILL_REPLAN (planner.cu)
+    int64_t replan;  // DTWGPU_UNDERFILL_REPLAN, DTWGPU_PLAN_TABLE (planner.cu)
     bool operator==(const PlanKey& o) const {
       return hw == o.hw && sb == o.sb && se == o.se && auto_widen == o.auto_widen &&
              fp32 == o.fp32 && force_family == o.force_family && force_G == o.force_G &&

@@ -2,6 +2,8 @@
 // the slot lists of the resulting pair classes ("Planner").
 #include "host_ctx.cuh"
 
+#include <chrono>
+
 namespace dtwgpu {
 namespace host {
 
@@ -336,6 +338,180 @@ void split_tail_round(dtwg_ctx* ctx, std::vector<PlanClass>& plan, const Shape& 
   plan.push_back(t);
 }
 
+// Ragged datasets whose lengths fit a (n, m) table (max length <= 8191): everything the
+// plan needs per slot is a function of its shape, so one scan counts the pairs of every
+// shape (in order of first appearance), the distinct shapes are costed on all host
+// threads, classes and their statistics come from the shape counts (the underfill re-plan
+// included), and a second scan writes every slot straight to its final position -- the
+// same order as the general path below (per class: passes, then rows, then the shorter
+// length, all descending; slots ascending inside a shape). c5: 12.5M pairs, ~1M shapes.
+std::vector<PlanClass> make_plan_table(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool fp32,
+                                       int64_t sb, int64_t se, int64_t L1) {
+  const int64_t p = ctx->p;
+  const bool verbose = env_or("DTWGPU_VERBOSE", 0) != 0;
+  auto tnow = [] { return std::chrono::steady_clock::now(); };
+  auto ms_since = [&](std::chrono::steady_clock::time_point t) {
+    return std::chrono::duration<double, std::milli>(tnow() - t).count();
+  };
+  auto tp = tnow();
+  int64_t i0;
+  {
+    int64_t lo = 0, hi = p - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) / 2;
+      if (row_off(mid, p) <= sb) lo = mid;
+      else hi = mid - 1;
+    }
+    i0 = lo;
+  }
+  const int64_t j0 = i0 + 1 + (sb - row_off(i0, p));
+  const int64_t* len = ctx->h_len.data();
+  // scan 1: pairs per shape, shapes in order of first appearance
+  std::vector<int32_t> qidx((size_t)(L1 * L1), -1);
+  std::vector<Shape> sh;
+  std::vector<int64_t> cnt;
+  {
+    int64_t i = i0, j = j0;
+    for (int64_t slot = sb; slot < se; ++slot) {
+      const int64_t la = len[i], lb = len[j];
+      const int64_t n = std::max(la, lb), m = std::min(la, lb);
+      int32_t& q = qidx[(size_t)(n * L1 + m)];
+      if (q < 0) {
+        q = (int32_t)sh.size();
+        Shape t;
+        t.n = n;
+        t.m = m;
+        if (hw < 0) {
+          t.hw = n;
+        } else {
+          const int64_t gap = n - m;
+          t.hw = (auto_widen && gap > hw) ? gap : hw;
+        }
+        if (t.hw > t.n) t.hw = t.n;
+        sh.push_back(t);
+        cnt.push_back(0);
+      }
+      ++cnt[(size_t)q];
+      if (++j == p) {
+        ++i;
+        j = i + 1;
+      }
+    }
+  }
+  const size_t ns = sh.size();
+  if (verbose) fprintf(stderr, "dtwgpu: plan: %zu shapes counted in %.1f ms\n", ns, ms_since(tp));
+  tp = tnow();
+  // configurations per shape on all host threads (hint: pair count for the re-plan)
+  std::vector<KernelCfg> cfg(ns);
+  std::vector<int64_t> hint(ns, 0);
+  std::vector<uint8_t> todo(ns, 1);
+  auto cost_all = [&]() {
+    const int nt = (int)std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)std::thread::hardware_concurrency(), (int64_t)(ns / 4096) + 1));
+    std::vector<std::thread> th;
+    for (int w = 0; w < nt; ++w)
+      th.emplace_back([&, w] {
+        for (size_t q = (size_t)w; q < ns; q += (size_t)nt) {
+          if (!todo[q]) continue;
+          double cst = 0;
+          cfg[q] = choose_cfg(ctx, sh[q], fp32, &cst, hint[q]);
+        }
+      });
+    for (auto& t : th) t.join();
+  };
+  std::vector<PlanClass> plan;
+  std::vector<int> cls(ns);
+  std::map<std::tuple<int, int, int, bool, int, int, int>, int> cls_of_cfg;
+  auto assign = [&]() {  // classes in order of first appearance of their shapes
+    plan.clear();
+    cls_of_cfg.clear();
+    for (size_t q = 0; q < ns; ++q) {
+      const KernelCfg& c = cfg[q];
+      const auto key = std::make_tuple((int)c.family * 2 + (int)c.ring + 4 * c.U, c.G, c.R,
+                                       c.mask, c.kr, c.P, c.TR + 100 * (int)c.ysm);
+      auto it = cls_of_cfg.find(key);
+      if (it == cls_of_cfg.end()) {
+        PlanClass pc;
+        pc.cfg = c;
+        plan.push_back(pc);
+        it = cls_of_cfg.emplace(key, (int)plan.size() - 1).first;
+      }
+      cls[q] = it->second;
+    }
+  };
+  cost_all();
+  assign();
+  // underfill re-plan (see make_plan): re-cost the shapes of Full classes that cannot keep
+  // half the GPU's warp slots busy with their lanes per pair, with the class's pair count
+  if (ctx->force_family < 0 && env_or("DTWGPU_UNDERFILL_REPLAN", 1) != 0) {
+    std::vector<int64_t> ccount(plan.size(), 0);
+    for (size_t q = 0; q < ns; ++q) ccount[(size_t)cls[q]] += cnt[q];
+    bool any = false;
+    for (size_t q = 0; q < ns; ++q) {
+      const PlanClass& pc = plan[(size_t)cls[q]];
+      const bool under = pc.cfg.family == Family::Full &&
+                         fill_factor(ccount[(size_t)cls[q]], pc.cfg.G, ctx->num_sms) < 0.5;
+      todo[q] = under;
+      hint[q] = under ? ccount[(size_t)cls[q]] : 0;
+      any = any || under;
+    }
+    if (any) {
+      cost_all();
+      assign();
+    }
+  }
+  if (verbose) fprintf(stderr, "dtwgpu: plan: shapes costed in %.1f ms\n", ms_since(tp));
+  tp = tnow();
+  // per class: statistics, and the shapes in slot order -> start position of every shape
+  std::vector<std::vector<int32_t>> members(plan.size());
+  for (size_t q = 0; q < ns; ++q) {
+    PlanClass& pc = plan[(size_t)cls[q]];
+    members[(size_t)cls[q]].push_back((int32_t)q);
+    pc.max_n = std::max(pc.max_n, sh[q].n);
+    pc.max_m = std::max(pc.max_m, sh[q].m);
+    pc.cost += double(cnt[q]) * double(sh[q].n) * double(sh[q].m);
+    pc.cells += double(cnt[q]) * double(pair_cells(sh[q].n, sh[q].m, sh[q].hw));
+  }
+  std::vector<int64_t> start(ns, 0);
+  for (size_t c = 0; c < plan.size(); ++c) {
+    const KernelCfg& cc = plan[c].cfg;
+    const int64_t W = (int64_t)cc.G * cc.R;
+    auto npass = [&](int32_t q) { return cc.family == Family::Full ? (sh[q].m + W - 1) / W : 1; };
+    auto& mem = members[c];
+    std::sort(mem.begin(), mem.end(), [&](int32_t a, int32_t b) {
+      const int64_t pa = npass(a), pb = npass(b);
+      if (pa != pb) return pa > pb;
+      if (sh[a].n != sh[b].n) return sh[a].n > sh[b].n;
+      return sh[a].m > sh[b].m;
+    });
+    int64_t acc = 0;
+    for (int32_t q : mem) {
+      start[(size_t)q] = acc;
+      acc += cnt[(size_t)q];
+    }
+    plan[c].slots.resize((size_t)acc);
+  }
+  // scan 2: every slot to its final position
+  {
+    int64_t i = i0, j = j0;
+    for (int64_t slot = sb; slot < se; ++slot) {
+      const int64_t la = len[i], lb = len[j];
+      const int32_t q = qidx[(size_t)(std::max(la, lb) * L1 + std::min(la, lb))];
+      plan[(size_t)cls[(size_t)q]].slots[(size_t)start[(size_t)q]++] = slot;
+      if (++j == p) {
+        ++i;
+        j = i + 1;
+      }
+    }
+  }
+  if (verbose) fprintf(stderr, "dtwgpu: plan: slots placed in %.1f ms\n", ms_since(tp));
+  for (auto& pc : plan) {
+    maybe_strip(ctx, pc, (int64_t)pc.slots.size(), -1);
+    set_single_strip(pc);
+  }
+  return plan;
+}
+
 std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool fp32,
                                  int64_t sb, int64_t se) {
   std::vector<PlanClass> plan;
@@ -362,6 +538,8 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
   const int64_t L1 = maxlen + 1;
   std::vector<int> cls_tab;
   const bool use_tab = L1 * L1 <= (int64_t)1 << 26;
+  if (use_tab && env_or("DTWGPU_PLAN_TABLE", 1) != 0)
+    return make_plan_table(ctx, hw, auto_widen, fp32, sb, se, L1);
   if (use_tab) cls_tab.assign((size_t)(L1 * L1), -1);
   std::map<Shape, int> cls_of_shape;
   std::map<std::tuple<int, int, int, bool, int, int, int>, int> cls_of_cfg;
@@ -455,7 +633,9 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
     }
     const size_t ns = shapes.size();
     std::vector<KernelCfg>& cfgs = pre_cfgs;
-    cfgs.assign(ns, KernelCfg{});
+    // re-plan round: only shapes of underfilled first-round classes change (count hints)
+    const bool again = cfgs.size() == ns;
+    if (!again) cfgs.assign(ns, KernelCfg{});
     std::vector<Shape> sh(ns);
     for (size_t q = 0; q < ns; ++q) {
       // shape_of from the lengths alone (the pair's indices only pick the lengths)
@@ -477,8 +657,10 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
     for (int w = 0; w < nt; ++w)
       th.emplace_back([&, w] {
         for (size_t q = (size_t)w; q < ns; q += (size_t)nt) {
+          const int64_t hint = count_hint(sh[q]);
+          if (again && hint == 0) continue;
           double cst = 0;
-          cfgs[q] = choose_cfg(ctx, sh[q], fp32, &cst, count_hint(sh[q]));
+          cfgs[q] = choose_cfg(ctx, sh[q], fp32, &cst, hint);
         }
       });
     for (auto& t : th) t.join();
@@ -507,8 +689,17 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
       }
     }
   };
+  const bool verbose = env_or("DTWGPU_VERBOSE", 0) != 0;
+  auto tnow = [] { return std::chrono::steady_clock::now(); };
+  auto ms_since = [&](std::chrono::steady_clock::time_point t) {
+    return std::chrono::duration<double, std::milli>(tnow() - t).count();
+  };
+  auto tp = tnow();
   precost();
+  if (verbose) fprintf(stderr, "dtwgpu: plan: %zu shapes costed in %.1f ms\n", shapes.size(), ms_since(tp));
+  tp = tnow();
   pass1();
+  if (verbose) fprintf(stderr, "dtwgpu: plan: pass 1 %.1f ms\n", ms_since(tp));
   // Shapes are first costed without a pair count (fill factor 1), which favours few lanes
   // per pair. A Full class that cannot keep ~half the GPU's warp slots busy with its
   // lanes per pair is re-costed with its real pair count (fill_factor), and the pass runs
@@ -531,10 +722,13 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
       plan.clear();
       cls_of_cfg.clear();
       counts.clear();
+      tp = tnow();
       precost();
       pass1();
+      if (verbose) fprintf(stderr, "dtwgpu: plan: underfill re-plan %.1f ms\n", ms_since(tp));
     }
   }
+  tp = tnow();
   // descending bucket order -> start offsets
   std::vector<std::vector<int64_t>> start(plan.size());
   for (size_t c = 0; c < plan.size(); ++c) {
@@ -590,10 +784,13 @@ std::vector<PlanClass> make_plan(dtwg_ctx* ctx, int64_t hw, int auto_widen, bool
       }
     }
   }
+  if (verbose) fprintf(stderr, "dtwgpu: plan: passes 2-3 %.1f ms\n", ms_since(tp));
+  tp = tnow();
   for (auto& pc : plan) {
     maybe_strip(ctx, pc, (int64_t)pc.slots.size(), -1);
     set_single_strip(pc);
   }
+  if (verbose) fprintf(stderr, "dtwgpu: plan: strip check %.1f ms\n", ms_since(tp));
   return plan;
 }
 

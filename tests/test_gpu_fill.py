@@ -519,6 +519,29 @@ def test_planner_mixed_classes_short_and_long(eng, prec, replan, monkeypatch):
             assert "G=1,R=46" not in eng.last_plan(), eng.last_plan()
 
 
+@pytest.mark.parametrize("prec", [0, 1])
+def test_table_planner_equals_general_planner(eng, prec, monkeypatch):
+    """The table-driven ragged planner (shape counts, parallel costing, one placement scan)
+    makes exactly the plan of the general per-slot path: same classes, pair counts, cells
+    and slot order (bitwise-equal matrices), on c5-like ragged data with underfilled
+    classes (re-plan) and a slot sub-range."""
+    ds = gen.config5(n=260, hi=700)
+    total = ds.p * (ds.p - 1) // 2
+    for sb, se in ((0, total), (1234, total - 777)):
+        plans, outs = [], []
+        for table in ("1", "0"):
+            monkeypatch.setenv("DTWGPU_PLAN_TABLE", table)
+            eng.upload(ds.samples, ds.offsets)
+            import torch
+            out = torch.empty(se - sb, dtype=torch.float64, device="cuda")
+            eng.fill_slots(ds.half_width, ds.auto_widen, prec, sb, se, out.data_ptr())
+            eng.synchronize()
+            plans.append(eng.last_plan())
+            outs.append(out.cpu().numpy())
+        assert plans[0] == plans[1], plans
+        assert np.array_equal(outs[0].view(np.uint64), outs[1].view(np.uint64))
+
+
 @pytest.mark.parametrize("fam,G,R,prec", [(0, 1, 46, 0), (3, 1, 46, 1), (3, 16, 30, 1),
                                          (3, 2, 16, 0)])
 def test_new_instantiations_on_tiny_inputs(eng, fam, G, R, prec):
