@@ -14,7 +14,7 @@
 #define DTWG_FULL_CFGS_F64(X) X(2, 30, 4) X(4, 30, 4) X(8, 30, 4)
 #define DTWG_FULL_CFGS_F32(X) X(16, 30, 4) X(1, 46, 4) X(16, 32, 4) X(1, 56, 4) X(1, 64, 4)
 // One lane per pair, fp64, single strip (dtw_lane_kernel): (R, rows per step)
-#define DTWG_LANE_CFGS_F64(X) X(46, 2) X(46, 4)
+#define DTWG_LANE_CFGS_F64(X) X(46, 2)
 #define DTWG_BAND_CFGS_G16(X) X(16, 7) X(16, 9) X(16, 11) X(16, 13)
 #define DTWG_BAND_CFGS_G32(X) X(32, 3) X(32, 5) X(32, 7) X(32, 9) X(32, 13)
 // Band family, shared-memory y ring variant
