@@ -139,6 +139,24 @@ __device__ __forceinline__ void store_result(const FillArgs& A, int64_t slot, do
   for (int r = 0; r < A.n_peer; ++r) A.peer_out[r][slot - A.peer_base] = v;
 }
 
+// Dynamic item scheduling: a warp takes its next `per` consecutive items of the launch from
+// the class's counter (A.work, zeroed before the launch); without a counter, the static
+// grid-stride item `static_base`. Classes run concurrently on side streams, so the CTAs of
+// one class start as those of another exit; with a static split the late CTAs still held
+// a full share (c5 shards of 8 GPUs: 254-318 ms for equal cells). Ragged classes list
+// their pairs longest first, so taking items in order is longest-processing-time first.
+__device__ __forceinline__ int64_t take_items(const FillArgs& A, int64_t static_base, int per) {
+  if (A.work == nullptr) return static_base;
+  unsigned long long b = 0;
+  if ((threadIdx.x & 31) == 0) b = atomicAdd(A.work, (unsigned long long)per);
+  return (int64_t)__shfl_sync(0xffffffffu, b, 0);
+}
+// The item after `base`: the next counter grab, or the static grid stride.
+__device__ __forceinline__ int64_t next_items(const FillArgs& A, int64_t base, int64_t stride,
+                                              int per) {
+  return take_items(A, base + stride, per);
+}
+
 struct Pair {
   int64_t slot;
   int64_t xoff, yoff;  // rows series (longer), columns series (shorter)
@@ -298,7 +316,8 @@ __device__ __forceinline__ void full_body(const FillArgs& A, volatile typename A
   const T INF = Ar::inf();
   const T* S = Ar::base(A);
 
-  for (int64_t base = warp * GPW; base < A.count; base += nwarps * GPW) {
+  for (int64_t base = take_items(A, warp * GPW, GPW); base < A.count;
+       base = next_items(A, base, nwarps * GPW, GPW)) {
     const int64_t item = base + gw;
     const bool valid = item < A.count;
     const Pair P = load_pair(A, valid ? item : base);
@@ -533,7 +552,8 @@ __global__ void __launch_bounds__(kThreads) dtw_lane_kernel(const FillArgs A) {
   const T* S = Ar::base(A);
   const int64_t base0 = tid - (threadIdx.x & 31);  // the warp's first item
 
-  for (int64_t base = base0; base < A.count; base += nthreads) {
+  for (int64_t base = take_items(A, base0, 32); base < A.count;
+       base = next_items(A, base, nthreads, 32)) {
     const int64_t item = base + (threadIdx.x & 31);
     const bool valid = item < A.count;
     const Pair P = load_pair(A, valid ? item : base);
@@ -982,7 +1002,8 @@ __global__ void __launch_bounds__(kThreads, P == 1 ? 5 : 3) dtw_band_kernel(cons
   const T INF = Ar::inf();
   const T* S = Ar::bbase(A);
 
-  for (int64_t base = warp * GPW * P; base < A.count; base += nwarps * GPW * P) {
+  for (int64_t base = take_items(A, warp * GPW * P, GPW * P); base < A.count;
+       base = next_items(A, base, nwarps * GPW * P, GPW * P)) {
     const T* xp[P];
     const T* yp[P];
     const T* Y[P];
@@ -1174,7 +1195,8 @@ __global__ void DTWG_RING_BOUNDS dtw_bandring_kernel(const FillArgs A) {
   T* ring = rings[threadIdx.x / G];
   constexpr int JOFF = 4 * kRing;  // keeps ring indices of j >= 1 - hw - G non-negative
 
-  for (int64_t base = warp * GPW; base < A.count; base += nwarps * GPW) {
+  for (int64_t base = take_items(A, warp * GPW, GPW); base < A.count;
+       base = next_items(A, base, nwarps * GPW, GPW)) {
     const int64_t item = base + gw;
     const bool valid = item < A.count;
     const Pair Pp = load_pair(A, valid ? item : base);
@@ -1399,7 +1421,8 @@ __global__ void __launch_bounds__(kThreads, Ar::kFp32 ? DTWG_UNIT_MINB32(R) : DT
   T* ring = rings[threadIdx.x / G];
   constexpr int JOFF = 4 * RING;
 
-  for (int64_t base = warp * GPW; base < A.count; base += nwarps * GPW) {
+  for (int64_t base = take_items(A, warp * GPW, GPW); base < A.count;
+       base = next_items(A, base, nwarps * GPW, GPW)) {
     const int64_t item = base + gw;
     const bool valid = item < A.count;
     const Pair Pp = load_pair(A, valid ? item : base);

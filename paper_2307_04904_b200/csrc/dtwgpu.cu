@@ -127,7 +127,9 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
   }
   const dtwg_ctx::PlanKey key{hw, sb, se, auto_widen, fp32, ctx->force_family, ctx->force_G,
                               ctx->force_R,
-                              env_or("DTWGPU_UNDERFILL_REPLAN", 1) * 2 + env_or("DTWGPU_PLAN_TABLE", 1)};
+                              env_or("DTWGPU_UNDERFILL_REPLAN", 1) * 2 + env_or("DTWGPU_PLAN_TABLE", 1) +
+                                  4 * env_or("DTWGPU_TAIL_SPLIT", 1) +
+                                  8 * env_or("DTWGPU_TAIL_SERIAL", 1)};
   if (!(ctx->plan_valid && ctx->plan_key == key)) {
     const auto t0 = std::chrono::steady_clock::now();
     ctx->plan_cache = make_plan(ctx, hw, auto_widen, fp32, sb, se);
@@ -225,13 +227,17 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
     }
   }
   if (scratch_total) CU(ctx->d_scratch.reserve((size_t)scratch_total), "cudaMalloc scratch");
+  // One item counter per class: dynamic item scheduling in every fill kernel (take_items,
+  // dtw_kernels.cuh), strip items in the Strip family. DTWGPU_DYNAMIC_ITEMS=0: static
+  // grid-stride items (diagnostics).
+  const bool dynamic_items = env_or("DTWGPU_DYNAMIC_ITEMS", 1) != 0;
+  CU(ctx->d_work.reserve((size_t)plan.size()), "cudaMalloc work");
+  CU(cudaMemsetAsync(ctx->d_work.ptr, 0, plan.size() * sizeof(unsigned long long), ctx->stream),
+     "memset work");
   if (n_strip_cls) {
     CU(ctx->d_prog.reserve((size_t)prog_total), "cudaMalloc prog");
     CU(ctx->d_cols.reserve((size_t)cols_total), "cudaMalloc cols");
-    CU(ctx->d_work.reserve((size_t)plan.size()), "cudaMalloc work");
     CU(cudaMemsetAsync(ctx->d_prog.ptr, 0, prog_total * sizeof(int), ctx->stream), "memset prog");
-    CU(cudaMemsetAsync(ctx->d_work.ptr, 0, plan.size() * sizeof(unsigned long long), ctx->stream),
-       "memset work");
     if (sb_total) {
       CU(ctx->d_strip_base.reserve((size_t)sb_total), "cudaMalloc strip_base");
       for (size_t c = 0; c < plan.size(); ++c)
@@ -248,6 +254,7 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
   }
   size_t pos = 0;
   int next_aux = 0;
+  cudaStream_t prev_st = ctx->stream;
   for (size_t c = 0; c < plan.size(); ++c) {
     auto& pc = plan[c];
     if (!dtwgpu::fill_cfg_supported(pc.cfg))
@@ -284,6 +291,7 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
       for (int r = 0; r < a.n_peer; ++r) a.peer_out[r] = ctx->peers[r];
       a.peer_base = 0;
     }
+    a.work = dynamic_items ? ctx->d_work.ptr + c : nullptr;
     if (pc.cfg.family == Family::Strip) {
       a.strip_base = sb_off[c] >= 0 ? ctx->d_strip_base.ptr + sb_off[c] : nullptr;
       a.strips_per_pair = pc.strips_per_pair;
@@ -292,7 +300,10 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
       a.cols = ctx->d_cols.ptr + cols_off[c];
       a.col_stride = pc.max_n + 2;
     }
-    cudaStream_t st = concurrent ? ctx->aux[next_aux++ % dtwg_ctx::kAux] : ctx->stream;
+    cudaStream_t st = concurrent ? (pc.after_prev && c > 0 ? prev_st
+                                                          : ctx->aux[next_aux++ % dtwg_ctx::kAux])
+                                 : ctx->stream;
+    prev_st = st;
     CU(dtwgpu::launch_fill(pc.cfg, a, (int)blocks, st), "fill launch");
     ctx->launches++;
     char buf[200];

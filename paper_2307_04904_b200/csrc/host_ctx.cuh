@@ -93,6 +93,9 @@ struct PlanClass {
   // Strip family: strips per pair (uniform) or prefix sums over `slots` (ragged)
   int strips_per_pair = 0;
   std::vector<int64_t> strip_base;
+  // Launch on the previous class's stream, after it (a split tail round: its CTAs must not
+  // take SM slots before every CTA of the full rounds is resident)
+  bool after_prev = false;
 };
 
 inline int64_t row_off(int64_t i, int64_t p) { return i * p - i * (i + 1) / 2; }

@@ -309,25 +309,73 @@ void set_single_strip(PlanClass& pc) {
   if (dtwgpu::fill_cfg_supported(one)) pc.cfg = one;  // multi-pass-only instantiations keep mp
 }
 
+// Lane groups of `k` resident on the whole GPU (the persistent grid's item stride).
+int64_t resident_groups(const dtwg_ctx* ctx, const KernelCfg& k) {
+  return (int64_t)dtwgpu::fill_blocks_per_sm(k) * ctx->num_sms * (dtwgpu::kThreads / k.G);
+}
+
+// GPU-ns of a class of `count` same-shape pairs on `k` (cost: GPU-ns per pair at full
+// occupancy, full_cost). Uniform pairs run in whole rounds of the resident lane groups, so
+// a partial last round costs a full one; an underfilled launch (fewer than ~8 warps per SM)
+// runs at the fill_factor fraction of the rate.
+double class_time(const dtwg_ctx* ctx, const KernelCfg& k, double cost, int64_t count) {
+  const double fill = fill_factor(count, k.G, ctx->num_sms);
+  if (fill < 1.0) return double(count) * cost / fill;
+  const int64_t groups = resident_groups(ctx, k);
+  const int64_t rounds = (count + groups - 1) / groups;
+  return double(std::max<int64_t>(rounds * groups, count)) * cost;
+}
+
 // Same-length pairs all cost the same, so a class of few lanes per pair (one lane per
 // pair for c4) runs in whole rounds of its resident lane groups -- c4: 499,500 pairs over
-// 37,888 groups = 13.18 rounds, the last one 18% occupied at the speed of a full one. The
-// pairs of that partial round become a second class with more lanes per pair (chosen by
-// the cost model for that pair count), which runs on the whole GPU once the full rounds
-// drain (classes run on concurrent side streams): 13 + ~0.25 rounds instead of 14.
+// 37,888 groups = 13.18 rounds, the last one 18% occupied at the speed of a full one; one
+// GPU's shard of c4 at 8 GPUs is 1.65 rounds. The pairs of that partial round become a
+// second class with more lanes per pair, which runs on the whole GPU once the full rounds
+// drain (classes run on concurrent side streams), when the cost model puts it below one
+// full round: c4 13 + ~0.25 rounds instead of 14; c4 / 8 GPUs 1 + ~0.72 instead of 2.
+// The tail configuration is the fastest candidate with more lanes per pair, its own round
+// quantisation included (class_time).
 void split_tail_round(dtwg_ctx* ctx, std::vector<PlanClass>& plan, const Shape& s, bool fp32,
                       int64_t sb, int64_t se) {
   if (ctx->force_family >= 0 || plan.size() != 1 || env_or("DTWGPU_TAIL_SPLIT", 1) == 0) return;
   PlanClass& pc = plan[0];
   if (pc.cfg.family != Family::Full || pc.cfg.G > 2) return;
   const int64_t count = se - sb;
-  const int64_t groups = (int64_t)dtwgpu::fill_blocks_per_sm(pc.cfg) * ctx->num_sms *
-                         (dtwgpu::kThreads / pc.cfg.G);
+  const int64_t groups = resident_groups(ctx, pc.cfg);
   const int64_t full_rounds = count / groups, tail = count - full_rounds * groups;
-  if (full_rounds < 1 || tail == 0 || tail * 2 > groups) return;
+  if (full_rounds < 1 || tail == 0) return;
+  const bool mask = s.hw < s.n - 1;
+  // the partial round on the class's own configuration: one full round
+  // (pc.cost: GPU-ns per pair at full occupancy -- count >= one round fills the GPU)
+  const double keep = double(groups) * pc.cost;
   PlanClass t;
-  t.cfg = choose_cfg(ctx, s, fp32, &t.cost, tail);
-  if (t.cfg.G <= pc.cfg.G) return;  // nothing gained
+  double best = keep * 0.97;  // split only for a clear gain
+  bool found = false;
+  for (const Cand& c : kFull) {
+    if (c.G <= pc.cfg.G || (c.f32_only && !fp32) || (c.f64_only && fp32) ||
+        (c.unmasked && mask) || (c.masked_only && !mask))
+      continue;
+    KernelCfg k{Family::Full, c.G, c.R, mask, fp32, -1, 1, c.TR};
+    k.ysm = c.ysm;
+    if (s.m <= (int64_t)c.G * c.R) {
+      KernelCfg one = k;
+      one.mp = false;
+      if (dtwgpu::fill_cfg_supported(one)) k = one;
+    }
+    if (!dtwgpu::fill_cfg_supported(k)) continue;
+    const double tt = class_time(ctx, k, full_cost(s, c, mask, fp32), tail);
+    if (tt < best) {
+      best = tt;
+      t.cfg = k;
+      t.cost = tt / double(tail);
+      found = true;
+    }
+  }
+  if (!found) return;
+  // Serial after the full rounds (same stream): their lanes all finish together, while a
+  // concurrent launch let tail CTAs take SM slots first on some runs and pushed full-round
+  // CTAs into a second wave (c4 / 8 GPUs: 217 -> 244 ms on one shard of eight).
+  t.after_prev = env_or("DTWGPU_TAIL_SERIAL", 1) != 0;
   t.max_n = pc.max_n;
   t.max_m = pc.max_m;
   set_single_strip(t);

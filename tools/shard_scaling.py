@@ -21,6 +21,7 @@ sys.path.insert(0, ROOT)
 
 import torch  # noqa: E402
 
+from bench import ClockSampler  # noqa: E402
 from paper_2307_04904_b200 import api, distributed as dd, generators as gen  # noqa: E402
 
 
@@ -49,19 +50,26 @@ def main():
         t1 = best_ms(eng, ds, prec, 0, total, out, a.reps)
         cells = eng.count_cells(ds.half_width, ds.auto_widen, 0, total)
         rec = {"config": c, "precision": "fp32" if prec else "fp64", "fill_ms_1": t1,
+               "plan_1": eng.last_plan()[:300],
                "gcups_1": cells / t1 / 1e6, "worlds": {}}
         for w in [int(v) for v in a.worlds.split(",")]:
             bounds = dd.cell_bounds(ds.lengths, ds.half_width, ds.auto_widen, w)
-            shard_ms, shard_cells = [], []
+            shard_ms, shard_cells, plans, clocks = [], [], [], []
             for b, e in bounds:
-                shard_ms.append(best_ms(eng, ds, prec, b, e, out, a.reps) if e > b else 0.0)
+                with ClockSampler(0) as clk:
+                    shard_ms.append(best_ms(eng, ds, prec, b, e, out, a.reps) if e > b else 0.0)
+                cs = clk.summary()
+                clocks.append([cs.get("sm_mhz"), cs.get("reasons")])
                 shard_cells.append(eng.count_cells(ds.half_width, ds.auto_widen, b, e))
+                plans.append(eng.last_plan()[:300])
             worst = max(shard_ms)
             rec["worlds"][w] = {"shard_ms": [round(v, 3) for v in shard_ms],
                                 "shard_cells_frac": [round(v / cells, 4) for v in shard_cells],
                                 "max_ms": worst,
                                 "fill_efficiency": t1 / (w * worst),
-                                "predicted_fill_gcups": cells / worst / 1e6}
+                                "predicted_fill_gcups": cells / worst / 1e6,
+                                "plan_slowest": plans[shard_ms.index(worst)],
+                                "clocks": clocks}
         print(json.dumps(rec), flush=True)
         del out
         torch.cuda.empty_cache()
