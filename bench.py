@@ -636,8 +636,10 @@ def run_gpu_arm(a, ds):
                          "peak_source": peak_src,
                          "live_cell_ceiling": live_peak,
                          "frac_of_live_ceiling": (achieved / live_peak) if achieved else None,
-                         "live_ceiling_source": "dtwg_measure_cell_peak (cell body, 8 "
-                                                "independent chains/thread, all SMs), measured now"},
+                         "live_ceiling_source": "dtwg_measure_cell_peak (the cell body as independent "
+                                                "chains with three distinct inputs per cell, best "
+                                                "of the select and predicated-add forms, all SMs), "
+                                                "measured now"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

@@ -114,6 +114,45 @@ struct F64 {
     const T d = __dsub_rn(x, y);
     return __dadd_rn(__dmul_rn(d, d), best);
   }
+  // (x - y)^2 + min(m, left) with the minimum folded into the add: the same predicate
+  // that would select `left` or `m` picks one of two DADDs (`@q DADD v = dd + left;
+  // @!q DADD v = dd + m`), bit-identical to cell(x, y, mn(m, left)). 6 fp64-pipe + 2 ALU
+  // instructions per cell instead of 5 + 4. Written as PTX branches, which ptxas
+  // if-converts into the predicated pair (predicated PTX adds come out as two DADDs and
+  // four selects).
+  static __device__ __forceinline__ T cell3(T x, T y, T m, T left) {
+#ifndef DTWG_PD_CELL  // bit 0: Full family, bit 1: band family (0 = plain selects)
+#define DTWG_PD_CELL 3
+#endif
+#if DTWG_PD_CELL & 1
+    return cell3pd(x, y, m, left);
+#else
+    return cell(x, y, mn(m, left));
+#endif
+  }
+  static __device__ __forceinline__ T cell3b(T x, T y, T m, T left) {  // band family
+#if DTWG_PD_CELL & 2
+    return cell3pd(x, y, m, left);
+#else
+    return cell(x, y, mn(m, left));
+#endif
+  }
+  static __device__ __forceinline__ T cell3pd(T x, T y, T m, T left) {
+    T v;
+    asm("{\n\t.reg .pred q;\n\t.reg .f64 d;\n\t"
+        "sub.rn.f64 d, %1, %2;\n\t"
+        "mul.rn.f64 d, d, d;\n\t"
+        "setp.lt.f64 q, %4, %3;\n\t"
+        "@q bra L1_%=;\n\t"
+        "add.rn.f64 %0, d, %3;\n\t"
+        "bra L2_%=;\n\t"
+        "L1_%=:\n\t"
+        "add.rn.f64 %0, d, %4;\n\t"
+        "L2_%=:\n\t}"
+        : "=d"(v)
+        : "d"(x), "d"(y), "d"(m), "d"(left));
+    return v;
+  }
   static __device__ __forceinline__ const T* base(const FillArgs& A) { return A.samples; }
   static __device__ __forceinline__ const T* bbase(const FillArgs& A) { return A.bsamples; }
 };
@@ -126,6 +165,12 @@ struct F32 {
   static __device__ __forceinline__ T cell(T x, T y, T best) {
     const T d = __fsub_rn(x, y);
     return __fadd_rn(__fmul_rn(d, d), best);
+  }
+  static __device__ __forceinline__ T cell3(T x, T y, T m, T left) {
+    return cell(x, y, mn(m, left));
+  }
+  static __device__ __forceinline__ T cell3b(T x, T y, T m, T left) {
+    return cell(x, y, mn(m, left));
   }
   static __device__ __forceinline__ const T* base(const FillArgs& A) { return A.samples32; }
   static __device__ __forceinline__ const T* bbase(const FillArgs& A) { return A.bsamples32; }
@@ -215,7 +260,7 @@ __device__ __forceinline__ double min_unless(double a, double b, int k, int c) {
   return r;
 }
 
-template <int R, int NR, int KILL, class Ar>
+template <int R, int NR, int KILL, class Ar, bool PD = true>
 struct FullRows {
   using T = typename Ar::T;
   // NR consecutive rows r0 .. r0+NR-1 of this lane's R-column strip. Row t's cell at
@@ -246,15 +291,17 @@ struct FullRows {
       for (int t = 0; t < NR; ++t) {
         T v;
         if constexpr (KILL == 0) {
-          v = Ar::cell(x[t], yr, Ar::mn(Ar::mn(d[t], up), l[t]));
+          if constexpr (PD) v = Ar::cell3(x[t], yr, Ar::mn(d[t], up), l[t]);
+          else v = Ar::cell(x[t], yr, Ar::mn(Ar::mn(d[t], up), l[t]));
         } else if constexpr (Ar::kFp32) {
           v = Ar::cell(x[t], yr, Ar::mn(Ar::mn(d[t], up), l[t]));
           const bool k = ((KILL & 1) && r - t == klo) || ((KILL & 2) && r - t == khi);
           v = k ? INF : v;
         } else {
           const T m1 = (KILL & 1) ? min_unless(d[t], up, klo, r - t) : Ar::mn(d[t], up);
-          const T m = (KILL & 2) ? min_unless(m1, l[t], khi, r - t) : Ar::mn(m1, l[t]);
-          v = Ar::cell(x[t], yr, m);
+          if constexpr (KILL & 2) v = Ar::cell(x[t], yr, min_unless(m1, l[t], khi, r - t));
+          else if constexpr (PD) v = Ar::cell3(x[t], yr, m1, l[t]);
+          else v = Ar::cell(x[t], yr, Ar::mn(m1, l[t]));
         }
         d[t] = up;  // (t-1, r) is the diagonal of (t, r+1)
         l[t] = v;
@@ -596,10 +643,10 @@ __global__ void __launch_bounds__(kThreads) dtw_lane_kernel(const FillArgs A) {
       }
       T out[TR];
       if (r0 + TR - 1 <= n) {
-        if (need == 0) FullRows<R, TR, 0, Ar>::run(pv, ys, x, diag0, L, klo, khi, out);
-        else if (need == 1) FullRows<R, TR, 1, Ar>::run(pv, ys, x, diag0, L, klo, khi, out);
-        else if (need == 2) FullRows<R, TR, 2, Ar>::run(pv, ys, x, diag0, L, klo, khi, out);
-        else FullRows<R, TR, 3, Ar>::run(pv, ys, x, diag0, L, klo, khi, out);
+        if (need == 0) FullRows<R, TR, 0, Ar, false>::run(pv, ys, x, diag0, L, klo, khi, out);
+        else if (need == 1) FullRows<R, TR, 1, Ar, false>::run(pv, ys, x, diag0, L, klo, khi, out);
+        else if (need == 2) FullRows<R, TR, 2, Ar, false>::run(pv, ys, x, diag0, L, klo, khi, out);
+        else FullRows<R, TR, 3, Ar, false>::run(pv, ys, x, diag0, L, klo, khi, out);
         if (r0 + TR - 1 == n) {
           T rv = pv[0];
 #pragma unroll
@@ -615,7 +662,7 @@ __global__ void __launch_bounds__(kThreads) dtw_lane_kernel(const FillArgs A) {
             const T xt[1] = {x[t]};
             const T Lt[1] = {INF};
             T ot[1];
-            FullRows<R, 1, MASK ? 3 : 0, Ar>::run(pv, ys, xt, dg, Lt, klo + t, khi + t, ot);
+            FullRows<R, 1, MASK ? 3 : 0, Ar, false>::run(pv, ys, xt, dg, Lt, klo + t, khi + t, ot);
             dg = INF;
           }
         }
@@ -924,7 +971,7 @@ __device__ __forceinline__ void band_steps(
       }
       if (gl == 0) L = INF;  // k = -1 is outside the band
       // First cell of the strip (k = lR): needs only own previous row + L.
-      T v = Ar::cell(x[p], yb[p][(q + 1) % R], Ar::mn(Ar::mn(pv[p][0], pv[p][1]), L));
+      T v = Ar::cell3b(x[p], yb[p][(q + 1) % R], Ar::mn(pv[p][0], pv[p][1]), L);
       if (CHECK) v = act[p] ? v : pv[p][0];
       if (KR == 0 || KR < 0) {
         if (lK[p] == gl && rK[p] == 0) v = INF;  // k == K is this lane's first cell
@@ -950,7 +997,7 @@ __device__ __forceinline__ void band_steps(
 #pragma unroll
         for (int p = 0; p < P; ++p) {
           const T up = (r < R - 1) ? pv[p][r + 1] : U[p];
-          T v = Ar::cell(x[p], yb[p][(r + q + 1) % R], Ar::mn(Ar::mn(pv[p][r], up), left[p]));
+          T v = Ar::cell3b(x[p], yb[p][(r + q + 1) % R], Ar::mn(pv[p][r], up), left[p]);
           if (CHECK && P > 1 && !all) v = act[p] ? v : pv[p][r];
           pv[p][r] = v;
           left[p] = v;
@@ -1118,7 +1165,7 @@ __device__ __forceinline__ void ring_steps(int nst, int& i1, const typename Ar::
       L = L + (T)(loff - off);
     }
     if (gl == 0) L = INF;
-    T v0 = Ar::cell(x, yr[0], Ar::mn(Ar::mn(pv[0], pv[1]), L));
+    T v0 = Ar::cell3b(x, yr[0], Ar::mn(pv[0], pv[1]), L);
     if (CHECK) v0 = act ? v0 : pv[0];
     if (KR == 0 || KR < 0) {
       if (lK == gl && rK == 0) v0 = INF;
@@ -1134,7 +1181,7 @@ __device__ __forceinline__ void ring_steps(int nst, int& i1, const typename Ar::
 #pragma unroll
       for (int r = 1; r < R; ++r) {
         const T up = (r < R - 1) ? pv[r + 1] : U;
-        const T v = Ar::cell(x, yr[r], Ar::mn(Ar::mn(pv[r], up), left));
+        const T v = Ar::cell3b(x, yr[r], Ar::mn(pv[r], up), left);
         pv[r] = v;
         left = v;
       }
@@ -1322,7 +1369,7 @@ __device__ __forceinline__ void unit_steps(int nst, int& i1, const typename Ar::
     for (int h = 0; h < U; ++h) {
       const int s0 = Un::start(h);
       const T left = h == 0 ? L : pv[s0 - 1];
-      T v = Ar::cell(xs[h], yr[s0 - h], Ar::mn(Ar::mn(pv[s0], pv[s0 + 1]), left));
+      T v = Ar::cell3b(xs[h], yr[s0 - h], Ar::mn(pv[s0], pv[s0 + 1]), left);
       if (CHECK) v = act[h] ? v : pv[s0];
       if (KR < 0 || KR == s0) {
         if (lK == gl && rK == s0) v = INF;  // k == K is this unit's first cell
@@ -1347,7 +1394,7 @@ __device__ __forceinline__ void unit_steps(int nst, int& i1, const typename Ar::
           const int r = Un::start(h) + c;
           const bool lastc = c == Un::width(h) - 1;
           const T up = !lastc ? pv[r + 1] : (h == U - 1 ? Ud : v0[h + 1]);
-          T v = Ar::cell(xs[h], yr[r - h], Ar::mn(Ar::mn(pv[r], up), left[h]));
+          T v = Ar::cell3b(xs[h], yr[r - h], Ar::mn(pv[r], up), left[h]);
           if (CHECK) v = act[h] ? v : pv[r];
           pv[r] = v;
           left[h] = v;
