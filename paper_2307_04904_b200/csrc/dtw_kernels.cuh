@@ -43,6 +43,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <type_traits>
 
 #include "dtw_fill.cuh"
 
@@ -104,6 +105,9 @@ __device__ __forceinline__ void chk_row(const FillArgs& A, int64_t row) {
 }
 
 // ---- arithmetic policies ----------------------------------------------------------
+#ifndef DTWG_PD_CELL  // predicated-add cell form in: bit 0 the Full family, bit 1 the band family
+#define DTWG_PD_CELL 3
+#endif
 struct F64 {
   using T = double;
   static constexpr bool kFp32 = false;
@@ -120,16 +124,6 @@ struct F64 {
   // instructions per cell instead of 5 + 4. Written as PTX branches, which ptxas
   // if-converts into the predicated pair (predicated PTX adds come out as two DADDs and
   // four selects).
-  static __device__ __forceinline__ T cell3(T x, T y, T m, T left) {
-#ifndef DTWG_PD_CELL  // bit 0: Full family, bit 1: band family (0 = plain selects)
-#define DTWG_PD_CELL 3
-#endif
-#if DTWG_PD_CELL & 1
-    return cell3pd(x, y, m, left);
-#else
-    return cell(x, y, mn(m, left));
-#endif
-  }
   static __device__ __forceinline__ T cell3b(T x, T y, T m, T left) {  // band family
 #if DTWG_PD_CELL & 2
     return cell3pd(x, y, m, left);
@@ -139,16 +133,19 @@ struct F64 {
   }
   static __device__ __forceinline__ T cell3pd(T x, T y, T m, T left) {
     T v;
+#ifndef DTWG_PD_SALT  // label prefix (ptxas's schedule shifts with the label names)
+#define DTWG_PD_SALT "L"
+#endif
     asm("{\n\t.reg .pred q;\n\t.reg .f64 d;\n\t"
         "sub.rn.f64 d, %1, %2;\n\t"
         "mul.rn.f64 d, d, d;\n\t"
         "setp.lt.f64 q, %4, %3;\n\t"
-        "@q bra L1_%=;\n\t"
+        "@q bra " DTWG_PD_SALT "1_%=;\n\t"
         "add.rn.f64 %0, d, %3;\n\t"
-        "bra L2_%=;\n\t"
-        "L1_%=:\n\t"
+        "bra " DTWG_PD_SALT "2_%=;\n\t"
+        DTWG_PD_SALT "1_%=:\n\t"
         "add.rn.f64 %0, d, %4;\n\t"
-        "L2_%=:\n\t}"
+        DTWG_PD_SALT "2_%=:\n\t}"
         : "=d"(v)
         : "d"(x), "d"(y), "d"(m), "d"(left));
     return v;
@@ -166,7 +163,7 @@ struct F32 {
     const T d = __fsub_rn(x, y);
     return __fadd_rn(__fmul_rn(d, d), best);
   }
-  static __device__ __forceinline__ T cell3(T x, T y, T m, T left) {
+  static __device__ __forceinline__ T cell3pd(T x, T y, T m, T left) {
     return cell(x, y, mn(m, left));
   }
   static __device__ __forceinline__ T cell3b(T x, T y, T m, T left) {
@@ -260,6 +257,10 @@ __device__ __forceinline__ double min_unless(double a, double b, int k, int c) {
   return r;
 }
 
+#ifndef DTWG_PD_LANE  // the one-lane single-strip kernel (c3) keeps plain selects
+#define DTWG_PD_LANE 0
+#endif
+constexpr bool kLanePd = DTWG_PD_LANE;
 template <int R, int NR, int KILL, class Ar, bool PD = true>
 struct FullRows {
   using T = typename Ar::T;
@@ -272,11 +273,26 @@ struct FullRows {
   // Out: out[t] = (r0+t, last column); pv becomes row r0+NR-1.
   // yv: the strip's R y samples -- a register array, or a pointer into shared memory
   // (dtw_lane_kernel), indexed with compile-time offsets either way.
+  // Which rows fold their second minimum into a predicated DADD pair (F64::cell3pd).
+  // Strips with y in registers alternate the two cell forms row by row, which keeps the
+  // fp64 pipe and the ALU pipe both busy (c4: selects only 2478, predicated adds only
+  // 2533, alternating 2575 GCUPS); the shared-memory-y strips (12 warps per SM) do best
+  // with predicated adds on every row (c5: 2255 against 2222 alternating).
+#ifndef DTWG_PD_PATTERN  // which cells of a register-y strip take the predicated adds
+#define DTWG_PD_PATTERN ((r + t) % 2 != 0)
+#endif
+  static __device__ __forceinline__ constexpr bool pd_row(bool ysm, int t, int r) {
+#ifndef DTWG_PD_YSM_ALL
+#define DTWG_PD_YSM_ALL 1
+#endif
+    return !Ar::kFp32 && PD && (DTWG_PD_CELL & 1) && ((ysm && DTWG_PD_YSM_ALL) || DTWG_PD_PATTERN);
+  }
   template <class YV>
   static __device__ __forceinline__ void run(T (&pv)[R], const YV& yv, const T (&x)[NR],
                                              T diag0, const T (&L)[NR], int klo, int khi,
                                              T (&out)[NR]) {
     const T INF = Ar::inf();
+    constexpr bool kYsm = std::is_pointer<YV>::value;
     T d[NR], l[NR];
 #pragma unroll
     for (int t = 0; t < NR; ++t) {
@@ -291,7 +307,7 @@ struct FullRows {
       for (int t = 0; t < NR; ++t) {
         T v;
         if constexpr (KILL == 0) {
-          if constexpr (PD) v = Ar::cell3(x[t], yr, Ar::mn(d[t], up), l[t]);
+          if (pd_row(kYsm, t, r)) v = Ar::cell3pd(x[t], yr, Ar::mn(d[t], up), l[t]);
           else v = Ar::cell(x[t], yr, Ar::mn(Ar::mn(d[t], up), l[t]));
         } else if constexpr (Ar::kFp32) {
           v = Ar::cell(x[t], yr, Ar::mn(Ar::mn(d[t], up), l[t]));
@@ -300,7 +316,7 @@ struct FullRows {
         } else {
           const T m1 = (KILL & 1) ? min_unless(d[t], up, klo, r - t) : Ar::mn(d[t], up);
           if constexpr (KILL & 2) v = Ar::cell(x[t], yr, min_unless(m1, l[t], khi, r - t));
-          else if constexpr (PD) v = Ar::cell3(x[t], yr, m1, l[t]);
+          else if (pd_row(kYsm, t, r)) v = Ar::cell3pd(x[t], yr, m1, l[t]);
           else v = Ar::cell(x[t], yr, Ar::mn(m1, l[t]));
         }
         d[t] = up;  // (t-1, r) is the diagonal of (t, r+1)
@@ -643,10 +659,10 @@ __global__ void __launch_bounds__(kThreads) dtw_lane_kernel(const FillArgs A) {
       }
       T out[TR];
       if (r0 + TR - 1 <= n) {
-        if (need == 0) FullRows<R, TR, 0, Ar, false>::run(pv, ys, x, diag0, L, klo, khi, out);
-        else if (need == 1) FullRows<R, TR, 1, Ar, false>::run(pv, ys, x, diag0, L, klo, khi, out);
-        else if (need == 2) FullRows<R, TR, 2, Ar, false>::run(pv, ys, x, diag0, L, klo, khi, out);
-        else FullRows<R, TR, 3, Ar, false>::run(pv, ys, x, diag0, L, klo, khi, out);
+        if (need == 0) FullRows<R, TR, 0, Ar, kLanePd>::run(pv, ys, x, diag0, L, klo, khi, out);
+        else if (need == 1) FullRows<R, TR, 1, Ar, kLanePd>::run(pv, ys, x, diag0, L, klo, khi, out);
+        else if (need == 2) FullRows<R, TR, 2, Ar, kLanePd>::run(pv, ys, x, diag0, L, klo, khi, out);
+        else FullRows<R, TR, 3, Ar, kLanePd>::run(pv, ys, x, diag0, L, klo, khi, out);
         if (r0 + TR - 1 == n) {
           T rv = pv[0];
 #pragma unroll
@@ -662,7 +678,7 @@ __global__ void __launch_bounds__(kThreads) dtw_lane_kernel(const FillArgs A) {
             const T xt[1] = {x[t]};
             const T Lt[1] = {INF};
             T ot[1];
-            FullRows<R, 1, MASK ? 3 : 0, Ar, false>::run(pv, ys, xt, dg, Lt, klo + t, khi + t, ot);
+            FullRows<R, 1, MASK ? 3 : 0, Ar, kLanePd>::run(pv, ys, xt, dg, Lt, klo + t, khi + t, ot);
             dg = INF;
           }
         }

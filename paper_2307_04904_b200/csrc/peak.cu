@@ -3,7 +3,8 @@
 // The DTW fill is min-plus, so neither the HBM copy nor the bf16 GEMM peak bounds it.
 // Its ceiling is the rate at which an SM issues the cell body itself:
 //   fp64:  DADD(sub) DMUL DSETP+2xFSEL DSETP+2xFSEL DADD   (5 fp64-pipe ops, 9 issues), or
-//          DADD DMUL DSETP+2xFSEL DSETP @q DADD @!q DADD    (6 fp64-pipe ops, 8 issues)
+//          DADD DMUL DSETP+2xFSEL DSETP @q DADD @!q DADD    (6 fp64-pipe ops, 8 issues),
+//          or the two forms on alternate cells
 //   fp32:  FADD FMUL FMNMX3 FADD
 // This kernel runs CH independent chains of exactly that body per thread on every SM
 // with no memory and no wavefront. A chain's three registers rotate through the roles
@@ -20,11 +21,12 @@
 namespace dtwgpu {
 namespace {
 
+// FORM 0: selects; 1: predicated adds; 2: the two forms on alternate chains
 template <int FORM, class T>
-__device__ __forceinline__ T peak_cell(T x, T diag, T up, T left) {
+__device__ __forceinline__ T peak_cell(T x, T diag, T up, T left, int chain) {
   if constexpr (sizeof(T) == 8) {
     const T m = up < diag ? up : diag;
-    if constexpr (FORM == 1) return kern::F64::cell3pd(x, left, m, left);
+    if (FORM == 1 || (FORM == 2 && chain % 2 == 0)) return kern::F64::cell3pd(x, left, m, left);
     else return kern::F64::cell(x, left, left < m ? left : m);
   } else {
     const T d = __fsub_rn(x, left);
@@ -44,9 +46,9 @@ __global__ void cell_peak_kernel(const T* in, T* out, int iters) {
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int i = 0; i < CH; ++i) {
-      c[i] = peak_cell<FORM>(x, c[i], b[i], a[i]);  // newest value replaces the oldest
-      b[i] = peak_cell<FORM>(x, b[i], a[i], c[i]);
-      a[i] = peak_cell<FORM>(x, a[i], c[i], b[i]);
+      c[i] = peak_cell<FORM>(x, c[i], b[i], a[i], i);  // newest value replaces the oldest
+      b[i] = peak_cell<FORM>(x, b[i], a[i], c[i], i);
+      a[i] = peak_cell<FORM>(x, a[i], c[i], b[i], i);
     }
   }
   T s = 0;
@@ -87,6 +89,14 @@ cudaError_t run(cudaStream_t st, int sms, double* cells_per_s) {
   if (v > best) best = v;
   if (e == cudaSuccess && sizeof(T) == 8) {
     e = time_form<2, 1, T>(st, sms, buf, &v);
+    if (v > best) best = v;
+  }
+  if (e == cudaSuccess && sizeof(T) == 8) {
+    e = time_form<2, 2, T>(st, sms, buf, &v);
+    if (v > best) best = v;
+  }
+  if (e == cudaSuccess && sizeof(T) == 8) {
+    e = time_form<4, 2, T>(st, sms, buf, &v);
     if (v > best) best = v;
   }
   if (e == cudaSuccess) {
