@@ -124,12 +124,11 @@ struct F64 {
   // instructions per cell instead of 5 + 4. Written as PTX branches, which ptxas
   // if-converts into the predicated pair (predicated PTX adds come out as two DADDs and
   // four selects).
-  static __device__ __forceinline__ T cell3b(T x, T y, T m, T left) {  // band family
+  static __device__ __forceinline__ T cell3b(T x, T y, T m, T left, bool pd = true) {  // band family
 #if DTWG_PD_CELL & 2
-    return cell3pd(x, y, m, left);
-#else
-    return cell(x, y, mn(m, left));
+    if (pd) return cell3pd(x, y, m, left);
 #endif
+    return cell(x, y, mn(m, left));
   }
   static __device__ __forceinline__ T cell3pd(T x, T y, T m, T left) {
     T v;
@@ -166,7 +165,7 @@ struct F32 {
   static __device__ __forceinline__ T cell3pd(T x, T y, T m, T left) {
     return cell(x, y, mn(m, left));
   }
-  static __device__ __forceinline__ T cell3b(T x, T y, T m, T left) {
+  static __device__ __forceinline__ T cell3b(T x, T y, T m, T left, bool = true) {
     return cell(x, y, mn(m, left));
   }
   static __device__ __forceinline__ const T* base(const FillArgs& A) { return A.samples32; }
@@ -1410,7 +1409,10 @@ __device__ __forceinline__ void unit_steps(int nst, int& i1, const typename Ar::
           const int r = Un::start(h) + c;
           const bool lastc = c == Un::width(h) - 1;
           const T up = !lastc ? pv[r + 1] : (h == U - 1 ? Ud : v0[h + 1]);
-          T v = Ar::cell3b(xs[h], yr[r - h], Ar::mn(pv[r], up), left[h]);
+          #ifndef DTWG_PD_UNIT_PATTERN  // which unit chains take the predicated-add cell form:
+#define DTWG_PD_UNIT_PATTERN (h % 2 == 0)  // even units (c2: 2167 GCUPS; every cell 2136,
+#endif                                     // (c+h) odd 2144, odd columns 2136, h != 0 2152)
+          T v = Ar::cell3b(xs[h], yr[r - h], Ar::mn(pv[r], up), left[h], DTWG_PD_UNIT_PATTERN);
           if (CHECK) v = act[h] ? v : pv[r];
           pv[r] = v;
           left[h] = v;
