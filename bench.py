@@ -230,7 +230,7 @@ def _fill_once(eng, ds, prec, out_ptr):
 
 
 def all_configs_block(eng, dev, a):
-    """One timed fill of each BASELINE config (fp64; c4 also fp32), plus the k-medoids runs
+    """Two timed fills (the faster reported) of each BASELINE config (fp64; c4 also fp32), plus the k-medoids runs
     of c5 (parity against the reference's own kmedoids, timed as its CPU baseline) and c3,
     each over the matrix its fill just left in HBM."""
     import torch
@@ -250,13 +250,19 @@ def all_configs_block(eng, dev, a):
         t0 = time.perf_counter()
         _fill_once(eng, ds, prec, buf.data_ptr())  # plans + warms
         first_s = time.perf_counter() - t0
-        flush.zero_()
-        ms = _fill_once(eng, ds, prec, buf.data_ptr())
+        # two timed fills (L2 flushed before each), the faster one reported: a single fill
+        # of the one-lane classes occasionally runs one item round longer (dynamic items)
+        ms_all = []
+        for _ in range(2):
+            flush.zero_()
+            ms_all.append(_fill_once(eng, ds, prec, buf.data_ptr()))
+        ms = min(ms_all)
         key = f"c{c}" + ("_fp32" if prec else "")
         peak = peak32 if prec else peak64
         out[key] = {"gcups": cells / (ms * 1e-3) / 1e9, "fill_ms": ms, "cells": cells,
                     "pairs": total, "frac_of_peak": cells / (ms * 1e-3) / 1e9 / peak,
-                    "first_call_s": first_s, "plan": eng.last_plan()[:400]}
+                    "fill_ms_all": ms_all, "first_call_s": first_s,
+                    "plan": eng.last_plan()[:400]}
         if c == 5 and prec == 0:
             # cold first call through the public API on a fresh context (planning, H2D,
             # fill, checks, D2H all inside)
