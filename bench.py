@@ -634,6 +634,7 @@ def run_gpu_arm(a, ds):
                        "l2": "flushed (256 MB write) between timed steps",
                        "plan": headline_plan},
             "pairs_per_s": total * a.steps / (max_ms * 1e-3),
+            "step_ms": [round(v, 3) for v in step_ms],  # this rank's timed steps
             "roofline": {"bound": "fp64" if prec == 0 else "fp32",
                          "achieved": achieved, "peak": peak,
                          "unit": "GCUPS (cell updates/s; fp64 cell = 5 fp64-pipe ops, fp32 cell = FADD FMUL FMNMX3 FADD)",
