@@ -105,9 +105,26 @@ __device__ __forceinline__ void chk_row(const FillArgs& A, int64_t row) {
 }
 
 // ---- arithmetic policies ----------------------------------------------------------
-#ifndef DTWG_PD_CELL  // predicated-add cell form in: bit 0 the Full family, bit 1 the band family
+// The fp64 cell has two instruction forms: selects only (F64::cell over two
+// F64::mn, 5 fp64 + 4 ALU instructions) and the second minimum folded into a predicated
+// DADD pair (F64::cell3pd, 6 fp64 + 2 ALU). Which cells take which form is a per-kernel
+// choice, measured on the B200; the switches below exist for those measurements (the
+// pattern macros are expanded where the unrolled row t / column r / unit h are in scope).
+#ifndef DTWG_PD_CELL  // cell3pd allowed in: bit 0 the Full family, bit 1 the band family
 #define DTWG_PD_CELL 3
 #endif
+#ifndef DTWG_PD_PATTERN  // register-y Full strips: checkerboard, odd (row + column) take it
+#define DTWG_PD_PATTERN ((r + t) % 2 != 0)
+#endif
+#ifndef DTWG_PD_YSM_ALL  // shared-memory-y Full strips: every cell (0: the pattern above)
+#define DTWG_PD_YSM_ALL 1
+#endif
+#ifndef DTWG_PD_LANE  // the one-lane single-strip kernel (c3): plain selects
+#define DTWG_PD_LANE 0
+#endif
+#ifndef DTWG_PD_UNIT_PATTERN  // unit-ring band kernel: the even units' chains take it (c2:
+#define DTWG_PD_UNIT_PATTERN (h % 2 == 0)  // 2167 GCUPS; every cell 2136, (c + h) odd 2144,
+#endif                                     // odd columns 2136, h != 0 2152, h == 1 2134)
 struct F64 {
   using T = double;
   static constexpr bool kFp32 = false;
@@ -124,30 +141,28 @@ struct F64 {
   // instructions per cell instead of 5 + 4. Written as PTX branches, which ptxas
   // if-converts into the predicated pair (predicated PTX adds come out as two DADDs and
   // four selects).
-  static __device__ __forceinline__ T cell3b(T x, T y, T m, T left, bool pd = true) {  // band family
-#if DTWG_PD_CELL & 2
-    if (pd) return cell3pd(x, y, m, left);
-#endif
-    return cell(x, y, mn(m, left));
-  }
   static __device__ __forceinline__ T cell3pd(T x, T y, T m, T left) {
     T v;
-#ifndef DTWG_PD_SALT  // label prefix (ptxas's schedule shifts with the label names)
-#define DTWG_PD_SALT "L"
-#endif
     asm("{\n\t.reg .pred q;\n\t.reg .f64 d;\n\t"
         "sub.rn.f64 d, %1, %2;\n\t"
         "mul.rn.f64 d, d, d;\n\t"
         "setp.lt.f64 q, %4, %3;\n\t"
-        "@q bra " DTWG_PD_SALT "1_%=;\n\t"
+        "@q bra L1_%=;\n\t"
         "add.rn.f64 %0, d, %3;\n\t"
-        "bra " DTWG_PD_SALT "2_%=;\n\t"
-        DTWG_PD_SALT "1_%=:\n\t"
+        "bra L2_%=;\n\t"
+        "L1_%=:\n\t"
         "add.rn.f64 %0, d, %4;\n\t"
-        DTWG_PD_SALT "2_%=:\n\t}"
+        "L2_%=:\n\t}"
         : "=d"(v)
         : "d"(x), "d"(y), "d"(m), "d"(left));
     return v;
+  }
+  // Band family: cell3pd on every cell unless the call site passes its own pattern.
+  static __device__ __forceinline__ T cell3b(T x, T y, T m, T left, bool pd = true) {
+#if DTWG_PD_CELL & 2
+    if (pd) return cell3pd(x, y, m, left);
+#endif
+    return cell(x, y, mn(m, left));
   }
   static __device__ __forceinline__ const T* base(const FillArgs& A) { return A.samples; }
   static __device__ __forceinline__ const T* bbase(const FillArgs& A) { return A.bsamples; }
@@ -256,9 +271,6 @@ __device__ __forceinline__ double min_unless(double a, double b, int k, int c) {
   return r;
 }
 
-#ifndef DTWG_PD_LANE  // the one-lane single-strip kernel (c3) keeps plain selects
-#define DTWG_PD_LANE 0
-#endif
 constexpr bool kLanePd = DTWG_PD_LANE;
 template <int R, int NR, int KILL, class Ar, bool PD = true>
 struct FullRows {
@@ -272,18 +284,14 @@ struct FullRows {
   // Out: out[t] = (r0+t, last column); pv becomes row r0+NR-1.
   // yv: the strip's R y samples -- a register array, or a pointer into shared memory
   // (dtw_lane_kernel), indexed with compile-time offsets either way.
-  // Which rows fold their second minimum into a predicated DADD pair (F64::cell3pd).
-  // Strips with y in registers alternate the two cell forms row by row, which keeps the
-  // fp64 pipe and the ALU pipe both busy (c4: selects only 2478, predicated adds only
-  // 2533, alternating 2575 GCUPS); the shared-memory-y strips (12 warps per SM) do best
-  // with predicated adds on every row (c5: 2255 against 2222 alternating).
-#ifndef DTWG_PD_PATTERN  // which cells of a register-y strip take the predicated adds
-#define DTWG_PD_PATTERN ((r + t) % 2 != 0)
-#endif
+  // Which cells fold their second minimum into a predicated DADD pair (F64::cell3pd).
+  // Strips with y in registers lay the two cell forms out as a checkerboard -- each
+  // anti-diagonal of the block is one form, consecutive anti-diagonals alternate -- which
+  // keeps the fp64 pipe and the ALU pipe both busy (c4: selects only 2478, predicated adds
+  // only 2533, checkerboard 2575 GCUPS; alternate rows 2538, alternate columns 2529); the
+  // shared-memory-y strips (12 warps per SM) do best with predicated adds on every cell
+  // (c5: 2255 against 2241 checkerboard).
   static __device__ __forceinline__ constexpr bool pd_row(bool ysm, int t, int r) {
-#ifndef DTWG_PD_YSM_ALL
-#define DTWG_PD_YSM_ALL 1
-#endif
     return !Ar::kFp32 && PD && (DTWG_PD_CELL & 1) && ((ysm && DTWG_PD_YSM_ALL) || DTWG_PD_PATTERN);
   }
   template <class YV>
@@ -1409,9 +1417,6 @@ __device__ __forceinline__ void unit_steps(int nst, int& i1, const typename Ar::
           const int r = Un::start(h) + c;
           const bool lastc = c == Un::width(h) - 1;
           const T up = !lastc ? pv[r + 1] : (h == U - 1 ? Ud : v0[h + 1]);
-          #ifndef DTWG_PD_UNIT_PATTERN  // which unit chains take the predicated-add cell form:
-#define DTWG_PD_UNIT_PATTERN (h % 2 == 0)  // even units (c2: 2167 GCUPS; every cell 2136,
-#endif                                     // (c+h) odd 2144, odd columns 2136, h != 0 2152)
           T v = Ar::cell3b(xs[h], yr[r - h], Ar::mn(pv[r], up), left[h], DTWG_PD_UNIT_PATTERN);
           if (CHECK) v = act[h] ? v : pv[r];
           pv[r] = v;

@@ -1,4 +1,8 @@
 // cell_microbench.cu -- measures the sm_100a ceiling of the DTW cell update itself.
+// NOTE (round 2, session 4): the throughput kernels here feed one chain's previous value
+// in as both `up` and `left`, which lets the compiler drop part of the compares/selects
+// (their ~3045-3080 GCUPS overstates the fp64 cell; the chain latency figures stand).
+// tools/dispatch_microbench.cu and csrc/peak.cu are the corrected measurements.
 //
 // Each thread runs CH independent chains of the exact fp64 cell body used by the fill
 //   v = (x - y)^2 + min(min(diag, up), left)     (DADD, DMUL, 2x DSETP+2 FSEL, DADD)

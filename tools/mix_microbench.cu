@@ -1,4 +1,9 @@
 // mix_microbench.cu -- which pipe should do the two minima of the fp64 DTW cell?
+// NOTE (round 2, session 4): this harness feeds one chain's previous value in as both
+// `up` and `left`, so the compiler drops part of the compares/selects, and its V4/V5
+// "predicated IMAD" come out as IMAD + SEL; its absolute cycles per cell are too low.
+// tools/dispatch_microbench.cu is the corrected measurement.
+//
 //
 // All DTW cell values are +0, positive or +inf doubles (squares and sums of them; no -0,
 // no NaN), and such doubles order exactly like their bit patterns as unsigned 64-bit
