@@ -129,7 +129,7 @@ int run_fill(dtwg_ctx* ctx, int64_t hw, int auto_widen, int precision, int64_t s
                               ctx->force_R,
                               env_or("DTWGPU_UNDERFILL_REPLAN", 1) * 2 + env_or("DTWGPU_PLAN_TABLE", 1) +
                                   4 * env_or("DTWGPU_TAIL_SPLIT", 1) +
-                                  8 * env_or("DTWGPU_TAIL_SERIAL", 1)};
+                                  8 * (env_or("DTWGPU_TAIL_SERIAL", -1) + 1)};
   if (!(ctx->plan_valid && ctx->plan_key == key)) {
     const auto t0 = std::chrono::steady_clock::now();
     ctx->plan_cache = make_plan(ctx, hw, auto_widen, fp32, sb, se);

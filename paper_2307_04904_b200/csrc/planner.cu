@@ -372,10 +372,15 @@ void split_tail_round(dtwg_ctx* ctx, std::vector<PlanClass>& plan, const Shape& 
     }
   }
   if (!found) return;
-  // Serial after the full rounds (same stream): their lanes all finish together, while a
-  // concurrent launch let tail CTAs take SM slots first on some runs and pushed full-round
-  // CTAs into a second wave (c4 / 8 GPUs: 217 -> 244 ms on one shard of eight).
-  t.after_prev = env_or("DTWGPU_TAIL_SERIAL", 1) != 0;
+  // With few full rounds the tail runs serially after them (same stream): their lanes all
+  // finish together, while a concurrent launch let tail CTAs take SM slots first on some
+  // runs and pushed full-round CTAs into a second wave (c4 / 8 GPUs: 217 -> 244 ms on one
+  // shard of eight). With many rounds that delay is small against the run and the tail
+  // fills the SMs whose lanes finish early: the whole c4 (13 rounds) averages 1571-1577 ms
+  // concurrent against 1579-1587 serial over 15 fills each, slow fills included.
+  // DTWGPU_TAIL_SERIAL = 0 / 1 forces either.
+  const int64_t serial = env_or("DTWGPU_TAIL_SERIAL", -1);
+  t.after_prev = serial < 0 ? full_rounds < 4 : serial != 0;
   t.max_n = pc.max_n;
   t.max_m = pc.max_m;
   set_single_strip(t);
