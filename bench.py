@@ -640,6 +640,12 @@ def run_gpu_arm(a, ds):
                          "unit": "GCUPS (cell updates/s; fp64 cell = 5 fp64-pipe ops, fp32 cell = FADD FMUL FMNMX3 FADD)",
                          "frac": (achieved / peak) if achieved else None,
                          "traffic": traffic,
+                         # DRAM rate that traffic means at this step time, against the
+                         # measured HBM peak: the fill is not HBM-bound
+                         "traffic_gbs": (traffic / (kernel_ms * 1e-3) / 1e9
+                                         if traffic and kernel_ms else None),
+                         "traffic_frac_of_hbm": (traffic / (kernel_ms * 1e-3) / 1e9 / _hbm_peak()[0]
+                                                 if traffic and kernel_ms else None),
                          "peak_source": peak_src,
                          "live_cell_ceiling": live_peak,
                          "frac_of_live_ceiling": (achieved / live_peak) if achieved else None,
